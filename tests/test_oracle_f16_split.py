@@ -1,0 +1,113 @@
+"""Pins for the oracle's FP32->FP16 RN conversion and the SHGEMM split
+(Eqs 14-15; split inequalities P:576; 0.25-bit expected loss P:572)."""
+import ctypes
+import os
+import subprocess
+
+import numpy as np
+import pytest
+
+HERE = os.path.dirname(__file__)
+GOLDEN = os.path.join(HERE, "golden")
+
+
+@pytest.fixture(scope="module")
+def f16c(orc):
+    src = os.path.join(HERE, "helpers", "f16c_check.c")
+    out = os.path.join(HERE, "helpers", "libf16c_check.so")
+    libdir = os.path.dirname(orc.build())
+    if not os.path.exists(out) or os.path.getmtime(out) < os.path.getmtime(src):
+        subprocess.run(["gcc", "-O2", "-mf16c", "-fopenmp", "-fPIC", "-shared", "-o", out, src,
+                        "-L" + libdir, "-loracle", "-Wl,-rpath," + libdir], check=True)
+    orc.lib()  # make sure liboracle is loaded globally first
+    ctypes.CDLL(orc.build(), mode=ctypes.RTLD_GLOBAL)
+    L = ctypes.CDLL(out)
+    L.f16c_mismatches.argtypes = [ctypes.c_uint64, ctypes.c_uint64, ctypes.POINTER(ctypes.c_uint32)]
+    L.f16c_mismatches.restype = ctypes.c_uint64
+    return L
+
+
+def test_f32_to_f16_exhaustive_vs_f16c(f16c):
+    """All 2^32 FP32 patterns: software RN == x86 F16C vcvtps2ph (NaN classes equal)."""
+    first = ctypes.c_uint32(0)
+    bad = f16c.f16c_mismatches(0, 1 << 32, ctypes.byref(first))
+    assert bad == 0, hex(first.value)
+
+
+def test_f32_to_f16_vs_numpy_sample(orc):
+    rng = np.random.default_rng(0)
+    bits = rng.integers(0, 1 << 32, size=1 << 20, dtype=np.uint64).astype(np.uint32)
+    x = bits.view(np.float32)
+    got = orc.f32_to_f16_batch(x)
+    with np.errstate(all="ignore"):
+        ref = x.astype(np.float16).view(np.uint16)
+    nan = np.isnan(x)
+    assert np.array_equal(got[~nan], ref[~nan])
+    assert np.all((got[nan] & 0x7C00) == 0x7C00) and np.all((got[nan] & 0x3FF) != 0)
+
+
+def test_f16_to_f32_all_halfs(orc):
+    h = np.arange(1 << 16, dtype=np.uint16)
+    ref = h.view(np.float16).astype(np.float32)
+    got = np.array([orc.f16_bits_to_f32(int(v)) for v in h], dtype=np.float32)
+    ok = np.isnan(ref)
+    assert np.array_equal(got[~ok].view(np.uint32), ref[~ok].view(np.uint32))
+    assert np.all(np.isnan(got[ok]))
+
+
+def test_split_golden(orc):
+    """Worked examples, tests/golden/split_examples.txt (SPEC.md:218 and the definition)."""
+    n = 0
+    for line in open(os.path.join(GOLDEN, "split_examples.txt")):
+        if line.startswith("#") or not line.strip():
+            continue
+        a_bits, hi_bits, lo_bits = (int(t, 16) for t in line.split()[:3])
+        a = np.array([a_bits], dtype=np.uint32).view(np.float32)
+        hi, lo = orc.split(a)
+        assert (int(hi[0]), int(lo[0])) == (hi_bits, lo_bits), line
+        n += 1
+    assert n == 9
+
+
+def test_split_exact_for_fp16_values(orc):
+    """A exactly FP16-representable -> hi = A, lo = 0 (north_star)."""
+    rng = np.random.default_rng(1)
+    h = rng.integers(0, 1 << 16, size=1 << 18, dtype=np.uint32).astype(np.uint16)
+    h = h[(h & 0x7C00) != 0x7C00]  # finite halves only
+    a = h.view(np.float16).astype(np.float32)
+    hi, lo = orc.split(a)
+    same = (hi == h) | ((a == 0) & ((hi & 0x7FFF) == 0))
+    assert np.all(same)
+    assert np.all((lo & 0x7FFF) == 0)
+
+
+def test_split_inequalities_and_quarter_bit_loss(orc):
+    """|hi| <= (1+u)|a|, |lo 2^-11| <= u|a|, |A_delta| <= u^2 |a| (u = 2^-11);
+    P:572: the lost mantissa is ~0.25 bit: reconstruction exact in 75%, 1 ulp off in 25%."""
+    rng = np.random.default_rng(2)
+    N = 1 << 20
+    mag = np.exp2(rng.uniform(-12, 15.99, N))
+    a = (mag * rng.choice([-1.0, 1.0], N)).astype(np.float32)
+    a = a[np.abs(a) < 65504]
+    hi, lo = orc.split(a)
+    hf = hi.view(np.float16).astype(np.float64)
+    lf = lo.view(np.float16).astype(np.float64) * 2.0 ** -11
+    a64 = a.astype(np.float64)
+    u = 2.0 ** -11
+    assert np.all(np.abs(hf) <= (1 + u) * np.abs(a64))
+    assert np.all(np.abs(lf) <= u * np.abs(a64))
+    delta = a64 - (hf + lf)
+    assert np.all(np.abs(delta) <= u * u * np.abs(a64))
+    ulp = np.spacing(np.abs(a)).astype(np.float64)
+    assert np.all(np.abs(delta) <= ulp)
+    frac = np.mean(delta != 0)
+    assert 0.22 < frac < 0.28, frac
+
+
+def test_split_overflow_and_nan(orc):
+    """|a| >= 65520 -> hi = +-inf (FP16 range); NaN propagates."""
+    a = np.array([65520.0, -1e6, np.inf, np.nan, 65519.0], dtype=np.float32)
+    hi, lo = orc.split(a)
+    assert hi[0] == 0x7C00 and hi[1] == 0xFC00 and hi[2] == 0x7C00
+    assert (hi[3] & 0x7C00) == 0x7C00 and (hi[3] & 0x3FF)
+    assert hi[4] == 0x7BFF
