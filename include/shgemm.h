@@ -1,0 +1,169 @@
+/*
+ * shgemm.h — C ABI of the B200 (sm_100a) SHGEMM random-projection library (libshgemm.so).
+ *
+ * Paper: H. Ootomo, R. Yokota, "Mixed-precision random projection for RandNLA on Tensor Cores"
+ * (arXiv 2304.04612), /root/reference/PAPER.md, cited as P:<line>.
+ *
+ * The library computes the paper's one data-parallel hot path, the random projection
+ * Y = A . Omega (Eq 1; Alg 1 line 1; Alg 2 line 2), with A in FP32 and
+ * Omega a random matrix stored in FP16, by SHGEMM (Eqs 14-17): every FP32
+ * element of A is split in-kernel into an FP16 hi and a 2^11-scaled FP16 lo part, both products
+ * run on the tensor cores, and accumulation is promoted to round-to-nearest FP32 adds
+ * (P:36-37).
+ *
+ * Conventions for every call
+ *  - Pointers named A/Omega/Y/W/workspace/hi/lo are DEVICE pointers (CUDA global memory) unless
+ *    the name says host. The caller owns every buffer; the library keeps no allocation past a call
+ *    (project() without a workspace uses stream-ordered cudaMallocAsync/cudaFreeAsync).
+ *  - All work is enqueued asynchronously on `stream` (a cudaStream_t; NULL = legacy default).
+ *    Argument errors are returned synchronously and nothing is enqueued; faults inside kernels
+ *    surface at the caller's next synchronization (CUDA convention).
+ *  - Layouts: A is row-major m x k with leading dimension lda >= k (elements);
+ *    Omega is k x n COLUMN-major (Omega[i][j] at Omega[j*ldo + i], ldo >= k), i.e. K-contiguous,
+ *    FP16 stored as uint16_t bit patterns; Y is row-major m x n, ldc >= n.
+ *  - Tensor-core fast path preconditions: A, Omega, Y 16-byte aligned, lda % 4 == 0,
+ *    ldo % 8 == 0 (TMA row pitch multiple of 16 B). Otherwise a CUDA-core fallback with the same
+ *    numerics contract runs (slower).
+ *  - Numerical exceptions are not errors: |a| >= 65520 overflows the FP16 hi part to +-inf and
+ *    the affected Y rows become non-finite — the paper's expected SHGEMM-FP16 failure on
+ *    A_Cauchy. NaN propagates. The _ex variants can raise a device flag.
+ *  - Determinism: identical inputs, shapes and tunables give bitwise-identical Y (fixed-order
+ *    split-K reduction, no atomics on data).
+ *  - Requires a compute-capability 10.0 device (B200); otherwise SHG_ERR_UNSUPPORTED_DEVICE.
+ */
+#ifndef SHGEMM_H_
+#define SHGEMM_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct CUstream_st *shg_stream_t; /* == cudaStream_t */
+
+typedef enum {
+    SHG_OK = 0,
+    SHG_ERR_INVALID_VALUE = 1,      /* bad dimension, leading dimension, mode or NULL pointer */
+    SHG_ERR_UNSUPPORTED_DEVICE = 2, /* current device is not sm_100 */
+    SHG_ERR_CUDA = 3,               /* a CUDA runtime/driver call failed; see shg_last_error() */
+    SHG_ERR_WORKSPACE = 4           /* caller workspace smaller than required */
+} shg_status_t;
+
+/* Omega distributions (OMEGA_SPEC.md §3-4). Gaussian N(0,1) rounded RN to FP16;
+ * sparse sign matrices of Eq 7 without the sqrt(s) factor. */
+typedef enum {
+    SHG_DIST_GAUSSIAN = 0,
+    SHG_DIST_RADEMACHER = 1,  /* s = 1 */
+    SHG_DIST_SPARSE3 = 2,     /* s = 3 (Achlioptas) */
+    SHG_DIST_VERYSPARSE = 3   /* s = sqrt(k) (Li et al.), k = rows of the full Omega */
+} shg_dist_t;
+
+/* Tunables for shgemm_ex. Zero-initialise for the heuristics. */
+typedef struct {
+    int32_t bn;          /* N tile (multiple of 16, <= 256); 0 = heuristic */
+    int32_t split_k;     /* number of k splits; 0 = heuristic, 1 = none */
+    int32_t max_ctas;    /* persistent grid size cap; 0 = number of SMs */
+    int32_t force_simt;  /* 1 = force the CUDA-core fallback (tests) */
+} shg_tune_t;
+
+/* Plan the library would use for an (m, n, k) shgemm on the current device. */
+typedef struct {
+    int32_t path;        /* 0 = tcgen05 mainloop, 1 = SIMT fallback, 2 = trivial (no GEMM) */
+    int32_t bn, n_tiles, m_tiles, split_k, grid, stages_a, stages_b, smem_bytes;
+    int32_t kernels;     /* kernel launches one call makes */
+    int64_t workspace_bytes;
+} shg_plan_t;
+
+/* ---------------------------------------------------------------------------------------------
+ * shgemm — Y[m x n] = A[m x k] . Omega[k x n] by SHGEMM-FP16 (Eqs 14-17).
+ *   m, n, k  >= 0. m == 0 or n == 0: no-op. k == 0: Y = 0.
+ *   A        device, row-major, lda >= max(k,1).   Omega device, column-major, ldo >= max(k,1).
+ *   Y        device, row-major, ldc >= max(n,1); overwritten (beta = 0).
+ * Split-K scratch, when the heuristic uses it, is stream-ordered cudaMallocAsync memory.
+ * ------------------------------------------------------------------------------------------- */
+shg_status_t shgemm(int64_t m, int64_t n, int64_t k, const float *A, int64_t lda, const uint16_t *Omega,
+                    int64_t ldo, float *Y, int64_t ldc, shg_stream_t stream);
+
+/* shgemm with tunables, caller workspace (>= shg_workspace_size bytes, or NULL), and an optional
+ * device int flag set to 1 if any output is non-finite (never cleared by the library). */
+shg_status_t shgemm_ex(int64_t m, int64_t n, int64_t k, const float *A, int64_t lda, const uint16_t *Omega,
+                       int64_t ldo, float *Y, int64_t ldc, const shg_tune_t *tune, void *workspace,
+                       size_t workspace_bytes, int *nonfinite_flag, shg_stream_t stream);
+
+/* Bytes of split-K workspace shgemm_ex needs for (m, n, k) with `tune` (NULL = heuristics). */
+size_t shg_workspace_size(int64_t m, int64_t n, int64_t k, const shg_tune_t *tune);
+
+/* Fill *plan for (m, n, k) with `tune` (NULL = heuristics), without launching anything. */
+shg_status_t shg_plan(int64_t m, int64_t n, int64_t k, const shg_tune_t *tune, shg_plan_t *plan);
+
+/* ---------------------------------------------------------------------------------------------
+ * gen_omega_f16 — Omega[i][j] = OMEGA_SPEC(seed, stream_id = 0, dist, i, j) for 0 <= i < k,
+ * 0 <= j < n, written column-major with ldo >= k (FP16 bits). Bit-identical to the CPU oracle.
+ * ------------------------------------------------------------------------------------------- */
+shg_status_t gen_omega_f16(int64_t k, int64_t n, uint64_t seed, int dist, uint16_t *Omega, int64_t ldo,
+                           shg_stream_t stream);
+
+/* As gen_omega_f16 with an explicit Philox stream id, a row offset (local row r holds spec row
+ * row0 + r; used for K-sharding) and the full-Omega row count k_total for SHG_DIST_VERYSPARSE. */
+shg_status_t gen_omega_f16_ex(int64_t k, int64_t n, uint64_t seed, int dist, uint32_t stream_id,
+                              int64_t row0, int64_t k_total, uint16_t *Omega, int64_t ldo,
+                              shg_stream_t stream);
+
+/* ---------------------------------------------------------------------------------------------
+ * project — W[I_mode x n] = A'_(mode) . Omega_(mode) (Alg 2 line 2).
+ *   A        device, C-order tensor with ndim dims (1 <= ndim <= 8), dims[i] >= 1.
+ *   mode     0 <= mode < ndim. The unfolding's column index is the C-order linear index over the
+ *            remaining modes in ascending order (== torch.movedim(A, mode, 0).reshape(I_mode, -1)).
+ *   Omega_(mode) = gen_omega_f16_ex(K = prod_{j != mode} dims[j], n, seed, dist,
+ *            stream_id = mode, row0 = 0, k_total = K).
+ *   W        device, row-major I_mode x n, ldw >= n.
+ *   workspace  device scratch of >= shg_project_workspace_size(...) bytes, or NULL (then the
+ *            library allocates stream-ordered memory and frees it on `stream`).
+ * ------------------------------------------------------------------------------------------- */
+shg_status_t project(const float *A, int ndim, const int64_t *dims, int mode, int64_t n, uint64_t seed,
+                     int dist, float *W, int64_t ldw, void *workspace, size_t workspace_bytes,
+                     shg_stream_t stream);
+
+size_t shg_project_workspace_size(int ndim, const int64_t *dims, int mode, int64_t n);
+
+/* ---------------------------------------------------------------------------------------------
+ * Test / bench support (not part of the method).
+ * ------------------------------------------------------------------------------------------- */
+/* Elementwise split of Eqs 14-15 with the SAME device function the mainloop uses:
+ * hi[t], lo[t] = FP16 bits of toLow(a[t]) and toLow((a[t] - hi) * 2^11). Device pointers. */
+shg_status_t shg_debug_split(const float *a, int64_t count, uint16_t *hi, uint16_t *lo, shg_stream_t stream);
+
+/* Synthetic FP32 input of OMEGA_SPEC §6 (kind 0 Gaussian, 1 uniform [0,1)):
+ * A[i*lda + l] = synth(seed, stream_id, global row row0 + i, column l), 0 <= i < m, 0 <= l < k. */
+shg_status_t shg_synth_f32(int kind, uint64_t seed, uint32_t stream_id, int64_t m, int64_t k, int64_t row0,
+                           float *A, int64_t lda, shg_stream_t stream);
+
+/* Number of kernels this library has launched in this process (monotonic). */
+uint64_t shg_launch_count(void);
+
+/* Message of the last SHG_ERR_CUDA in this thread ("" if none). */
+const char *shg_last_error(void);
+
+/* 1 if the current device can run the tcgen05 path (cc 10.0), else 0. */
+int shg_device_supported(void);
+
+/* Library version, e.g. "shgemm-b200 0.1.0 sm_100a". */
+const char *shg_version(void);
+
+/* Tensor-core semantics probe: ONE CTA runs tcgen05.mma.cta_group::1.kind::f16
+ * with M = 128, N = n (16 <= n <= 256, n % 16 == 0), K = 64 (four K=16 instructions) on
+ *   A  device, 128 x 64 FP16 bits, row-major (K-contiguous);  B  device, n x 64 FP16 bits, row-major;
+ *   D_init device 128 x n FP32 row-major preloaded into TMEM with tcgen05.st, or NULL (D starts
+ *          undefined and the first instruction runs with enable-input-d = 0);
+ *   mode 0: D = D_init + sum_{j<nsteps} A_j B_j^T                 (j = 16-wide K step)
+ *   mode 1: D = D_init * 2^-11 + sum_{j<nsteps} A_j B_j^T   (first instruction has scale-input-d = 11)
+ *   nsteps 1..4 instructions; D_out device 128 x n FP32 row-major. */
+shg_status_t shg_probe_umma(const uint16_t *A, const uint16_t *B, int n, const float *D_init, int mode,
+                            int nsteps, float *D_out, shg_stream_t stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SHGEMM_H_ */

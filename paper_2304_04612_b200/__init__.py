@@ -1,0 +1,225 @@
+"""SHGEMM random projection for B200 (sm_100a) — Python binding of libshgemm.so.
+
+Paper: Ootomo & Yokota, "Mixed-precision random projection for RandNLA on Tensor Cores"
+(arXiv 2304.04612). The library computes Y = A . Omega (Eq 1) with A in FP32
+and Omega in FP16 by SHGEMM (Eqs 14-17) in hand-written tcgen05 CUDA.
+
+This module only marshals arguments (torch tensors -> device pointers, the current CUDA stream)
+into the C ABI of include/shgemm.h. Every step of the path runs in the library's kernels; there
+is no CPU or PyTorch fallback — if libshgemm.so is missing or the device is not a B200 the calls
+raise.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+
+import torch
+
+__all__ = ["shgemm", "gen_omega", "project", "split", "synth", "plan", "launch_count", "lib",
+           "probe_umma", "project_workspace_size", "SHGError", "DISTS"]
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libshgemm.so")
+DISTS = {"gaussian": 0, "rademacher": 1, "sparse3": 2, "verysparse": 3}
+_STATUS = {0: "SHG_OK", 1: "SHG_ERR_INVALID_VALUE", 2: "SHG_ERR_UNSUPPORTED_DEVICE", 3: "SHG_ERR_CUDA",
+           4: "SHG_ERR_WORKSPACE"}
+_lock = threading.Lock()
+_lib = None
+
+
+class SHGError(RuntimeError):
+    pass
+
+
+class Tune(ctypes.Structure):
+    _fields_ = [("bn", ctypes.c_int32), ("split_k", ctypes.c_int32), ("max_ctas", ctypes.c_int32),
+                ("force_simt", ctypes.c_int32)]
+
+
+class Plan(ctypes.Structure):
+    _fields_ = [("path", ctypes.c_int32), ("bn", ctypes.c_int32), ("n_tiles", ctypes.c_int32),
+                ("m_tiles", ctypes.c_int32), ("split_k", ctypes.c_int32), ("grid", ctypes.c_int32),
+                ("stages_a", ctypes.c_int32), ("stages_b", ctypes.c_int32), ("smem_bytes", ctypes.c_int32),
+                ("kernels", ctypes.c_int32), ("workspace_bytes", ctypes.c_int64)]
+
+
+def lib():
+    """Load libshgemm.so (built in-tree by __graft_entry__.build()); raise if absent."""
+    global _lib
+    with _lock:
+        if _lib is None:
+            if not os.path.exists(LIB_PATH):
+                raise SHGError(f"{LIB_PATH} is not built (run `python __graft_entry__.py` / build())")
+            L = ctypes.CDLL(LIB_PATH)
+            i32, i64, u32, u64, vp, sz = (ctypes.c_int, ctypes.c_int64, ctypes.c_uint32, ctypes.c_uint64,
+                                          ctypes.c_void_p, ctypes.c_size_t)
+            L.shgemm.argtypes = [i64, i64, i64, vp, i64, vp, i64, vp, i64, vp]
+            L.shgemm_ex.argtypes = [i64, i64, i64, vp, i64, vp, i64, vp, i64, ctypes.POINTER(Tune), vp, sz, vp, vp]
+            L.shg_workspace_size.argtypes = [i64, i64, i64, ctypes.POINTER(Tune)]
+            L.shg_workspace_size.restype = sz
+            L.shg_plan.argtypes = [i64, i64, i64, ctypes.POINTER(Tune), ctypes.POINTER(Plan)]
+            L.gen_omega_f16.argtypes = [i64, i64, u64, i32, vp, i64, vp]
+            L.gen_omega_f16_ex.argtypes = [i64, i64, u64, i32, u32, i64, i64, vp, i64, vp]
+            L.project.argtypes = [vp, i32, vp, i32, i64, u64, i32, vp, i64, vp, sz, vp]
+            L.shg_project_workspace_size.argtypes = [i32, vp, i32, i64]
+            L.shg_project_workspace_size.restype = sz
+            L.shg_debug_split.argtypes = [vp, i64, vp, vp, vp]
+            L.shg_synth_f32.argtypes = [i32, u64, u32, i64, i64, i64, vp, i64, vp]
+            L.shg_launch_count.restype = u64
+            L.shg_last_error.restype = ctypes.c_char_p
+            L.shg_device_supported.restype = i32
+            L.shg_version.restype = ctypes.c_char_p
+            L.shg_probe_umma.argtypes = [vp, vp, i32, vp, i32, i32, vp, vp]
+            for name in ("shgemm", "shgemm_ex", "shg_plan", "gen_omega_f16", "gen_omega_f16_ex", "project",
+                         "shg_debug_split", "shg_synth_f32", "shg_probe_umma"):
+                getattr(L, name).restype = i32
+            _lib = L
+    return _lib
+
+
+def _check(status: int, what: str):
+    if status != 0:
+        msg = lib().shg_last_error().decode()
+        raise SHGError(f"{what}: {_STATUS.get(status, status)} {msg}")
+
+
+def _stream(stream=None):
+    s = torch.cuda.current_stream() if stream is None else stream
+    return ctypes.c_void_p(s.cuda_stream)
+
+
+def _p(t: torch.Tensor | None):
+    return ctypes.c_void_p(0 if t is None else t.data_ptr())
+
+
+def _dist(d) -> int:
+    return DISTS[d] if isinstance(d, str) else int(d)
+
+
+def launch_count() -> int:
+    """Kernels this process has launched through the library (monotonic)."""
+    return int(lib().shg_launch_count())
+
+
+def device_supported() -> bool:
+    return bool(lib().shg_device_supported())
+
+
+def version() -> str:
+    return lib().shg_version().decode()
+
+
+# ----------------------------------------------------------------------------------------- Omega
+def gen_omega(k: int, n: int, seed: int = 0, dist="gaussian", stream_id: int = 0, row0: int = 0,
+              k_total: int | None = None, device=None, stream=None) -> torch.Tensor:
+    """Omega (k x n, FP16) of OMEGA_SPEC.md, returned as a column-major view (strides (1, ldo))."""
+    device = torch.device("cuda") if device is None else torch.device(device)
+    ldo = (k + 7) // 8 * 8 if k > 0 else 8
+    buf = torch.empty((n, ldo), dtype=torch.float16, device=device)
+    _check(lib().gen_omega_f16_ex(k, n, seed & (2 ** 64 - 1), _dist(dist), stream_id, row0,
+                                  k if k_total is None else k_total, _p(buf), ldo, _stream(stream)),
+           "gen_omega_f16_ex")
+    return buf[:, :k].t()
+
+
+# ----------------------------------------------------------------------------------------- SHGEMM
+def _tune(tune):
+    if tune is None:
+        return None
+    t = Tune()
+    for key, val in dict(tune).items():
+        setattr(t, key, int(val))
+    return ctypes.byref(t)
+
+
+def shgemm(A: torch.Tensor, Omega: torch.Tensor, out: torch.Tensor | None = None, tune=None,
+           nonfinite: torch.Tensor | None = None, workspace: torch.Tensor | None = None,
+           stream=None) -> torch.Tensor:
+    """Y = A . Omega. A: (m, k) float32, row-major (stride(1) == 1). Omega: (k, n) float16,
+    column-major (stride(0) == 1), e.g. from gen_omega(). Returns Y (m, n) float32 row-major."""
+    if A.dtype != torch.float32 or Omega.dtype != torch.float16:
+        raise TypeError("A must be float32 and Omega float16")
+    m, k = A.shape
+    k2, n = Omega.shape
+    if k2 != k:
+        raise ValueError(f"shape mismatch {tuple(A.shape)} x {tuple(Omega.shape)}")
+    if m and k and A.stride(1) != 1:
+        raise ValueError("A must be row-major (stride(1) == 1)")
+    if k and n and Omega.stride(0) != 1:
+        raise ValueError("Omega must be column-major (stride(0) == 1)")
+    if out is None:
+        out = torch.empty((m, n), dtype=torch.float32, device=A.device)
+    elif out.dtype != torch.float32 or tuple(out.shape) != (m, n) or (m and n and out.stride(1) != 1):
+        raise ValueError("out must be (m, n) float32 row-major")
+    lda = A.stride(0) if m > 1 else max(k, 1)
+    ldo = Omega.stride(1) if n > 1 else max(k, 1)
+    ldc = out.stride(0) if m > 1 else max(n, 1)
+    ws_bytes = 0 if workspace is None else workspace.numel() * workspace.element_size()
+    _check(lib().shgemm_ex(m, n, k, _p(A), lda, _p(Omega), ldo, _p(out), ldc, _tune(tune), _p(workspace),
+                           ws_bytes, _p(nonfinite), _stream(stream)), "shgemm_ex")
+    return out
+
+
+def plan(m: int, n: int, k: int, tune=None) -> dict:
+    p = Plan()
+    _check(lib().shg_plan(m, n, k, _tune(tune), ctypes.byref(p)), "shg_plan")
+    return {f: getattr(p, f) for f, _ in Plan._fields_}
+
+
+def workspace_size(m: int, n: int, k: int, tune=None) -> int:
+    return int(lib().shg_workspace_size(m, n, k, _tune(tune)))
+
+
+# ----------------------------------------------------------------------------------------- project
+def project_workspace_size(dims, mode: int, n: int) -> int:
+    d = (ctypes.c_int64 * len(dims))(*dims)
+    return int(lib().shg_project_workspace_size(len(dims), d, mode, n))
+
+
+def project(T: torch.Tensor, mode: int, n: int, seed: int = 0, dist="gaussian", out=None, workspace=None,
+            stream=None) -> torch.Tensor:
+    """W = A'_(mode) . Omega_(mode) (Alg 2 line 2) for a C-contiguous FP32 tensor."""
+    if T.dtype != torch.float32 or not T.is_contiguous():
+        raise ValueError("T must be a contiguous float32 tensor")
+    dims = list(T.shape)
+    M = dims[mode]
+    if out is None:
+        out = torch.empty((M, n), dtype=torch.float32, device=T.device)
+    d = (ctypes.c_int64 * len(dims))(*dims)
+    ws_bytes = 0 if workspace is None else workspace.numel() * workspace.element_size()
+    _check(lib().project(_p(T), len(dims), d, mode, n, seed, _dist(dist), _p(out), out.stride(0), _p(workspace),
+                         ws_bytes, _stream(stream)), "project")
+    return out
+
+
+# ----------------------------------------------------------------------------------------- test support
+def split(a: torch.Tensor, stream=None):
+    """Eqs 14-15 elementwise with the mainloop's device function. Returns (hi, lo) int16 bit tensors."""
+    a = a.contiguous().view(-1)
+    hi = torch.empty(a.numel(), dtype=torch.int16, device=a.device)
+    lo = torch.empty(a.numel(), dtype=torch.int16, device=a.device)
+    _check(lib().shg_debug_split(_p(a), a.numel(), _p(hi), _p(lo), _stream(stream)), "shg_debug_split")
+    return hi, lo
+
+
+def synth(kind: str, seed: int, stream_id: int, m: int, k: int, row0: int = 0, out=None, device=None,
+          stream=None) -> torch.Tensor:
+    """Counter-based synthetic FP32 matrix of OMEGA_SPEC §6 (kind 'gauss' | 'unif'), made on the device."""
+    if out is None:
+        out = torch.empty((m, k), dtype=torch.float32, device=device or "cuda")
+    _check(lib().shg_synth_f32(0 if kind == "gauss" else 1, seed, stream_id, m, k, row0, _p(out),
+                               out.stride(0) if m > 1 else max(k, 1), _stream(stream)), "shg_synth_f32")
+    return out
+
+
+def probe_umma(A16: torch.Tensor, B16: torch.Tensor, D_init: torch.Tensor | None = None, mode: int = 0,
+               nsteps: int = 4, stream=None) -> torch.Tensor:
+    """One 128 x n x 64 tcgen05 kind::f16 MMA on given FP16 inputs (see include/shgemm.h)."""
+    n = B16.shape[0]
+    D = torch.empty((128, n), dtype=torch.float32, device=A16.device)
+    _check(lib().shg_probe_umma(_p(A16.contiguous()), _p(B16.contiguous()), n,
+                                _p(None if D_init is None else D_init.contiguous()), mode, nsteps, _p(D),
+                                _stream(stream)), "shg_probe_umma")
+    return D

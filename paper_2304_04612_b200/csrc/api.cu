@@ -1,0 +1,497 @@
+// api.cu — the C ABI of include/shgemm.h: validation, planning (tile N, split-K, grid),
+// TMA tensor-map encoding (cuTensorMapEncodeTiled through cudaGetDriverEntryPoint, no -lcuda),
+// and kernel launches. No torch types cross this boundary.
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+
+#include "../../include/shgemm.h"
+#include "omega.cuh"
+#include "shgemm_sm100.cuh"
+#include "simt_fallback.cuh"
+#include "split.cuh"
+
+namespace {
+
+std::atomic<uint64_t> g_launches{0};
+thread_local char g_err[256] = "";
+
+shg_status_t cuda_fail(cudaError_t e, const char* what) {
+    std::snprintf(g_err, sizeof(g_err), "%s: %s", what, cudaGetErrorString(e));
+    return SHG_ERR_CUDA;
+}
+
+#define SHG_CUDA(call)                                              \
+    do {                                                            \
+        cudaError_t e_ = (call);                                    \
+        if (e_ != cudaSuccess) return cuda_fail(e_, #call);         \
+    } while (0)
+
+struct DevInfo {
+    int sms = 0;
+    int major = 0, minor = 0;
+    bool ok = false;
+};
+
+DevInfo& dev_info() {
+    static DevInfo infos[64];
+    static std::once_flag flags[64];
+    int dev = 0;
+    cudaGetDevice(&dev);
+    dev = std::min(std::max(dev, 0), 63);
+    std::call_once(flags[dev], [dev]() {
+        DevInfo& d = infos[dev];
+        cudaDeviceGetAttribute(&d.sms, cudaDevAttrMultiProcessorCount, dev);
+        cudaDeviceGetAttribute(&d.major, cudaDevAttrComputeCapabilityMajor, dev);
+        cudaDeviceGetAttribute(&d.minor, cudaDevAttrComputeCapabilityMinor, dev);
+        d.ok = (d.major == 10 && d.minor == 0);
+    });
+    return infos[dev];
+}
+
+// ------------------------------------------------------------------ TMA encode
+using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                              const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                              CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeFn encode_fn() {
+    static EncodeFn fn = nullptr;
+    static std::once_flag flag;
+    std::call_once(flag, []() {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<EncodeFn>(p);
+    });
+    return fn;
+}
+
+// A view: dims {S (k inner), M, P (k outer)}, strides (bytes) {row, slab}; box {32, 128, 1}
+bool encode_a(CUtensorMap* map, const float* A, int64_t S, int64_t M, int64_t P, int64_t row_stride_el,
+              int64_t slab_stride_el) {
+    EncodeFn fn = encode_fn();
+    if (!fn) return false;
+    cuuint64_t dims[3] = {static_cast<cuuint64_t>(S), static_cast<cuuint64_t>(M), static_cast<cuuint64_t>(P)};
+    cuuint64_t strides[2] = {static_cast<cuuint64_t>(row_stride_el) * 4, static_cast<cuuint64_t>(slab_stride_el) * 4};
+    cuuint32_t box[3] = {32, 128, 1};
+    cuuint32_t estr[3] = {1, 1, 1};
+    return fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(A), dims, strides, box, estr,
+              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+// Omega (column-major k x n == n rows of ldo halves): dims {k, n}, box {64, bn}
+bool encode_b(CUtensorMap* map, const uint16_t* Om, int64_t k, int64_t n, int64_t ldo, int bn) {
+    EncodeFn fn = encode_fn();
+    if (!fn) return false;
+    cuuint64_t dims[2] = {static_cast<cuuint64_t>(k), static_cast<cuuint64_t>(n)};
+    cuuint64_t strides[1] = {static_cast<cuuint64_t>(ldo) * 2};
+    cuuint32_t box[2] = {64, static_cast<cuuint32_t>(bn)};
+    cuuint32_t estr[2] = {1, 1};
+    return fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, const_cast<uint16_t*>(Om), dims, strides, box, estr,
+              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+// ------------------------------------------------------------------ planning
+constexpr int kBNs[] = {16, 32, 64, 96, 128, 144, 192, 256};
+
+int smem_for_bn(int bn) {
+    switch (bn) {
+        case 16: return shg::Cfg<16>::kSmemBytes;
+        case 32: return shg::Cfg<32>::kSmemBytes;
+        case 64: return shg::Cfg<64>::kSmemBytes;
+        case 96: return shg::Cfg<96>::kSmemBytes;
+        case 128: return shg::Cfg<128>::kSmemBytes;
+        case 144: return shg::Cfg<144>::kSmemBytes;
+        case 192: return shg::Cfg<192>::kSmemBytes;
+        default: return shg::Cfg<256>::kSmemBytes;
+    }
+}
+int sa_for_bn(int bn) {
+    switch (bn) {
+        case 16: return shg::Cfg<16>::SA;
+        case 32: return shg::Cfg<32>::SA;
+        case 64: return shg::Cfg<64>::SA;
+        case 96: return shg::Cfg<96>::SA;
+        case 128: return shg::Cfg<128>::SA;
+        case 144: return shg::Cfg<144>::SA;
+        case 192: return shg::Cfg<192>::SA;
+        default: return shg::Cfg<256>::SA;
+    }
+}
+
+struct Plan {
+    int path = 0;  // 0 tc, 1 simt, 2 trivial
+    int bn = 0, n_tiles = 0, m_tiles = 0, splits = 1, grid = 0, num_kb = 0;
+    int64_t ws_bytes = 0, ld_ws = 0;
+};
+
+bool valid_bn(int bn) {
+    for (int b : kBNs) if (b == bn) return true;
+    return false;
+}
+
+Plan make_plan(int64_t m, int64_t n, int64_t k, bool fast_ok, const shg_tune_t* tune, int sms) {
+    Plan pl;
+    if (m == 0 || n == 0 || k == 0) { pl.path = 2; return pl; }
+    if (!fast_ok || (tune && tune->force_simt)) { pl.path = 1; return pl; }
+    pl.path = 0;
+    if (tune && tune->bn > 0 && valid_bn(tune->bn)) {
+        pl.bn = tune->bn;
+        pl.n_tiles = static_cast<int>((n + pl.bn - 1) / pl.bn);
+    } else {
+        pl.n_tiles = static_cast<int>((n + 255) / 256);
+        const int64_t need = (n + pl.n_tiles - 1) / pl.n_tiles;
+        pl.bn = 256;
+        for (int b : kBNs) if (b >= need) { pl.bn = b; break; }
+    }
+    pl.m_tiles = static_cast<int>((m + shg::kBM - 1) / shg::kBM);
+    pl.num_kb = static_cast<int>((k + shg::kBK - 1) / shg::kBK);
+    const int64_t mn_tiles = static_cast<int64_t>(pl.m_tiles) * pl.n_tiles;
+    int splits = 1;
+    if (tune && tune->split_k > 0) {
+        splits = tune->split_k;
+    } else if (mn_tiles < sms) {
+        // fill the SMs with k-splits, keeping >= 4 k-blocks (256 k) per split
+        splits = static_cast<int>(std::max<int64_t>(1, sms / mn_tiles));
+        splits = static_cast<int>(std::min<int64_t>(splits, std::max<int64_t>(1, pl.num_kb / 4)));
+    }
+    splits = std::max(1, std::min(splits, pl.num_kb));
+    pl.splits = splits;
+    const int64_t tiles = mn_tiles * splits;
+    const int cap = (tune && tune->max_ctas > 0) ? tune->max_ctas : sms;
+    pl.grid = static_cast<int>(std::min<int64_t>(tiles, cap));
+    if (splits > 1) {
+        pl.ld_ws = (n + 3) / 4 * 4;
+        pl.ws_bytes = static_cast<int64_t>(splits) * m * pl.ld_ws * 4;
+    }
+    return pl;
+}
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+template <int BN>
+shg_status_t launch_tc(const CUtensorMap& mapA, const CUtensorMap& mapB, const shg::KParams& kp, int grid,
+                       cudaStream_t stream) {
+    using CF = shg::Cfg<BN>;
+    static std::once_flag flags[64];
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaError_t attr_err = cudaSuccess;
+    std::call_once(flags[std::min(std::max(dev, 0), 63)], [&]() {
+        attr_err = cudaFuncSetAttribute(shg::shgemm_sm100_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        CF::kSmemBytes);
+    });
+    if (attr_err != cudaSuccess) return cuda_fail(attr_err, "cudaFuncSetAttribute");
+    shg::shgemm_sm100_kernel<BN><<<grid, shg::kThreads, CF::kSmemBytes, stream>>>(mapA, mapB, kp);
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    SHG_CUDA(cudaGetLastError());
+    return SHG_OK;
+}
+
+shg_status_t dispatch_tc(int bn, const CUtensorMap& a, const CUtensorMap& b, const shg::KParams& kp, int grid,
+                         cudaStream_t s) {
+    switch (bn) {
+        case 16: return launch_tc<16>(a, b, kp, grid, s);
+        case 32: return launch_tc<32>(a, b, kp, grid, s);
+        case 64: return launch_tc<64>(a, b, kp, grid, s);
+        case 96: return launch_tc<96>(a, b, kp, grid, s);
+        case 128: return launch_tc<128>(a, b, kp, grid, s);
+        case 144: return launch_tc<144>(a, b, kp, grid, s);
+        case 192: return launch_tc<192>(a, b, kp, grid, s);
+        case 256: return launch_tc<256>(a, b, kp, grid, s);
+        default: return SHG_ERR_INVALID_VALUE;
+    }
+}
+
+int grid_for(int64_t work, int threads) {
+    const int sms = std::max(1, dev_info().sms);
+    return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>((work + threads - 1) / threads, int64_t(sms) * 16)));
+}
+
+// Generic A view used by shgemm (plain matrix) and project (unfoldings):
+// element (row, kk) at A[(kk / S) * slab + row * row_stride + kk % S].
+struct AView {
+    const float* A;
+    int64_t S, P, row_stride, slab;
+};
+
+shg_status_t run_shgemm(int64_t m, int64_t n, int64_t k, const AView& av, const uint16_t* Om, int64_t ldo,
+                        float* Y, int64_t ldc, const shg_tune_t* tune, void* ws, size_t ws_bytes, int* nonfinite,
+                        cudaStream_t stream) {
+    if (m == 0 || n == 0) return SHG_OK;
+    if (k == 0) {
+        SHG_CUDA(cudaMemset2DAsync(Y, ldc * sizeof(float), 0, n * sizeof(float), m, stream));
+        return SHG_OK;
+    }
+    DevInfo& d = dev_info();
+    if (!d.ok) return SHG_ERR_UNSUPPORTED_DEVICE;
+    const bool plain = (av.P == 1 && av.S == k);
+    const bool fast_ok = aligned16(av.A) && aligned16(Om) && (av.row_stride % 4 == 0) && (av.slab % 4 == 0) &&
+                         (ldo % 8 == 0) && (plain || av.S % shg::kBK == 0) && encode_fn() != nullptr &&
+                         k < (int64_t(1) << 31) && av.S < (int64_t(1) << 31);
+    Plan pl = make_plan(m, n, k, fast_ok, tune, d.sms);
+    if (pl.path == 1) {
+        if (!plain) return SHG_ERR_INVALID_VALUE;  // callers materialise non-plain views first
+        shg::shgemm_simt_kernel<<<grid_for(m * n, 256), 256, 0, stream>>>(m, n, k, av.A, av.row_stride, Om, ldo, Y,
+                                                                         ldc, nonfinite);
+        g_launches.fetch_add(1, std::memory_order_relaxed);
+        SHG_CUDA(cudaGetLastError());
+        return SHG_OK;
+    }
+    CUtensorMap mapA, mapB;
+    if (!encode_a(&mapA, av.A, av.S, m, av.P, av.row_stride, av.slab)) {
+        std::snprintf(g_err, sizeof(g_err), "cuTensorMapEncodeTiled(A) failed");
+        return SHG_ERR_CUDA;
+    }
+    if (!encode_b(&mapB, Om, k, n, ldo, pl.bn)) {
+        std::snprintf(g_err, sizeof(g_err), "cuTensorMapEncodeTiled(Omega) failed");
+        return SHG_ERR_CUDA;
+    }
+    shg::KParams kp{};
+    kp.m = m; kp.n = n; kp.k = k;
+    kp.k_inner = av.S;
+    kp.num_kb = pl.num_kb;
+    kp.m_tiles = pl.m_tiles; kp.n_tiles = pl.n_tiles; kp.splits = pl.splits;
+    void* own_ws = nullptr;
+    if (pl.splits > 1) {
+        float* wsf = nullptr;
+        if (ws && ws_bytes >= static_cast<size_t>(pl.ws_bytes)) {
+            wsf = static_cast<float*>(ws);
+        } else if (ws) {
+            return SHG_ERR_WORKSPACE;
+        } else {
+            SHG_CUDA(cudaMallocAsync(&own_ws, pl.ws_bytes, stream));
+            wsf = static_cast<float*>(own_ws);
+        }
+        kp.out = wsf;
+        kp.ldo_out = pl.ld_ws;
+        kp.split_stride = m * pl.ld_ws;
+        kp.vec_store = aligned16(wsf) ? 1 : 0;
+        kp.nonfinite = nullptr;
+    } else {
+        kp.out = Y;
+        kp.ldo_out = ldc;
+        kp.split_stride = 0;
+        kp.vec_store = (aligned16(Y) && ldc % 4 == 0) ? 1 : 0;
+        kp.nonfinite = nonfinite;
+    }
+    shg_status_t st = dispatch_tc(pl.bn, mapA, mapB, kp, pl.grid, stream);
+    if (st != SHG_OK) return st;
+    if (pl.splits > 1) {
+        shg::splitk_reduce_kernel<<<grid_for(m * n, 256), 256, 0, stream>>>(kp.out, pl.splits, m, n, pl.ld_ws,
+                                                                          kp.split_stride, Y, ldc, nonfinite);
+        g_launches.fetch_add(1, std::memory_order_relaxed);
+        SHG_CUDA(cudaGetLastError());
+        if (own_ws) SHG_CUDA(cudaFreeAsync(own_ws, stream));
+    }
+    return SHG_OK;
+}
+
+uint32_t sparse_threshold(int dist, int64_t k_total) {
+    if (dist == SHG_DIST_SPARSE3) return 715827882u;
+    if (dist == SHG_DIST_VERYSPARSE) {
+        double t = std::floor(2147483648.0 / std::sqrt(static_cast<double>(k_total)));
+        if (t > 2147483648.0) t = 2147483648.0;
+        return static_cast<uint32_t>(t);
+    }
+    return 0u;
+}
+
+}  // namespace
+
+extern "C" {
+
+shg_status_t gen_omega_f16_ex(int64_t k, int64_t n, uint64_t seed, int dist, uint32_t stream_id, int64_t row0,
+                              int64_t k_total, uint16_t* Omega, int64_t ldo, shg_stream_t stream) {
+    if (k < 0 || n < 0 || row0 < 0 || dist < 0 || dist > 3) return SHG_ERR_INVALID_VALUE;
+    if (k == 0 || n == 0) return SHG_OK;
+    if (!Omega || ldo < k) return SHG_ERR_INVALID_VALUE;
+    if (dist == SHG_DIST_VERYSPARSE && k_total < 1) return SHG_ERR_INVALID_VALUE;
+    const bool vec = ((reinterpret_cast<uintptr_t>(Omega) & 7u) == 0) && (ldo % 4 == 0) && (row0 % 4 == 0);
+    const int64_t nq = ((row0 + k - 1) >> 2) - (row0 >> 2) + 1;
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    shg::omega::gen_omega_kernel<<<grid_for(nq * n, 256), 256, 0, s>>>(k, n, seed, stream_id, row0, dist,
+                                                                      sparse_threshold(dist, k_total), Omega, ldo, vec);
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    SHG_CUDA(cudaGetLastError());
+    return SHG_OK;
+}
+
+shg_status_t gen_omega_f16(int64_t k, int64_t n, uint64_t seed, int dist, uint16_t* Omega, int64_t ldo,
+                           shg_stream_t stream) {
+    return gen_omega_f16_ex(k, n, seed, dist, 0u, 0, k, Omega, ldo, stream);
+}
+
+shg_status_t shgemm_ex(int64_t m, int64_t n, int64_t k, const float* A, int64_t lda, const uint16_t* Omega,
+                       int64_t ldo, float* Y, int64_t ldc, const shg_tune_t* tune, void* workspace,
+                       size_t workspace_bytes, int* nonfinite_flag, shg_stream_t stream) {
+    if (m < 0 || n < 0 || k < 0) return SHG_ERR_INVALID_VALUE;
+    if (m == 0 || n == 0) return SHG_OK;
+    if (!Y || ldc < n) return SHG_ERR_INVALID_VALUE;
+    if (k > 0 && (!A || !Omega || lda < k || ldo < k)) return SHG_ERR_INVALID_VALUE;
+    if (tune && tune->bn > 0 && !valid_bn(tune->bn)) return SHG_ERR_INVALID_VALUE;
+    AView av{A, k, 1, lda, lda * std::max<int64_t>(m, 1)};
+    return run_shgemm(m, n, k, av, Omega, ldo, Y, ldc, tune, workspace, workspace_bytes, nonfinite_flag,
+                      reinterpret_cast<cudaStream_t>(stream));
+}
+
+shg_status_t shgemm(int64_t m, int64_t n, int64_t k, const float* A, int64_t lda, const uint16_t* Omega,
+                    int64_t ldo, float* Y, int64_t ldc, shg_stream_t stream) {
+    return shgemm_ex(m, n, k, A, lda, Omega, ldo, Y, ldc, nullptr, nullptr, 0, nullptr, stream);
+}
+
+size_t shg_workspace_size(int64_t m, int64_t n, int64_t k, const shg_tune_t* tune) {
+    if (m <= 0 || n <= 0 || k <= 0) return 0;
+    const Plan pl = make_plan(m, n, k, true, tune, std::max(1, dev_info().sms));
+    return static_cast<size_t>(pl.ws_bytes);
+}
+
+shg_status_t shg_plan(int64_t m, int64_t n, int64_t k, const shg_tune_t* tune, shg_plan_t* out) {
+    if (!out || m < 0 || n < 0 || k < 0) return SHG_ERR_INVALID_VALUE;
+    const int sms = std::max(1, dev_info().sms);
+    const Plan pl = make_plan(m, n, k, true, tune, sms);
+    std::memset(out, 0, sizeof(*out));
+    out->path = pl.path;
+    out->bn = pl.bn; out->n_tiles = pl.n_tiles; out->m_tiles = pl.m_tiles; out->split_k = pl.splits;
+    out->grid = pl.grid;
+    if (pl.path == 0) {
+        out->stages_a = sa_for_bn(pl.bn);
+        out->stages_b = 2;
+        out->smem_bytes = smem_for_bn(pl.bn);
+        out->kernels = pl.splits > 1 ? 2 : 1;
+    } else {
+        out->kernels = pl.path == 1 ? 1 : (k == 0 && m > 0 && n > 0 ? 0 : 0);
+    }
+    out->workspace_bytes = pl.ws_bytes;
+    return SHG_OK;
+}
+
+size_t shg_project_workspace_size(int ndim, const int64_t* dims, int mode, int64_t n) {
+    if (ndim < 1 || ndim > 8 || !dims || mode < 0 || mode >= ndim || n <= 0) return 0;
+    int64_t K = 1, P = 1, S = 1;
+    for (int i = 0; i < ndim; ++i) {
+        if (i != mode) K *= dims[i];
+        if (i < mode) P *= dims[i];
+        if (i > mode) S *= dims[i];
+    }
+    const int64_t M = dims[mode];
+    const int64_t ldo = (K + 7) / 8 * 8;
+    size_t bytes = static_cast<size_t>((n * ldo * 2 + 255) / 256 * 256);
+    const bool needs_copy = !(mode == 0 || (S % shg::kBK == 0 && S % 4 == 0));
+    if (needs_copy) bytes += static_cast<size_t>((M * ((K + 3) / 4 * 4) * 4 + 255) / 256 * 256);
+    bytes += shg_workspace_size(M, n, K, nullptr);
+    return bytes;
+}
+
+shg_status_t project(const float* A, int ndim, const int64_t* dims, int mode, int64_t n, uint64_t seed, int dist,
+                     float* W, int64_t ldw, void* workspace, size_t workspace_bytes, shg_stream_t stream) {
+    if (!A || !dims || !W || ndim < 1 || ndim > 8 || mode < 0 || mode >= ndim || n < 0 || ldw < n)
+        return SHG_ERR_INVALID_VALUE;
+    if (dist < 0 || dist > 3) return SHG_ERR_INVALID_VALUE;
+    for (int i = 0; i < ndim; ++i) if (dims[i] < 1) return SHG_ERR_INVALID_VALUE;
+    if (n == 0) return SHG_OK;
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    int64_t K = 1, P = 1, S = 1;
+    for (int i = 0; i < ndim; ++i) {
+        if (i != mode) K *= dims[i];
+        if (i < mode) P *= dims[i];
+        if (i > mode) S *= dims[i];
+    }
+    const int64_t M = dims[mode];
+    const size_t need = shg_project_workspace_size(ndim, dims, mode, n);
+    void* own = nullptr;
+    uint8_t* ws = static_cast<uint8_t*>(workspace);
+    if (!ws) {
+        SHG_CUDA(cudaMallocAsync(&own, need, s));
+        ws = static_cast<uint8_t*>(own);
+    } else if (workspace_bytes < need) {
+        return SHG_ERR_WORKSPACE;
+    }
+    const int64_t ldo = (K + 7) / 8 * 8;
+    uint16_t* Om = reinterpret_cast<uint16_t*>(ws);
+    size_t off = static_cast<size_t>((n * ldo * 2 + 255) / 256 * 256);
+    shg_status_t st = gen_omega_f16_ex(K, n, seed, dist, static_cast<uint32_t>(mode), 0, K, Om, ldo, stream);
+    if (st != SHG_OK) return st;
+    AView av{A, K, 1, K, K * M};
+    if (mode == 0) {
+        av = AView{A, K, 1, K, K * M};
+    } else if (S % shg::kBK == 0 && S % 4 == 0) {
+        // A[p][r][s] -> unfold[r][p*S + s]: 3-D view {S, M, P}, row stride S, slab stride M*S
+        av = AView{A, S, P, S, M * S};
+    } else {
+        // materialise the unfolding (last mode: (P x M) row-major -> M x P, i.e. a transpose)
+        // TODO(M-major stager): read the last-mode unfolding in place
+        float* T = reinterpret_cast<float*>(ws + off);
+        const int64_t ldt = (K + 3) / 4 * 4;
+        off += static_cast<size_t>((M * ldt * 4 + 255) / 256 * 256);
+        if (S == 1) {
+            dim3 blk(32, 8);
+            shg::transpose_f32_kernel<<<grid_for(((P + 31) / 32) * ((M + 31) / 32) * 256, 256), blk, 0, s>>>(
+                A, P, M, M, T, ldt);
+            g_launches.fetch_add(1, std::memory_order_relaxed);
+            SHG_CUDA(cudaGetLastError());
+        } else {
+            // general middle mode with S % 64 != 0: copy slab by slab (p) as S-wide row blocks
+            for (int64_t p = 0; p < P; ++p) {
+                SHG_CUDA(cudaMemcpy2DAsync(T + p * S, ldt * 4, A + p * M * S, S * 4, S * 4, M,
+                                           cudaMemcpyDeviceToDevice, s));
+            }
+        }
+        av = AView{T, K, 1, ldt, ldt * M};
+    }
+    void* sk = ws + off;
+    const size_t sk_bytes = need - off;
+    st = run_shgemm(M, n, K, av, Om, ldo, W, ldw, nullptr, sk_bytes ? sk : nullptr, sk_bytes, nullptr, s);
+    if (own) {
+        cudaError_t e = cudaFreeAsync(own, s);
+        if (st == SHG_OK && e != cudaSuccess) return cuda_fail(e, "cudaFreeAsync");
+    }
+    return st;
+}
+
+shg_status_t shg_debug_split(const float* a, int64_t count, uint16_t* hi, uint16_t* lo, shg_stream_t stream) {
+    if (count < 0 || (count > 0 && (!a || !hi || !lo))) return SHG_ERR_INVALID_VALUE;
+    if (count == 0) return SHG_OK;
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    shg::debug_split_kernel<<<grid_for((count + 1) / 2, 256), 256, 0, s>>>(a, count, hi, lo);
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    SHG_CUDA(cudaGetLastError());
+    return SHG_OK;
+}
+
+shg_status_t shg_synth_f32(int kind, uint64_t seed, uint32_t stream_id, int64_t m, int64_t k, int64_t row0,
+                           float* A, int64_t lda, shg_stream_t stream) {
+    if (kind < 0 || kind > 1 || m < 0 || k < 0 || row0 < 0) return SHG_ERR_INVALID_VALUE;
+    if (m == 0 || k == 0) return SHG_OK;
+    if (!A || lda < k) return SHG_ERR_INVALID_VALUE;
+    const bool vec = aligned16(A) && (lda % 4 == 0);
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    const int64_t work = ((k + 3) / 4) * m;
+    shg::omega::synth_f32_kernel<<<grid_for(work, 256), 256, 0, s>>>(kind, seed, stream_id, m, k, row0, A, lda, vec);
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    SHG_CUDA(cudaGetLastError());
+    return SHG_OK;
+}
+
+uint64_t shg_launch_count(void) { return g_launches.load(std::memory_order_relaxed); }
+
+const char* shg_last_error(void) { return g_err; }
+
+int shg_device_supported(void) {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0) return 0;
+    return dev_info().ok ? 1 : 0;
+}
+
+const char* shg_version(void) { return "shgemm-b200 0.1.0 sm_100a"; }
+
+}  // extern "C"

@@ -1,0 +1,103 @@
+// probes.cu — tcgen05 semantics probe. The paper's error analysis rests on the
+// A100 tensor-core accumulation properties it lists at PAPER.md:505-512 ("confirmed theoretically
+// or empirically through small numerical experiments"). This kernel lets the tests run the
+// same kind of small experiments on B200: a single 128 x n x 64 UMMA with chosen FP16 inputs and a
+// chosen FP32 accumulator preload, so RN-vs-RZ, alignment width and the scale-input-d semantics the
+// mainloop relies on can be measured instead of assumed.
+#include <cstdint>
+#include <cuda_runtime.h>
+#include "ptx.cuh"
+#include "../../include/shgemm.h"
+
+namespace shg {
+
+__global__ void __launch_bounds__(128, 1)
+probe_umma_kernel(const uint16_t* __restrict__ A, const uint16_t* __restrict__ B, int n,
+                  const float* __restrict__ Dinit, int mode, int nsteps, float* __restrict__ Dout) {
+    extern __shared__ uint8_t smem_raw[];
+    const uint32_t raw_addr = smem_u32(smem_raw);
+    uint8_t* base = smem_raw + ((1024u - (raw_addr & 1023u)) & 1023u);
+    uint8_t* sA = base;                 // 128 rows x 128 B
+    uint8_t* sB = base + 128 * 128;     // n rows x 128 B
+    uint64_t* bar = reinterpret_cast<uint64_t*>(sB + 256 * 128);
+    uint32_t* tslot = reinterpret_cast<uint32_t*>(bar + 1);
+    const int t = threadIdx.x;
+    const uint32_t warp = warp_id();
+
+    // K-major SWIZZLE_128B canonical layout: row r at r*128, 16-B chunk c at (c ^ (r & 7)) * 16
+    for (int r = t; r < 128 + n; r += 128) {
+        const uint16_t* src = r < 128 ? A + r * 64 : B + (r - 128) * 64;
+        uint8_t* dst = r < 128 ? sA + r * 128 : sB + (r - 128) * 128;
+        for (int c = 0; c < 8; ++c) {
+            const uint4 v = *reinterpret_cast<const uint4*>(src + 8 * c);
+            *reinterpret_cast<uint4*>(dst + ((c ^ (r & 7)) * 16)) = v;
+        }
+    }
+    fence_proxy_async_smem();
+    if (t == 0) { mbar_init(bar, 1); fence_mbar_init(); }
+    if (warp == 0) tmem_alloc<256>(tslot);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tbase = *tslot;
+    const uint32_t lane_base = (32u * warp) << 16;
+
+    if (Dinit != nullptr) {
+        for (int c = 0; c < n; c += 16) {
+            float v[16];
+            for (int i = 0; i < 16; ++i) v[i] = Dinit[t * n + c + i];
+            tmem_st16(tbase + lane_base + c, v);
+        }
+        tmem_st_wait();
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+
+    if (warp == 0) {
+        if (elect_one()) {
+            const uint32_t idesc = idesc_f16_f32(128, static_cast<uint32_t>(n));
+            const uint64_t ad = sw128_kmajor_desc(smem_u32(sA));
+            const uint64_t bd = sw128_kmajor_desc(smem_u32(sB));
+            for (int j = 0; j < nsteps; ++j) {
+                if (j == 0 && mode == 1) {
+                    mma_f16_ss_scaled<11>(tbase, ad, bd, idesc);
+                } else {
+                    const uint32_t acc = (j > 0 || Dinit != nullptr) ? 1u : 0u;
+                    mma_f16_ss(tbase, ad + 2 * j, bd + 2 * j, idesc, acc);
+                }
+            }
+            tc_commit(bar);
+        }
+        __syncwarp();
+    }
+    mbar_wait(bar, 0);
+    tc_fence_after();
+    for (int c = 0; c < n; c += 16) {
+        float v[16];
+        tmem_ld16(tbase + lane_base + c, v);
+        tmem_ld_wait();
+        for (int i = 0; i < 16; ++i) Dout[t * n + c + i] = v[i];
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 0) {
+        tc_fence_after();
+        tmem_dealloc<256>(tbase);
+    }
+}
+
+}  // namespace shg
+
+extern "C" shg_status_t shg_probe_umma(const uint16_t* A, const uint16_t* B, int n, const float* D_init,
+                                       int mode, int nsteps, float* D_out, shg_stream_t stream) {
+    if (!A || !B || !D_out || n < 16 || n > 256 || (n % 16) || nsteps < 1 || nsteps > 4 || mode < 0 || mode > 1)
+        return SHG_ERR_INVALID_VALUE;
+    if (mode == 1 && D_init == nullptr) return SHG_ERR_INVALID_VALUE;
+    const int smem = 1024 + 128 * 128 + 256 * 128 + 64;
+    cudaError_t e = cudaFuncSetAttribute(shg::probe_umma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return SHG_ERR_CUDA;
+    shg::probe_umma_kernel<<<1, 128, smem, reinterpret_cast<cudaStream_t>(stream)>>>(A, B, n, D_init, mode, nsteps, D_out);
+    e = cudaGetLastError();
+    return e == cudaSuccess ? SHG_OK : SHG_ERR_CUDA;
+}

@@ -1,0 +1,63 @@
+// simt_fallback.cuh — correctness-only SHGEMM on CUDA cores, used when the tensor-core path's
+// TMA alignment preconditions fail (base pointers not 16-B aligned, lda % 4 != 0, ldo % 8 != 0).
+// Same numerics contract as the mainloop: Eqs 14-16 with the hi+lo partial
+// of every 64-k chunk folded with RN into an FP32 accumulator (RZ avoidance).
+#pragma once
+#include <cstdint>
+#include <cuda_fp16.h>
+#include "split.cuh"
+
+namespace shg {
+
+__global__ void shgemm_simt_kernel(int64_t m, int64_t n, int64_t k, const float* __restrict__ A, int64_t lda,
+                                   const uint16_t* __restrict__ Om, int64_t ldo, float* __restrict__ Y,
+                                   int64_t ldc, int* nonfinite) {
+    const int64_t total = m * n;
+    for (int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; t < total;
+         t += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int64_t i = t / n, j = t - (t / n) * n;
+        const float* a = A + i * lda;
+        const uint16_t* w = Om + j * ldo;
+        float acc = 0.0f;
+        for (int64_t k0 = 0; k0 < k; k0 += 64) {
+            const int64_t k1 = k0 + 64 < k ? k0 + 64 : k;
+            float s_hi = 0.0f, s_lo = 0.0f;
+            for (int64_t l = k0; l < k1; ++l) {
+                uint32_t h, lo;
+                split2(a[l], 0.0f, h, lo);
+                const float hf = __half2float(__ushort_as_half(static_cast<uint16_t>(h & 0xFFFFu)));
+                const float lf = __half2float(__ushort_as_half(static_cast<uint16_t>(lo & 0xFFFFu)));
+                const float wf = __half2float(__ushort_as_half(w[l]));
+                s_hi = __fmaf_rn(hf, wf, s_hi);
+                s_lo = __fmaf_rn(lf, wf, s_lo);
+            }
+            acc = __fadd_rn(acc, __fmaf_rn(s_lo, 4.8828125e-4f, s_hi));
+        }
+        Y[i * ldc + j] = acc;
+        if (nonfinite && !isfinite(acc)) atomicOr(nonfinite, 1);
+    }
+}
+
+// out[c * ldo + r] = in[r * ldi + c] for an R x Cc matrix (used by project() for the M-major
+// last-mode unfolding until the native M-major stager lands).
+__global__ void transpose_f32_kernel(const float* __restrict__ in, int64_t R, int64_t Cc, int64_t ldi,
+                                     float* __restrict__ out, int64_t ldo) {
+    __shared__ float tile[32][33];
+    const int64_t tiles_c = (Cc + 31) / 32;
+    const int64_t tiles_r = (R + 31) / 32;
+    for (int64_t tb = blockIdx.x; tb < tiles_r * tiles_c; tb += gridDim.x) {
+        const int64_t br = (tb / tiles_c) * 32, bc = (tb % tiles_c) * 32;
+        for (int y = threadIdx.y; y < 32; y += blockDim.y) {
+            const int64_t r = br + y, c = bc + threadIdx.x;
+            if (r < R && c < Cc) tile[y][threadIdx.x] = in[r * ldi + c];
+        }
+        __syncthreads();
+        for (int y = threadIdx.y; y < 32; y += blockDim.y) {
+            const int64_t c = bc + y, r = br + threadIdx.x;
+            if (r < R && c < Cc) out[c * ldo + r] = tile[threadIdx.x][y];
+        }
+        __syncthreads();
+    }
+}
+
+}  // namespace shg

@@ -1,0 +1,52 @@
+// split.cuh — the in-kernel FP32 -> (FP16 hi, FP16 lo) split of Eqs 14-15:
+//   A_low  = toLow(A_F32)                                   (RN ties-to-even)
+//   dA_low = toLow((A_F32 - toF32(A_low)) * 2^11)
+// so that A_F32 ~= A_low + dA_low * 2^-11 (Eq 16). The subtraction is exact for
+// |a| in the FP16 range and the x2^11 is an exact exponent shift; both are written as explicit
+// _rn ops in exactly this order (no contraction into an fma) so |a| >= 65520 gives hi = +-inf,
+// lo = -+inf like the definition (the FP16-range failure mode of PAPER.md:495, :705-706).
+#pragma once
+#include <cstdint>
+#include <cuda_fp16.h>
+
+namespace shg {
+
+// two FP32 values -> packed FP16x2 hi and lo (low half = first value)
+__device__ __forceinline__ void split2(float a0, float a1, uint32_t& hi, uint32_t& lo) {
+    const __half2 h = __floats2half2_rn(a0, a1);               // cvt.rn.f16x2.f32
+    const float2 hf = __half22float2(h);
+    const float r0 = __fmul_rn(__fsub_rn(a0, hf.x), 2048.0f);
+    const float r1 = __fmul_rn(__fsub_rn(a1, hf.y), 2048.0f);
+    const __half2 l = __floats2half2_rn(r0, r1);
+    hi = *reinterpret_cast<const uint32_t*>(&h);
+    lo = *reinterpret_cast<const uint32_t*>(&l);
+}
+
+// eight consecutive-k FP32 values -> 16 B of hi and 16 B of lo
+__device__ __forceinline__ void split8(const float4& x0, const float4& x1, uint4& hi, uint4& lo) {
+    split2(x0.x, x0.y, hi.x, lo.x);
+    split2(x0.z, x0.w, hi.y, lo.y);
+    split2(x1.x, x1.y, hi.z, lo.z);
+    split2(x1.z, x1.w, hi.w, lo.w);
+}
+
+// Elementwise split, for the test ABI shg_debug_split (same device function as the mainloop).
+__global__ void debug_split_kernel(const float* __restrict__ a, int64_t count, uint16_t* __restrict__ hi,
+                                   uint16_t* __restrict__ lo) {
+    for (int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; 2 * t < count;
+         t += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int64_t i = 2 * t;
+        const float a0 = a[i];
+        const float a1 = (i + 1 < count) ? a[i + 1] : 0.0f;
+        uint32_t h, l;
+        split2(a0, a1, h, l);
+        hi[i] = static_cast<uint16_t>(h & 0xFFFFu);
+        lo[i] = static_cast<uint16_t>(l & 0xFFFFu);
+        if (i + 1 < count) {
+            hi[i + 1] = static_cast<uint16_t>(h >> 16);
+            lo[i + 1] = static_cast<uint16_t>(l >> 16);
+        }
+    }
+}
+
+}  // namespace shg

@@ -1,0 +1,77 @@
+"""CPU-side checks of the boundary: libshgemm.so builds for sm_100a, loads, exports every symbol
+include/shgemm.h declares, contains tcgen05/TMA instructions, and rejects bad arguments
+synchronously (no GPU needed for argument validation)."""
+import ctypes
+import os
+import re
+import subprocess
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "shgemm.h")
+
+
+@pytest.fixture(scope="module")
+def shg():
+    from paper_2304_04612_b200 import _build
+    _build.build()
+    import paper_2304_04612_b200 as m
+    return m
+
+
+def declared_functions():
+    text = open(HEADER).read()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    names = re.findall(r"^\s*(?:const\s+)?[A-Za-z_][\w\s\*]*?\b([a-z_][a-z0-9_]*)\s*\(", text, flags=re.M)
+    return sorted(set(n for n in names if n not in ("if", "return")))
+
+
+def test_header_declares_the_boundary():
+    names = declared_functions()
+    for need in ("shgemm", "shgemm_ex", "gen_omega_f16", "gen_omega_f16_ex", "project", "shg_debug_split",
+                 "shg_workspace_size", "shg_plan", "shg_project_workspace_size", "shg_synth_f32",
+                 "shg_launch_count", "shg_last_error", "shg_device_supported", "shg_version", "shg_probe_umma"):
+        assert need in names, need
+
+
+def test_library_exports_every_declared_symbol(shg):
+    L = ctypes.CDLL(shg.LIB_PATH)
+    for name in declared_functions():
+        assert hasattr(L, name), name
+    out = subprocess.run(["nm", "-D", "--defined-only", shg.LIB_PATH], capture_output=True, text=True).stdout
+    for name in declared_functions():
+        assert re.search(rf"\bT {name}$", out, flags=re.M), name
+
+
+def test_sass_is_blackwell_native(shg):
+    sass = subprocess.run(["cuobjdump", "-sass", shg.LIB_PATH], capture_output=True, text=True).stdout
+    assert "arch = sm_100a" in sass or "sm_100a" in sass
+    assert "UTCHMMA" in sass          # tcgen05.mma
+    assert "UTMALDG" in sass          # TMA loads
+    assert "LDTM" in sass             # tcgen05.ld
+    assert "HMMA" not in sass.replace("UTCHMMA", "")   # no legacy mma.sync path
+    # the scale-input-d = 11 fold of the lo product
+    assert re.search(r"UTCHMMA.*0xb\b", sass)
+
+
+def test_argument_validation_without_gpu(shg):
+    L = shg.lib()
+    # negative dims / bad leading dimensions are rejected before any CUDA call
+    assert L.shgemm(-1, 4, 4, None, 4, None, 4, None, 4, None) == 1
+    assert L.shgemm(4, 4, 8, ctypes.c_void_p(16), 4, ctypes.c_void_p(16), 8, ctypes.c_void_p(16), 4, None) == 1
+    assert L.shgemm(0, 4, 4, None, 4, None, 4, None, 4, None) == 0          # m == 0: no-op
+    assert L.gen_omega_f16(4, 4, 0, 7, None, 4, None) == 1                   # bad dist
+    dims = (ctypes.c_int64 * 3)(2, 3, 4)
+    assert L.project(ctypes.c_void_p(16), 3, dims, 3, 4, 0, 0, ctypes.c_void_p(16), 4, None, 0, None) == 1
+    assert L.shg_probe_umma(None, None, 24, None, 0, 4, None, None) == 1
+
+
+def test_python_binding_has_no_fallback(shg, monkeypatch, tmp_path):
+    import importlib
+    import paper_2304_04612_b200 as m
+    monkeypatch.setattr(m, "LIB_PATH", str(tmp_path / "missing.so"))
+    monkeypatch.setattr(m, "_lib", None)
+    with pytest.raises(m.SHGError):
+        m.lib()
+    importlib.reload(m)

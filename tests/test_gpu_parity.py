@@ -1,0 +1,302 @@
+"""GPU parity tests: the CUDA path (through the C ABI) against the CPU oracle on the same seeded
+inputs. Bars: Omega and the split bit-exact; Y within the north_star bars;
+exact-arithmetic cases bit-exact."""
+import json
+import os
+
+import numpy as np
+import pytest
+
+import synth
+from gpu_common import check_bars, omega_bits, to_np
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def shg():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2304_04612_b200 import _build
+    _build.build()
+    import paper_2304_04612_b200 as m
+    assert m.device_supported(), "device is not sm_100"
+    return m
+
+
+def cuda(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+# ------------------------------------------------------------------------------------------ Omega
+@pytest.mark.parametrize("k,n,seed,dist,stream_id,row0", [
+    (512, 32, 0, 0, 0, 0),             # config 1
+    (16384, 272, 0, 0, 0, 0),          # config 2 (4.46M elements)
+    (1001, 17, 123, 0, 5, 3),          # ragged, odd row offset
+    (4096, 256, 0, 0, 0, 0),           # config 4
+    (3000, 40, 9, 1, 2, 0),            # Rademacher
+    (3000, 40, 9, 2, 2, 8),            # s = 3
+    (10000, 33, 9, 3, 1, 0),           # very sparse s = sqrt(k)
+])
+def test_omega_bit_exact(shg, orc, k, n, seed, dist, stream_id, row0):
+    Om = shg.gen_omega(k, n, seed=seed, dist=dist, stream_id=stream_id, row0=row0)
+    torch.cuda.synchronize()
+    ref = orc.omega_f16(k, n, seed=seed, dist=dist, stream_id=stream_id, row0=row0, k_total=k)
+    got = omega_bits(Om)
+    assert got.shape == ref.shape
+    mism = int(np.sum(got != ref))
+    assert mism == 0, f"{mism} mismatches"
+
+
+def test_omega_bit_exact_1e8(shg, orc):
+    """>= 1e8 elements at the config-3 shape (K = 2^20 rows, n = 64 per mode, stream = mode)."""
+    total = 0
+    for mode in range(2):
+        Om = shg.gen_omega(1 << 20, 64, seed=0, stream_id=mode)
+        ref = orc.omega_f16(1 << 20, 64, seed=0, stream_id=mode)
+        assert np.array_equal(omega_bits(Om), ref)
+        total += ref.size
+    assert total >= 1e8
+
+
+# ------------------------------------------------------------------------------------------ split
+def test_split_exhaustive_all_fp32(shg, orc):
+    """Device split (the mainloop's device function) == oracle split on all 2^32 FP32 patterns."""
+    chunk = 1 << 28
+    for c in range((1 << 32) // chunk):
+        lo_pat = c * chunk
+        bits = torch.arange(lo_pat, lo_pat + chunk, dtype=torch.int64, device="cuda").to(torch.int32)
+        a = bits.view(torch.float32)
+        hi, lo = shg.split(a)
+        hi_np = to_np(hi).view(np.uint16)
+        lo_np = to_np(lo).view(np.uint16)
+        a_np = np.arange(lo_pat, lo_pat + chunk, dtype=np.uint64).astype(np.uint32).view(np.float32)
+        rhi, rlo = orc.split(a_np)
+        nan = np.isnan(a_np)
+        ok_hi = (hi_np == rhi) | (nan & ((hi_np & 0x7C00) == 0x7C00) & ((hi_np & 0x3FF) != 0))
+        # lo of NaN / inf inputs: NaN class compare
+        lo_nan_g = ((lo_np & 0x7C00) == 0x7C00) & ((lo_np & 0x3FF) != 0)
+        lo_nan_r = ((rlo & 0x7C00) == 0x7C00) & ((rlo & 0x3FF) != 0)
+        ok_lo = (lo_np == rlo) | (lo_nan_g & lo_nan_r)
+        assert ok_hi.all(), hex(int(a_np.view(np.uint32)[~ok_hi][0]))
+        assert ok_lo.all(), hex(int(a_np.view(np.uint32)[~ok_lo][0]))
+
+
+# ------------------------------------------------------------------------------------------ probes
+def _probe_inputs(n=64):
+    A = np.zeros((128, 64), np.float16)
+    B = np.zeros((n, 64), np.float16)
+    return A, B
+
+
+def test_probe_umma_exact_small_integers(shg):
+    """128 x 64 x 64 MMA on small integers is exact: validates descriptors, swizzle, TMEM ld."""
+    rng = np.random.default_rng(0)
+    A = rng.integers(-4, 5, size=(128, 64)).astype(np.float16)
+    B = rng.integers(-4, 5, size=(64, 64)).astype(np.float16)
+    D = shg.probe_umma(cuda(A.view(np.int16)), cuda(B.view(np.int16)), None, mode=0, nsteps=4)
+    ref = A.astype(np.float64) @ B.astype(np.float64).T
+    assert np.array_equal(to_np(D).astype(np.float64), ref)
+    D1 = shg.probe_umma(cuda(A.view(np.int16)), cuda(B.view(np.int16)), None, mode=0, nsteps=1)
+    ref1 = A[:, :16].astype(np.float64) @ B[:, :16].astype(np.float64).T
+    assert np.array_equal(to_np(D1).astype(np.float64), ref1)
+
+
+def test_probe_scale_input_d(shg):
+    """The fold the mainloop relies on: first MMA with scale-input-d = 11 computes
+    D = D_init * 2^-11 + A_0 B_0^T (then the rest accumulate)."""
+    rng = np.random.default_rng(1)
+    A = rng.integers(-3, 4, size=(128, 64)).astype(np.float16)
+    B = rng.integers(-3, 4, size=(32, 64)).astype(np.float16)
+    Dinit = (rng.integers(-2048 * 8, 2048 * 8, size=(128, 32))).astype(np.float32)
+    D = shg.probe_umma(cuda(A.view(np.int16)), cuda(B.view(np.int16)), cuda(Dinit), mode=1, nsteps=4)
+    ref = Dinit.astype(np.float64) * 2.0 ** -11 + A.astype(np.float64) @ B.astype(np.float64).T
+    assert np.array_equal(to_np(D).astype(np.float64), ref)
+
+
+def test_probe_accumulation_semantics(shg):
+    """Record B200 tensor-core accumulation behaviour (PAPER.md:505-512 lists A100's):
+    D = 1 plus one product 1.5 * 2^-24 -> RN gives 1 + 2^-23, RZ gives 1. Results go to
+    gpurun_out/probe_semantics.json; the mainloop's correctness does not depend on them."""
+    res = {}
+    for name, a, b, d0 in [("pos_1.5ulp_half", 1.5 * 2 ** -12, 2 ** -12, 1.0),
+                           ("neg_1.5ulp_half", -1.5 * 2 ** -12, 2 ** -12, -1.0),
+                           ("pos_0.75ulp", 0.75 * 2 ** -12, 2 ** -12, 1.0),
+                           ("pos_tiny_2^-30", 2 ** -15, 2 ** -15, 1.0)]:
+        A, B = _probe_inputs(16)
+        A[:, 0] = a
+        B[:, 0] = b
+        Dinit = np.full((128, 16), d0, np.float32)
+        D = to_np(shg.probe_umma(cuda(A.view(np.int16)), cuda(B.view(np.int16)), cuda(Dinit), mode=0, nsteps=1))
+        res[name] = float(D[0, 0]) - d0
+    # many small terms inside one K=16 instruction: 16 x 2^-25 on top of 1.0
+    A, B = _probe_inputs(16)
+    A[:, :16] = 2 ** -13
+    B[:, :16] = 2 ** -12
+    D = to_np(shg.probe_umma(cuda(A.view(np.int16)), cuda(B.view(np.int16)), cuda(np.ones((128, 16), np.float32)),
+                             mode=0, nsteps=1))
+    res["16x2^-25_on_1"] = float(D[0, 0]) - 1.0
+    os.makedirs("gpurun_out", exist_ok=True)
+    with open(os.path.join("gpurun_out", "probe_semantics.json"), "w") as f:
+        json.dump(res, f, indent=1)
+    assert np.isfinite(list(res.values())).all()
+
+
+# ------------------------------------------------------------------------------------------ SHGEMM
+def _run(shg, A, k, n, seed=0, dist=0, tune=None):
+    Om = shg.gen_omega(k, n, seed=seed, dist=dist)
+    Y = shg.shgemm(cuda(A), Om, tune=tune)
+    torch.cuda.synchronize()
+    return omega_bits(Om), to_np(Y)
+
+
+def test_identity_omega_reconstructs_split(shg, orc):
+    """Omega = [I; 0]: Y[i][j] = hi + lo 2^-11 of A[i][j] exactly (22-bit sum fits FP32)."""
+    m, k, n = 256, 192, 128
+    A = synth.gaussian(m, k, seed=3) * np.float32(7.0)
+    eye = np.eye(k, n, dtype=np.float32).astype(np.float16)
+    Om = torch.from_numpy(np.ascontiguousarray(eye.T)).cuda().t()      # column-major (k, n)
+    Y = to_np(shg.shgemm(cuda(A), Om))
+    hi, lo = orc.split(A[:, :n])
+    rec = (hi.view(np.float16).astype(np.float64) + lo.view(np.float16).astype(np.float64) * 2.0 ** -11)
+    rec = rec.reshape(m, n).astype(np.float32)
+    assert np.array_equal(Y, rec)
+    frac = np.mean(Y != A[:, :n])
+    assert 0.15 < frac < 0.35
+
+
+def test_exact_integer_case_bitwise(shg, orc):
+    """Small-integer A with Rademacher Omega: exact arithmetic -> Y_gpu == exact product."""
+    m, k, n = 300, 2048, 64
+    A = synth.small_int_matrix(m, k, seed=5)
+    om, Y = _run(shg, A, k, n, seed=3, dist=1)
+    assert np.array_equal(Y.astype(np.float64), orc.gemm_y64(A, om))
+
+
+def test_fp16_exact_A_split_is_exact(shg, orc):
+    """A exactly FP16-representable: lo == 0 and Y == sum of hi products (north_star)."""
+    m, k, n = 200, 512, 48
+    A = synth.gaussian(m, k, seed=9).astype(np.float16).astype(np.float32)
+    om, Y = _run(shg, A, k, n, seed=1)
+    check_bars(orc, A, om, Y)
+
+
+CASES = [
+    # (m, k, n, dist_A)        -- several tiles, ragged tails in every dimension
+    (512, 512, 32, "spectrum"),    # BASELINE config 1
+    (512, 512, 32, "normal"),
+    (512, 512, 32, "uniform"),
+    (300, 1000, 50, "normal"),
+    (129, 65, 17, "normal"),
+    (1000, 777, 272, "normal"),    # two N tiles of 144
+    (640, 4096, 256, "normal"),
+    (256, 3000, 512, "uniform"),   # two N tiles of 256
+    (130, 64, 16, "normal"),
+    (384, 16384, 64, "normal"),    # split-K
+]
+
+
+@pytest.mark.parametrize("m,k,n,kind", CASES)
+def test_shgemm_bars(shg, orc, m, k, n, kind):
+    if kind == "spectrum":
+        A = synth.spectrum_matrix(synth.spectrum("exp", m, 22, 1e-2), seed=1)[:, :k]
+    elif kind == "normal":
+        A = synth.gaussian(m, k, seed=m + k)
+    else:
+        A = synth.uniform(m, k, seed=m + k)
+    om, Y = _run(shg, A, k, n)
+    check_bars(orc, A, om, Y)
+
+
+@pytest.mark.parametrize("tune", [{"force_simt": 1}, {"split_k": 3}, {"bn": 64}, {"max_ctas": 3}])
+def test_shgemm_tunables(shg, orc, tune):
+    m, k, n = 400, 1500, 100
+    A = synth.gaussian(m, k, seed=2)
+    om, Y = _run(shg, A, k, n, tune=tune)
+    check_bars(orc, A, om, Y)
+
+
+def test_deterministic(shg):
+    A = cuda(synth.gaussian(700, 3000, seed=4))
+    Om = shg.gen_omega(3000, 200, seed=1)
+    Y1 = shg.shgemm(A, Om).clone()
+    Y2 = shg.shgemm(A, Om)
+    torch.cuda.synchronize()
+    assert torch.equal(Y1, Y2)
+
+
+def test_misaligned_leading_dims_fall_back(shg, orc):
+    m, k, n = 100, 130, 20
+    Afull = synth.gaussian(m, k + 3, seed=8)
+    A = cuda(Afull)[:, 1:k + 1]              # lda = k + 3 (not % 4), base offset 4 B
+    Om = shg.gen_omega(k, n, seed=2)
+    Y = to_np(shg.shgemm(A, Om))
+    check_bars(orc, Afull[:, 1:k + 1], omega_bits(Om), Y)
+
+
+def test_edge_sizes(shg):
+    Om = shg.gen_omega(0, 5)
+    Y = shg.shgemm(torch.zeros((3, 0), device="cuda"), Om)
+    torch.cuda.synchronize()
+    assert torch.equal(Y, torch.zeros((3, 5), device="cuda"))
+    Y = shg.shgemm(torch.zeros((0, 8), device="cuda"), shg.gen_omega(8, 4))
+    assert Y.shape == (0, 4)
+
+
+def test_fp16_range_failure_is_flagged(shg):
+    """|a| > 65504 -> non-finite Y rows and the flag (PAPER.md:705-706 'expected to fail')."""
+    A = synth.cauchy_like(256, seed=0)
+    flag = torch.zeros(1, dtype=torch.int32, device="cuda")
+    Om = shg.gen_omega(256, 32, seed=0)
+    Y = to_np(shg.shgemm(cuda(A), Om, nonfinite=flag))
+    assert int(flag.item()) == 1
+    bad_rows = np.any(np.abs(A) >= 65520, axis=1)
+    assert bad_rows.any()
+    assert np.all(np.any(~np.isfinite(Y[bad_rows]), axis=1))
+    assert np.all(np.isfinite(Y[~bad_rows]))
+
+
+# ------------------------------------------------------------------------------------------ synth / full size
+def test_device_synth_matches_oracle_rows(shg, orc):
+    A = shg.synth("gauss", 2, 0x100, 300, 1000, row0=77)
+    rows = np.array([0, 1, 150, 299]) + 77
+    ref = orc.synth_rows("gauss", 2, 0x100, rows, 1000)
+    assert np.array_equal(to_np(A)[rows - 77], ref)
+    U = shg.synth("unif", 5, 0x101, 10, 64)
+    assert np.array_equal(to_np(U), orc.synth_rows("unif", 5, 0x101, np.arange(10), 64))
+
+
+def test_config4_full_size_sampled(shg, orc):
+    """BASELINE config 4 at full size (A 4,194,304 x 4096 FP32 = 64 GiB on the device), the
+    launch configuration bench.py times; 256 sampled rows (first/last + random) checked."""
+    m, k, n = 4194304, 4096, 256
+    free, _ = torch.cuda.mem_get_info()
+    if free < (m * k * 4 + m * n * 4) * 1.05:
+        pytest.skip("not enough device memory")
+    A = shg.synth("gauss", 2, 0x100, m, k)
+    Om = shg.gen_omega(k, n, seed=0)
+    Y = shg.shgemm(A, Om)
+    torch.cuda.synchronize()
+    rng = np.random.default_rng(0)
+    rows = np.unique(np.concatenate([[0, 127, 128, m - 1], rng.integers(0, m, 252)]))
+    Arows = orc.synth_rows("gauss", 2, 0x100, rows, k)
+    assert np.array_equal(to_np(A[torch.from_numpy(rows).cuda()]), Arows)
+    Ys = to_np(Y[torch.from_numpy(rows).cuda()])
+    del A, Y
+    torch.cuda.empty_cache()
+    check_bars(orc, Arows, omega_bits(Om), Ys)
+
+
+# ------------------------------------------------------------------------------------------ project
+@pytest.mark.parametrize("dims", [(24, 40, 64), (16, 128, 32), (10, 12, 14)])
+def test_project_all_modes(shg, orc, dims):
+    from oracle import pipelines as pl
+    T = synth.gaussian(int(np.prod(dims)), 1, seed=sum(dims)).reshape(dims)
+    Tt = cuda(T)
+    for mode in range(3):
+        n = 24
+        W = to_np(shg.project(Tt, mode, n, seed=3))
+        U = np.ascontiguousarray(pl.unfold(T, mode))
+        om = orc.omega_f16(U.shape[1], n, seed=3, stream_id=mode)
+        check_bars(orc, U, om, W)
