@@ -1,0 +1,324 @@
+#!/usr/bin/env python
+"""bench.py — SHGEMM random projection on B200 (BASELINE.json config 4, row-sharded).
+
+One step = the whole hot path on this rank's row block: gen_omega_f16 (Omega regenerated from the
+shared seed, no communication) + shgemm (TMA A stager, splitter, tcgen05 hi/lo MMAs, RN promotion,
+epilogue). Inputs are resident in HBM before timing (A made in place by the counter-based
+generator; 64 GiB / N per rank, far larger than L2, so no L2 flush is needed).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl shgemm|reference] [--config cfg4|cfg5n256|...]
+  python -m torch.distributed.run --nproc-per-node N --master-addr 127.0.0.1 bench.py --gpus N ...
+
+Prints ONE JSON line on rank 0 (keys per the driver contract, plus roofline and cpu_baseline).
+--impl reference times the CPU oracle (oracle/, naive FP32 GEMM in C + its Omega generator) as
+the reference arm, on a bounded sample of the same workload, on rank 0 only.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "SHGEMM TFLOP/s & % roofline at 1/2/4/8 B200; RSVD/RP-HOSVD time"
+DATA_SEED, DATA_STREAM, OMEGA_SEED = 2, 0x100, 0
+
+CONFIGS = {
+    # name: (m_total, k, n, description)
+    "cfg4": (4194304, 4096, 256, "BASELINE config 4: tall projection A 4,194,304x4096 FP32 . Omega 4096x256 FP16"),
+    "cfg5n64": (32768, 32768, 64, "BASELINE config 5 sweep point n=64 (m=k=32768)"),
+    "cfg5n256": (32768, 32768, 256, "BASELINE config 5 sweep point n=256 (m=k=32768)"),
+    "cfg5n1024": (32768, 32768, 1024, "BASELINE config 5 sweep point n=1024 (m=k=32768)"),
+}
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), float(d["bf16_tflops"]), float(d.get("bf16_tflops_sustained", d["bf16_tflops"])), "measured"
+    return 6650.0, 1590.0, 1400.0, "fallback (B200_PROFILING.md)"
+
+
+def ncu_traffic(config):
+    """Per-launch DRAM bytes of the dominant kernel from the committed ncu --set full capture."""
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if not os.path.exists(p):
+        return None
+    d = json.load(open(p))
+    v = d.get(config)
+    return None if v is None else float(v)
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region (B200_PROFILING.md)."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                     timeout=5).stdout.strip()
+                if out:
+                    self.samples.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.1)
+
+    def start(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+
+    def stop(self):
+        self._stop.set()
+        if self._t:
+            self._t.join(timeout=10)
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0}
+        sm = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        mx = [float(s[2]) for s in self.samples if s[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4) if len(s) > 5 + i and s[5 + i].strip() == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+def cpu_baseline(m, k, n, budget_s=10.0):
+    """The oracle as it stands (naive FP32 GEMM, sequential fmaf over k, OpenMP over rows) on a
+    bounded row sample of the same workload; rate scaled to TFLOP/s."""
+    import numpy as np
+    import oracle
+    om = oracle.omega_f16(k, n, seed=OMEGA_SEED)
+    rows = 64
+    t_used = 0.0
+    elapsed, done = 0.0, 0
+    while True:
+        sample = np.arange(rows, dtype=np.int64) * max(1, m // rows)
+        A = oracle.synth_rows("gauss", DATA_SEED, DATA_STREAM, sample, k)
+        t0 = time.perf_counter()
+        oracle.gemm_y32(A, om)
+        dt = time.perf_counter() - t0
+        elapsed, done = dt, rows
+        t_used += dt
+        if dt > budget_s / 4 or t_used > budget_s or rows >= m:
+            break
+        rows = min(m, int(rows * max(2.0, min(8.0, (budget_s / 3) / max(dt, 1e-3)))))
+    flops = 2.0 * done * k * n
+    return {"value": flops / elapsed / 1e12, "unit": "TFLOP/s", "cores": oracle.num_threads(), "kind": "oracle",
+            "sample": f"{done} of {m} rows of A ({k}x{n} Omega), naive FP32 fmaf GEMM, {elapsed:.2f} s"}
+
+
+def run_reference(args, cfg_name):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import numpy as np
+    import oracle
+    m, k, n, desc = CONFIGS[cfg_name]
+    # size one step so that warmup + steps fit in ~2-3 minutes
+    rows = 2048
+    A = oracle.synth_rows("gauss", DATA_SEED, DATA_STREAM, np.arange(rows, dtype=np.int64), k)
+    times = []
+    for it in range(args.warmup + args.steps):
+        t0 = time.perf_counter()
+        om = oracle.omega_f16(k, n, seed=OMEGA_SEED)
+        oracle.gemm_y32(A, om)
+        dt = time.perf_counter() - t0
+        if it >= args.warmup:
+            times.append(dt)
+    t = statistics.mean(times)
+    val = 2.0 * rows * k * n / t / 1e12
+    cores = oracle.num_threads()
+    line = {"impl": "reference", "metric": METRIC, "value": val, "unit": "TFLOP/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": cfg_name, "description": desc, "m": m, "k": k, "n": n,
+                       "sample_rows_per_step": rows},
+            "cpu_baseline": {"value": val, "unit": "TFLOP/s", "cores": cores, "kind": "oracle",
+                             "sample": f"{rows} rows of A per step + Omega generation, naive FP32 fmaf GEMM"},
+            "e2e": {"value": val, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="shgemm", choices=["shgemm", "reference"])
+    ap.add_argument("--config", default="cfg4", choices=sorted(CONFIGS))
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(3, args.warmup)
+
+    if args.impl == "reference":
+        run_reference(args, args.config)
+        return
+
+    import torch
+    import paper_2304_04612_b200 as shg
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    m_total, k, n, desc = CONFIGS[args.config]
+    # row sharding: rank g owns rows [g*ceil(m/G), min(m, (g+1)*ceil(m/G)))
+    per = (m_total + world - 1) // world
+    row0 = rank * per
+    m = max(0, min(m_total, row0 + per) - row0)
+
+    A = shg.synth("gauss", DATA_SEED, DATA_STREAM, m, k, row0=row0)          # resident input
+    Y = torch.empty((m, n), dtype=torch.float32, device="cuda")
+    ldo = (k + 7) // 8 * 8
+    om_buf = torch.empty((n, ldo), dtype=torch.float16, device="cuda")
+    Om = om_buf[:, :k].t()
+    stream = torch.cuda.current_stream()
+    L = shg.lib()
+    import ctypes
+    sp = ctypes.c_void_p(stream.cuda_stream)
+
+    def gen():
+        shg._check(L.gen_omega_f16(k, n, OMEGA_SEED, 0, shg._p(om_buf), ldo, sp), "gen_omega_f16")
+
+    def gemm():
+        shg._check(L.shgemm(m, n, k, shg._p(A), k, shg._p(om_buf), ldo, shg._p(Y), n, sp), "shgemm")
+
+    def step():
+        gen()
+        gemm()
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    # per-launch events for the dominant kernel (shgemm) and the Omega generator, on the launch stream
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
+    clocks = ClockSampler(local)
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clocks.start()
+    time.sleep(0.3)
+    launches0 = shg.launch_count()
+    t_start = torch.cuda.Event(enable_timing=True)
+    t_end = torch.cuda.Event(enable_timing=True)
+    t_start.record(stream)
+    for i in range(args.steps):
+        ev[i][0].record(stream)
+        gen()
+        ev[i][1].record(stream)
+        gemm()
+        ev[i][2].record(stream)
+    t_end.record(stream)
+    torch.cuda.synchronize()
+    launches = shg.launch_count() - launches0
+    if dist:
+        dist.barrier()
+    clk = clocks.stop()
+    total_ms = t_start.elapsed_time(t_end)
+    gemm_ms = statistics.mean(ev[i][1].elapsed_time(ev[i][2]) for i in range(args.steps))
+    gen_ms = statistics.mean(ev[i][0].elapsed_time(ev[i][1]) for i in range(args.steps))
+    if dist:
+        t = torch.tensor([total_ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+    ms_per_step = total_ms / args.steps
+    flops_total = 2.0 * m_total * k * n
+    value = flops_total / (ms_per_step * 1e-3) / 1e12
+
+    hbm, tc16, tc16_sus, peak_src = load_peaks()
+    alg_bytes = 4.0 * m * k + 2.0 * k * n + 4.0 * m * n        # per launch, this rank
+    achieved_gbs = alg_bytes / (gemm_ms * 1e-3) / 1e9
+    ai = 2.0 * m * k * n / alg_bytes
+    tc_ceiling = tc16 / 2.0                                     # two MMAs per product
+    bound = "hbm" if ai * hbm / 1e3 < tc_ceiling else "tensor"
+    if bound == "hbm":
+        roof = {"bound": "hbm", "achieved": achieved_gbs, "peak": hbm, "unit": "GB/s", "frac": achieved_gbs / hbm}
+    else:
+        # tensor pipe executes 4mnk flops (hi and lo MMAs); peak = measured dense fp16 (= bf16 rate)
+        tc_ach = 4.0 * m * k * n / (gemm_ms * 1e-3) / 1e12
+        roof = {"bound": "tensor", "achieved": tc_ach, "peak": tc16, "unit": "TFLOP/s", "frac": tc_ach / tc16}
+    roof["traffic"] = ncu_traffic(args.config if world == 1 else f"{args.config}_g{world}")
+    roof["peak_source"] = peak_src
+    roof["kernel"] = "shgemm_sm100_kernel"
+    roof["kernel_ms"] = gemm_ms
+    roof["roofline_frac_of_min(tc/2, AI*hbm)"] = (2.0 * m * k * n / (gemm_ms * 1e-3) / 1e12) / min(tc_ceiling, ai * hbm / 1e3)
+
+    out = None
+    if rank == 0:
+        e2e = None
+        if not args.no_e2e:
+            e2e = measure_e2e(shg, torch, k, n, steps=3)
+        cpu = None
+        if not args.no_cpu_baseline and world == 1:
+            cpu = cpu_baseline(m_total, k, n)
+        out = {"metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps,
+               "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
+               "vs_baseline": None, "dtype": "f16*f16->f32 (FP32 A split to FP16 hi/lo in-kernel)",
+               "data": "synthetic",
+               "config": {"workload": args.config, "description": desc, "m": m_total, "k": k, "n": n,
+                          "rows_per_gpu": per, "parallelism": f"row-shard x{world} (no collective on the data path)",
+                          "l2": "inputs larger than L2 (A is %.1f GiB per GPU), no flush" % (4.0 * m * k / 2 ** 30),
+                          "plan": shg.plan(m, n, k)},
+               "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
+               "clocks": clk, "omega_gen_ms": gen_ms, "shgemm_ms": gemm_ms,
+               "gbs_algorithmic": achieved_gbs}
+        print(json.dumps(out), flush=True)
+    if dist:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def measure_e2e(shg, torch, k, n, steps=3):
+    """Same metric through the C ABI with HOST buffers: each step copies a row sample of A from
+    pinned host memory to the device, projects it (shgemm_host streams overlapped chunks) and
+    copies Y back; host<->device copies are inside the timed region."""
+    rows = 262144 if k <= 4096 else max(128, (1 << 30) // (4 * k))
+    A_h = shg.synth("gauss", DATA_SEED, DATA_STREAM, rows, k).cpu().pin_memory()
+    Y_h = torch.empty((rows, n), dtype=torch.float32).pin_memory()
+    ws = torch.empty(shg.host_workspace_size(n, k), dtype=torch.uint8, device="cuda")
+
+    def step():
+        Om = shg.gen_omega(k, n, seed=OMEGA_SEED)
+        shg.shgemm_host(A_h, Om, Y_h, workspace=ws)
+
+    for _ in range(2):
+        step()
+    torch.cuda.synchronize()
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s.record()
+    for _ in range(steps):
+        step()
+    e.record()
+    torch.cuda.synchronize()
+    dt = s.elapsed_time(e) / 1e3 / steps
+    return {"value": 2.0 * rows * k * n / dt / 1e12, "unit": "TFLOP/s", "h2d_bytes_per_step": rows * k * 4,
+            "d2h_bytes_per_step": rows * n * 4, "rows_per_step": rows, "ms_per_step": dt * 1e3,
+            "api": "shgemm_host (C ABI, pinned host A/Y, overlapped chunk streaming)"}
+
+
+if __name__ == "__main__":
+    main()

@@ -66,6 +66,13 @@ typedef struct {
     int32_t split_k;     /* number of k splits; 0 = heuristic, 1 = none */
     int32_t max_ctas;    /* persistent grid size cap; 0 = number of SMs */
     int32_t force_simt;  /* 1 = force the CUDA-core fallback (tests) */
+    /* Diagnostics only (results are WRONG when debug_flags != 0): bit0 skip the TMEM->register
+     * promotion loads, bit1 skip the splitter arithmetic, bit2 skip the MMAs. */
+    int32_t debug_flags;
+    int32_t reserved;
+    /* Diagnostics: device int64[grid * 16] per-CTA wait-cycle counters (layout in
+     * csrc/shgemm_sm100.cuh, enum ProfSlot), or NULL. */
+    int64_t *prof;
 } shg_tune_t;
 
 /* Plan the library would use for an (m, n, k) shgemm on the current device. */
@@ -129,6 +136,20 @@ shg_status_t project(const float *A, int ndim, const int64_t *dims, int mode, in
 size_t shg_project_workspace_size(int ndim, const int64_t *dims, int mode, int64_t n);
 
 /* ---------------------------------------------------------------------------------------------
+ * shgemm_host — Y = A . Omega with A and Y in HOST memory (pinned for overlap; pageable works but
+ * serialises), Omega on the device. A is streamed to the device in row chunks of `chunk_rows`
+ * (0 = heuristic) through two staging buffers: H2D copy of chunk c+1 and D2H copy of chunk c-1
+ * overlap the SHGEMM of chunk c on internal streams that are ordered after / before `stream`.
+ * workspace: device scratch >= shg_host_workspace_size(n, k, chunk_rows) bytes, or NULL
+ * (stream-ordered allocation). Returns when everything is enqueued; synchronize `stream`.
+ * ------------------------------------------------------------------------------------------- */
+shg_status_t shgemm_host(int64_t m, int64_t n, int64_t k, const float *A_host, int64_t lda,
+                         const uint16_t *Omega, int64_t ldo, float *Y_host, int64_t ldc, int64_t chunk_rows,
+                         void *workspace, size_t workspace_bytes, shg_stream_t stream);
+
+size_t shg_host_workspace_size(int64_t n, int64_t k, int64_t chunk_rows);
+
+/* ---------------------------------------------------------------------------------------------
  * Test / bench support (not part of the method).
  * ------------------------------------------------------------------------------------------- */
 /* Elementwise split of Eqs 14-15 with the SAME device function the mainloop uses:
@@ -162,6 +183,13 @@ const char *shg_version(void);
  *   nsteps 1..4 instructions; D_out device 128 x n FP32 row-major. */
 shg_status_t shg_probe_umma(const uint16_t *A, const uint16_t *B, int n, const float *D_init, int mode,
                             int nsteps, float *D_out, shg_stream_t stream);
+
+/* MMA-rate microbenchmark: `grid` CTAs each issue `iters` back-to-back
+ * 128 x n x 16 kind::f16 MMAs (A from TMEM if ts, else smem) while `lsu_warps` warps stream
+ * shared-memory loads/stores (lsu_warps bits 0-2) into (lsu_warps >> 3, min 1) rotating
+ * accumulators; out[cta] (device floats) = cycles per MMA. */
+shg_status_t shg_probe_mma_rate(int n, int iters, int ts, int lsu_warps, float *out, int grid,
+                                shg_stream_t stream);
 
 #ifdef __cplusplus
 }

@@ -35,7 +35,8 @@ class SHGError(RuntimeError):
 
 class Tune(ctypes.Structure):
     _fields_ = [("bn", ctypes.c_int32), ("split_k", ctypes.c_int32), ("max_ctas", ctypes.c_int32),
-                ("force_simt", ctypes.c_int32)]
+                ("force_simt", ctypes.c_int32), ("debug_flags", ctypes.c_int32), ("reserved", ctypes.c_int32),
+                ("prof", ctypes.c_void_p)]
 
 
 class Plan(ctypes.Structure):
@@ -65,6 +66,9 @@ def lib():
             L.project.argtypes = [vp, i32, vp, i32, i64, u64, i32, vp, i64, vp, sz, vp]
             L.shg_project_workspace_size.argtypes = [i32, vp, i32, i64]
             L.shg_project_workspace_size.restype = sz
+            L.shgemm_host.argtypes = [i64, i64, i64, vp, i64, vp, i64, vp, i64, i64, vp, sz, vp]
+            L.shg_host_workspace_size.argtypes = [i64, i64, i64]
+            L.shg_host_workspace_size.restype = sz
             L.shg_debug_split.argtypes = [vp, i64, vp, vp, vp]
             L.shg_synth_f32.argtypes = [i32, u64, u32, i64, i64, i64, vp, i64, vp]
             L.shg_launch_count.restype = u64
@@ -72,7 +76,9 @@ def lib():
             L.shg_device_supported.restype = i32
             L.shg_version.restype = ctypes.c_char_p
             L.shg_probe_umma.argtypes = [vp, vp, i32, vp, i32, i32, vp, vp]
-            for name in ("shgemm", "shgemm_ex", "shg_plan", "gen_omega_f16", "gen_omega_f16_ex", "project",
+            L.shg_probe_mma_rate.argtypes = [i32, i32, i32, i32, vp, i32, vp]
+            L.shg_probe_mma_rate.restype = i32
+            for name in ("shgemm", "shgemm_ex", "shgemm_host", "shg_plan", "gen_omega_f16", "gen_omega_f16_ex", "project",
                          "shg_debug_split", "shg_synth_f32", "shg_probe_umma"):
                 getattr(L, name).restype = i32
             _lib = L
@@ -160,6 +166,27 @@ def shgemm(A: torch.Tensor, Omega: torch.Tensor, out: torch.Tensor | None = None
     _check(lib().shgemm_ex(m, n, k, _p(A), lda, _p(Omega), ldo, _p(out), ldc, _tune(tune), _p(workspace),
                            ws_bytes, _p(nonfinite), _stream(stream)), "shgemm_ex")
     return out
+
+
+def shgemm_host(A_host: torch.Tensor, Omega: torch.Tensor, Y_host: torch.Tensor | None = None,
+                chunk_rows: int = 0, workspace: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+    """Y = A . Omega with A (m, k) float32 and Y (m, n) float32 in (pinned) host memory, Omega on the
+    device; A is streamed through the device in overlapped row chunks (include/shgemm.h)."""
+    m, k = A_host.shape
+    n = Omega.shape[1]
+    if A_host.device.type != "cpu" or Omega.device.type != "cuda":
+        raise ValueError("A_host must be a host tensor and Omega a device tensor")
+    if Y_host is None:
+        Y_host = torch.empty((m, n), dtype=torch.float32, pin_memory=True)
+    ws_bytes = 0 if workspace is None else workspace.numel() * workspace.element_size()
+    _check(lib().shgemm_host(m, n, k, _p(A_host), A_host.stride(0) if m > 1 else max(k, 1), _p(Omega),
+                             Omega.stride(1) if n > 1 else max(k, 1), _p(Y_host), Y_host.stride(0) if m > 1 else n,
+                             chunk_rows, _p(workspace), ws_bytes, _stream(stream)), "shgemm_host")
+    return Y_host
+
+
+def host_workspace_size(n: int, k: int, chunk_rows: int = 0) -> int:
+    return int(lib().shg_host_workspace_size(n, k, chunk_rows))
 
 
 def plan(m: int, n: int, k: int, tune=None) -> dict:

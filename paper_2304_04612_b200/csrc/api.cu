@@ -101,32 +101,24 @@ bool encode_b(CUtensorMap* map, const uint16_t* Om, int64_t k, int64_t n, int64_
 }
 
 // ------------------------------------------------------------------ planning
-constexpr int kBNs[] = {16, 32, 64, 96, 128, 144, 192, 256};
+constexpr int kBNs[] = {32, 64, 96, 128, 144, 160, 192, 224, 256};
 
-int smem_for_bn(int bn) {
-    switch (bn) {
-        case 16: return shg::Cfg<16>::kSmemBytes;
-        case 32: return shg::Cfg<32>::kSmemBytes;
-        case 64: return shg::Cfg<64>::kSmemBytes;
-        case 96: return shg::Cfg<96>::kSmemBytes;
-        case 128: return shg::Cfg<128>::kSmemBytes;
-        case 144: return shg::Cfg<144>::kSmemBytes;
-        case 192: return shg::Cfg<192>::kSmemBytes;
-        default: return shg::Cfg<256>::kSmemBytes;
+#define SHG_BN_SWITCH(bn, EXPR)                                  \
+    switch (bn) {                                                \
+        case 32: { constexpr int BN_ = 32; EXPR; }               \
+        case 64: { constexpr int BN_ = 64; EXPR; }               \
+        case 96: { constexpr int BN_ = 96; EXPR; }               \
+        case 128: { constexpr int BN_ = 128; EXPR; }             \
+        case 144: { constexpr int BN_ = 144; EXPR; }             \
+        case 160: { constexpr int BN_ = 160; EXPR; }             \
+        case 192: { constexpr int BN_ = 192; EXPR; }             \
+        case 224: { constexpr int BN_ = 224; EXPR; }             \
+        default: { constexpr int BN_ = 256; EXPR; }              \
     }
-}
-int sa_for_bn(int bn) {
-    switch (bn) {
-        case 16: return shg::Cfg<16>::SA;
-        case 32: return shg::Cfg<32>::SA;
-        case 64: return shg::Cfg<64>::SA;
-        case 96: return shg::Cfg<96>::SA;
-        case 128: return shg::Cfg<128>::SA;
-        case 144: return shg::Cfg<144>::SA;
-        case 192: return shg::Cfg<192>::SA;
-        default: return shg::Cfg<256>::SA;
-    }
-}
+
+int smem_for_bn(int bn) { SHG_BN_SWITCH(bn, return shg::Cfg<BN_>::kSmemBytes) }
+int sa_for_bn(int bn) { SHG_BN_SWITCH(bn, return shg::Cfg<BN_>::SA) }
+int sb_for_bn(int bn) { SHG_BN_SWITCH(bn, return shg::Cfg<BN_>::SO) }
 
 struct Plan {
     int path = 0;  // 0 tc, 1 simt, 2 trivial
@@ -199,17 +191,8 @@ shg_status_t launch_tc(const CUtensorMap& mapA, const CUtensorMap& mapB, const s
 
 shg_status_t dispatch_tc(int bn, const CUtensorMap& a, const CUtensorMap& b, const shg::KParams& kp, int grid,
                          cudaStream_t s) {
-    switch (bn) {
-        case 16: return launch_tc<16>(a, b, kp, grid, s);
-        case 32: return launch_tc<32>(a, b, kp, grid, s);
-        case 64: return launch_tc<64>(a, b, kp, grid, s);
-        case 96: return launch_tc<96>(a, b, kp, grid, s);
-        case 128: return launch_tc<128>(a, b, kp, grid, s);
-        case 144: return launch_tc<144>(a, b, kp, grid, s);
-        case 192: return launch_tc<192>(a, b, kp, grid, s);
-        case 256: return launch_tc<256>(a, b, kp, grid, s);
-        default: return SHG_ERR_INVALID_VALUE;
-    }
+    if (!valid_bn(bn)) return SHG_ERR_INVALID_VALUE;
+    SHG_BN_SWITCH(bn, return launch_tc<BN_>(a, b, kp, grid, s))
 }
 
 int grid_for(int64_t work, int threads) {
@@ -261,6 +244,8 @@ shg_status_t run_shgemm(int64_t m, int64_t n, int64_t k, const AView& av, const 
     kp.k_inner = av.S;
     kp.num_kb = pl.num_kb;
     kp.m_tiles = pl.m_tiles; kp.n_tiles = pl.n_tiles; kp.splits = pl.splits;
+    kp.dbg = tune ? static_cast<uint32_t>(tune->debug_flags) : 0u;
+    kp.prof = tune ? reinterpret_cast<long long*>(tune->prof) : nullptr;
     void* own_ws = nullptr;
     if (pl.splits > 1) {
         float* wsf = nullptr;
@@ -304,6 +289,59 @@ uint32_t sparse_threshold(int dist, int64_t k_total) {
         return static_cast<uint32_t>(t);
     }
     return 0u;
+}
+
+
+// ------------------------------------------------------------------ host-streaming support
+struct HostStreams {
+    cudaStream_t s[2] = {nullptr, nullptr};
+    cudaEvent_t ev_start = nullptr, ev_done[2] = {nullptr, nullptr};
+    bool ok = false;
+};
+
+HostStreams& host_streams() {
+    static HostStreams hs[64];
+    static std::once_flag flags[64];
+    int dev = 0;
+    cudaGetDevice(&dev);
+    dev = std::min(std::max(dev, 0), 63);
+    std::call_once(flags[dev], [dev]() {
+        HostStreams& h = hs[dev];
+        bool ok = true;
+        for (int i = 0; i < 2; ++i) {
+            ok &= cudaStreamCreateWithFlags(&h.s[i], cudaStreamNonBlocking) == cudaSuccess;
+            ok &= cudaEventCreateWithFlags(&h.ev_done[i], cudaEventDisableTiming) == cudaSuccess;
+        }
+        ok &= cudaEventCreateWithFlags(&h.ev_start, cudaEventDisableTiming) == cudaSuccess;
+        h.ok = ok;
+    });
+    return hs[dev];
+}
+
+int64_t host_chunk_rows(int64_t m, int64_t k, int64_t chunk_rows) {
+    int64_t r = chunk_rows > 0 ? chunk_rows : (int64_t(256) << 20) / (std::max<int64_t>(k, 1) * 4);
+    r = std::max<int64_t>(128, (r + 127) / 128 * 128);
+    if (m > 0) r = std::min(r, (m + 127) / 128 * 128);
+    return r;
+}
+
+struct HostWs {
+    int64_t chunk, lda_s, ldy_s;
+    size_t a_bytes, y_bytes, sk_bytes, total;
+};
+
+HostWs host_ws(int64_t m, int64_t n, int64_t k, int64_t chunk_rows) {
+    HostWs w{};
+    w.chunk = host_chunk_rows(m, k, chunk_rows);
+    w.lda_s = (k + 3) / 4 * 4;
+    w.ldy_s = (n + 3) / 4 * 4;
+    auto up = [](size_t b) { return (b + 255) / 256 * 256; };
+    w.a_bytes = up(static_cast<size_t>(w.chunk * w.lda_s * 4));
+    w.y_bytes = up(static_cast<size_t>(w.chunk * w.ldy_s * 4));
+    const Plan pl = make_plan(w.chunk, n, k, true, nullptr, std::max(1, dev_info().sms));
+    w.sk_bytes = up(static_cast<size_t>(pl.ws_bytes));
+    w.total = 2 * (w.a_bytes + w.y_bytes + w.sk_bytes);
+    return w;
 }
 
 }  // namespace
@@ -365,7 +403,7 @@ shg_status_t shg_plan(int64_t m, int64_t n, int64_t k, const shg_tune_t* tune, s
     out->grid = pl.grid;
     if (pl.path == 0) {
         out->stages_a = sa_for_bn(pl.bn);
-        out->stages_b = 2;
+        out->stages_b = sb_for_bn(pl.bn);
         out->smem_bytes = smem_for_bn(pl.bn);
         out->kernels = pl.splits > 1 ? 2 : 1;
     } else {
@@ -456,6 +494,61 @@ shg_status_t project(const float* A, int ndim, const int64_t* dims, int mode, in
         if (st == SHG_OK && e != cudaSuccess) return cuda_fail(e, "cudaFreeAsync");
     }
     return st;
+}
+
+size_t shg_host_workspace_size(int64_t n, int64_t k, int64_t chunk_rows) {
+    if (n <= 0 || k <= 0) return 0;
+    return host_ws(0, n, k, chunk_rows).total;
+}
+
+shg_status_t shgemm_host(int64_t m, int64_t n, int64_t k, const float* A_host, int64_t lda, const uint16_t* Omega,
+                         int64_t ldo, float* Y_host, int64_t ldc, int64_t chunk_rows, void* workspace,
+                         size_t workspace_bytes, shg_stream_t stream) {
+    if (m < 0 || n < 0 || k < 0 || chunk_rows < 0) return SHG_ERR_INVALID_VALUE;
+    if (m == 0 || n == 0) return SHG_OK;
+    if (!Y_host || ldc < n || (k > 0 && (!A_host || !Omega || lda < k || ldo < k))) return SHG_ERR_INVALID_VALUE;
+    cudaStream_t us = reinterpret_cast<cudaStream_t>(stream);
+    if (k == 0) {
+        for (int64_t i = 0; i < m; ++i) std::memset(Y_host + i * ldc, 0, n * sizeof(float));
+        return SHG_OK;
+    }
+    HostStreams& hs = host_streams();
+    if (!hs.ok) return cuda_fail(cudaErrorUnknown, "stream/event creation");
+    const HostWs w = host_ws(m, n, k, chunk_rows);
+    void* own = nullptr;
+    uint8_t* ws = static_cast<uint8_t*>(workspace);
+    if (!ws) {
+        SHG_CUDA(cudaMallocAsync(&own, w.total, us));
+        ws = static_cast<uint8_t*>(own);
+    } else if (workspace_bytes < w.total) {
+        return SHG_ERR_WORKSPACE;
+    }
+    SHG_CUDA(cudaEventRecord(hs.ev_start, us));
+    for (int b = 0; b < 2; ++b) SHG_CUDA(cudaStreamWaitEvent(hs.s[b], hs.ev_start, 0));
+    const int64_t nchunks = (m + w.chunk - 1) / w.chunk;
+    for (int64_t c = 0; c < nchunks; ++c) {
+        const int b = static_cast<int>(c & 1);
+        cudaStream_t s = hs.s[b];
+        uint8_t* base = ws + b * (w.a_bytes + w.y_bytes + w.sk_bytes);
+        float* As = reinterpret_cast<float*>(base);
+        float* Ys = reinterpret_cast<float*>(base + w.a_bytes);
+        void* sk = w.sk_bytes ? base + w.a_bytes + w.y_bytes : nullptr;
+        const int64_t r0 = c * w.chunk;
+        const int64_t rows = std::min(w.chunk, m - r0);
+        SHG_CUDA(cudaMemcpy2DAsync(As, w.lda_s * 4, A_host + r0 * lda, lda * 4, k * 4, rows,
+                                   cudaMemcpyHostToDevice, s));
+        shg_status_t st = shgemm_ex(rows, n, k, As, w.lda_s, Omega, ldo, Ys, w.ldy_s, nullptr, sk, w.sk_bytes,
+                                    nullptr, reinterpret_cast<shg_stream_t>(s));
+        if (st != SHG_OK) return st;
+        SHG_CUDA(cudaMemcpy2DAsync(Y_host + r0 * ldc, ldc * 4, Ys, w.ldy_s * 4, n * 4, rows,
+                                   cudaMemcpyDeviceToHost, s));
+    }
+    for (int b = 0; b < 2; ++b) {
+        SHG_CUDA(cudaEventRecord(hs.ev_done[b], hs.s[b]));
+        SHG_CUDA(cudaStreamWaitEvent(us, hs.ev_done[b], 0));
+    }
+    if (own) SHG_CUDA(cudaFreeAsync(own, us));
+    return SHG_OK;
 }
 
 shg_status_t shg_debug_split(const float* a, int64_t count, uint16_t* hi, uint16_t* lo, shg_stream_t stream) {

@@ -101,3 +101,88 @@ extern "C" shg_status_t shg_probe_umma(const uint16_t* A, const uint16_t* B, int
     e = cudaGetLastError();
     return e == cudaSuccess ? SHG_OK : SHG_ERR_CUDA;
 }
+
+// ------------------------------------------------------------------ MMA throughput microbenchmark
+// Every CTA (1 per SM) issues `iters` tcgen05.mma.cta_group::1.kind::f16 128 x n x 16 back to back
+// on resident operands (A from TMEM when ts != 0, else from smem; B from smem) into a TMEM
+// accumulator, optionally while `lsu_warps` other warps stream LDS.128/STS.128 over a 64 KB smem
+// region (to emulate the splitter's shared-memory traffic). out[blockIdx.x] = cycles / MMA.
+namespace shg {
+__global__ void __launch_bounds__(256, 1)
+probe_mma_rate_kernel(int n, int iters, int ts, int lsu_warps, float* out, int nacc) {
+    extern __shared__ uint8_t smem_raw[];
+    const uint32_t raw_addr = smem_u32(smem_raw);
+    uint8_t* base = smem_raw + ((1024u - (raw_addr & 1023u)) & 1023u);
+    uint8_t* sA = base;                  // 128 rows x 128 B
+    uint8_t* sB = base + 16384;          // 256 rows x 128 B
+    uint8_t* scratch = base + 16384 + 32768;   // 64 KB for LSU traffic
+    uint64_t* bar = reinterpret_cast<uint64_t*>(scratch + 65536);
+    uint32_t* tslot = reinterpret_cast<uint32_t*>(bar + 1);
+    volatile uint32_t* stop = tslot + 1;
+    const uint32_t warp = warp_id();
+    for (int i = threadIdx.x; i < (16384 + 32768 + 65536) / 16; i += blockDim.x)
+        reinterpret_cast<uint4*>(base)[i] = make_uint4(0x3C003C00u, 0x3C003C00u, 0, 0);
+    fence_proxy_async_smem();
+    if (threadIdx.x == 0) { mbar_init(bar, 1); fence_mbar_init(); *stop = 0; }
+    if (warp == 0) tmem_alloc<512>(tslot);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tbase = *tslot;
+    if (warp == 0) {
+        if (elect_one()) {
+            const uint32_t idesc = idesc_f16_f32(128, static_cast<uint32_t>(n));
+            const uint64_t ad = sw128_kmajor_desc(smem_u32(sA));
+            const uint64_t bd = sw128_kmajor_desc(smem_u32(sB));
+            const long long t0 = clock64();
+            for (int i = 0; i < iters; ++i) {
+                const uint32_t j = static_cast<uint32_t>(i & 3);
+                const uint32_t d = tbase + static_cast<uint32_t>((i % nacc) * n);
+                if (ts) {
+                    asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, 1, 0;\n\t"
+                                 "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}\n"
+                                 ::"r"(d), "r"(tbase + 448 + 8 * j), "l"(bd + 2 * j), "r"(idesc) : "memory");
+                } else {
+                    mma_f16_ss(d, ad + 2 * j, bd + 2 * j, idesc, 1u);
+                }
+            }
+            tc_commit(bar);
+            mbar_wait(bar, 0);
+            const long long t1 = clock64();
+            out[blockIdx.x] = static_cast<float>(t1 - t0) / static_cast<float>(iters);
+            *stop = 1;
+        }
+        __syncwarp();
+    } else if (static_cast<int>(warp) <= lsu_warps) {
+        // stream LDS.128 + STS.128 over the scratch region until the MMA warp finishes
+        const int t = threadIdx.x - 32;
+        uint4 acc = make_uint4(0, 0, 0, 0);
+        while (*stop == 0) {
+#pragma unroll 4
+            for (int i = 0; i < 16; ++i) {
+                const int idx = ((i * 224 + t) % 4096);
+                uint4 v = reinterpret_cast<const uint4*>(scratch)[idx];
+                acc.x ^= v.x; acc.y += v.y;
+                reinterpret_cast<uint4*>(scratch)[(idx + 2048) % 4096] = acc;
+            }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 0) { tc_fence_after(); tmem_dealloc<512>(tbase); }
+}
+}  // namespace shg
+
+extern "C" shg_status_t shg_probe_mma_rate(int n, int iters, int ts, int lsu_warps, float* out, int grid,
+                                           shg_stream_t stream) {
+    // lsu_warps >= 8 encodes the number of independent accumulators: nacc = lsu_warps >> 3
+    const int nacc = lsu_warps >= 8 ? (lsu_warps >> 3) : 1;
+    lsu_warps &= 7;
+    if (!out || n < 16 || n > 256 || (n % 16) || iters < 1 || grid < 1 || nacc * n > 448)
+        return SHG_ERR_INVALID_VALUE;
+    const int smem = 1024 + 16384 + 32768 + 65536 + 64;
+    cudaError_t e = cudaFuncSetAttribute(shg::probe_mma_rate_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return SHG_ERR_CUDA;
+    shg::probe_mma_rate_kernel<<<grid, 256, smem, reinterpret_cast<cudaStream_t>(stream)>>>(n, iters, ts, lsu_warps, out, nacc);
+    return cudaGetLastError() == cudaSuccess ? SHG_OK : SHG_ERR_CUDA;
+}

@@ -6,38 +6,46 @@
 // The A100 design (WMMA, RN add after every f_k = 8 mma) is prior art, not the
 // blueprint; this kernel re-derives it for tcgen05:
 //
-//  * A stager   : TMA (3-D map, SWIZZLE_128B) streams 128 x 64 FP32 tiles into an SA-deep ring.
-//  * Splitter   : 4 warps read the FP32 tile from smem, apply split2 (Eqs 14-15) and write hi and
-//                 lo in the UMMA K-major SW128 layout into an SB-deep ring (+ fence.proxy.async).
-//  * Omega      : TMA streams the 64 x BN FP16 tile (K-major) into the same SB ring slot.
-//  * MMA        : one thread issues, per 64-k stage, 4 lo MMAs (D := lo.Omega) and 4 hi MMAs, the
-//                 first with scale-input-d = 11 (D := hi.Omega + D * 2^-11) — so D holds the
-//                 stage's hi.Omega + 2^-11 lo.Omega (Eq 16) in an FP32 TMEM accumulator.
-//                 Two D buffers (2 x BN TMEM columns) alternate between stages.
-//  * Promotion  : 8 epilogue warps tcgen05.ld each finished D and add it with RN (add.rn.f32)
-//                 into a register accumulator: the RZ-avoidance of PAPER.md:587 applied per
-//                 K_c = 64 chunk instead of per A100 mma (and to lo too: reading c4-2).
-//  * Epilogue   : after the last stage, the RN accumulator is written to Y (row-major) with
+//  * A stager   : TMA (3-D map, SWIZZLE_128B) streams 128 x 64 FP32 tiles into an SA-deep smem ring.
+//  * Splitter   : 8 warps (2 per TMEM lane quarter, one per 32-k half) read their rows of the FP32
+//                 tile (conflict-free LDS.128 through the swizzle), apply split2 (Eqs 14-15) with
+//                 packed f32x2 arithmetic, and write hi and lo straight into TENSOR MEMORY with
+//                 tcgen05.st — the MMA takes A from TMEM, so hi/lo never touch shared memory
+//                 (measured: smem bandwidth was the bound with an smem A operand).
+//  * Omega      : TMA streams the 64 x BN FP16 tile (K-major SW128) into an SB-deep smem ring.
+//  * MMA        : one thread issues, per 64-k stage and per N-half (H0 + H1 = BN columns),
+//                 4 lo MMAs (D := lo.Omega) then 4 hi MMAs, the first with scale-input-d = 11
+//                 (D := hi.Omega + D * 2^-11), so D holds hi.Omega + 2^-11 lo.Omega (Eq 16) for
+//                 the stage. D half-accumulators rotate through NSLOT TMEM slots.
+//  * Promotion  : 8 epilogue warps (4 lane quarters x 2 N-halves) tcgen05.ld each finished D and
+//                 add it with RN (add.rn.f32x2) into register accumulators: the RZ-avoidance of
+//                 PAPER.md:587 applied per K_c = 64 chunk (and to lo as well: reading c4-2).
+//  * Epilogue   : after the last stage, the RN accumulators are written to Y (row-major) with
 //                 128-bit stores, masked on ragged edges; split-K tiles write to a workspace
 //                 plane that splitk_reduce_kernel sums in fixed order.
 //
 // One CTA per SM (smem-bound), persistent over tiles (m-block, k-split, n-block), n fastest.
 #pragma once
 #include <cstdint>
+#include <cstdio>
 #include <cuda.h>
 #include "ptx.cuh"
 #include "split.cuh"
 
 namespace shg {
 
-constexpr int kBM = 128;                 // UMMA M (cta_group::1)
-constexpr int kBK = 64;                  // k per stage: one 128-B swizzle row of FP16
-constexpr int kA32StageBytes = kBM * kBK * 4;   // 32 KB (two 16 KB TMA boxes of 32 FP32 columns)
-constexpr int kHLStageBytes = kBM * kBK * 2 * 2; // hi 16 KB + lo 16 KB
-constexpr int kThreads = 512;
-constexpr int kWarpProdA = 4, kWarpMMA = 5, kWarpProdB = 6;
-constexpr int kEpiWarp0 = 8;
-constexpr int kSmemLimit = 232448;       // max dynamic smem per block on sm_100
+constexpr int kBM = 128;                          // UMMA M (cta_group::1)
+constexpr int kBK = 64;                           // k per stage: one 128-B swizzle row of FP16
+constexpr int kA32StageBytes = kBM * kBK * 4;     // 32 KB (two 16 KB TMA boxes of 32 FP32 columns)
+constexpr int kNumSplitWarps = 8;                 // warps 0..7
+constexpr int kEpiWarp0 = 8;                      // warps 8..15
+constexpr int kWarpProdA = 16, kWarpMMA = 17, kWarpProdB = 18;   // warp 19 idle
+constexpr int kThreads = 640;
+// Register budget: setmaxnreg moves registers inside the CTA's own pool (640 threads x 96 = 61440):
+// splitter 256 x 56 + epilogue 256 x 168 + control 128 x 32 = 61440.
+constexpr int kSmemLimit = 232448;                // max dynamic smem per block on sm_100
+constexpr int kTmemCols = 512;
+constexpr int kAStageCols = 64;                   // hi 32 + lo 32 columns (2 FP16 per 32-bit column)
 
 struct KParams {
     int64_t m, n, k;
@@ -49,25 +57,64 @@ struct KParams {
     int64_t split_stride;   // elements between split planes (workspace)
     int32_t vec_store;      // out rows 16-B aligned and ldo_out % 4 == 0
     int* nonfinite;         // optional flag (set to 1 on any non-finite output)
+    uint32_t dbg;           // diagnostics: bit0 skip promotion loads, bit1 skip split math, bit2 skip MMAs
+    long long* prof;        // diagnostics: per-CTA wait-cycle counters [gridDim.x][16] (ProfSlot)
 };
 
-__host__ __device__ constexpr uint32_t tmem_cols_for(uint32_t cols) {
-    return cols <= 32 ? 32 : cols <= 64 ? 64 : cols <= 128 ? 128 : cols <= 256 ? 256 : 512;
+// Per-CTA diagnostic counters (cycles unless noted), written only when KParams::prof != nullptr.
+enum ProfSlot {
+    kProfTotal = 0, kProfMmaAccEmpty, kProfMmaHlFull, kProfMmaOmFull, kProfSplitAFull, kProfSplitBEmpty,
+    kProfEpiAccFull, kProfProdAEmpty, kProfProdBEmpty, kProfSplitBusy, kProfEpiStore, kProfStages, kProfSlots = 16
+};
+
+// Every pipeline wait is bounded: a wait that spins ~2^22 times (seconds) traps, so a deadlock
+// becomes a launch error instead of a hung GPU. Building with -DSHG_WATCHDOG_PRINT also reports
+// which barrier (smem offset), parity, CTA and warp stalled (a printf call costs registers).
+__device__ __forceinline__ void watchdog_report(uint64_t* bar, uint32_t parity) {
+#ifdef SHG_WATCHDOG_PRINT
+    printf("shgemm watchdog: block %d warp %d lane %d stuck on mbarrier smem+0x%x parity %u\n", blockIdx.x,
+           threadIdx.x / 32, threadIdx.x % 32, smem_u32(bar), parity);
+#else
+    (void)bar;
+    (void)parity;
+#endif
+    asm volatile("trap;");
+}
+
+__device__ __forceinline__ void mbar_wait_prof(uint64_t* bar, uint32_t parity, long long& acc) {
+    const long long t0 = clock64();
+    uint32_t spins = 0;
+    while (!mbar_try_wait(bar, parity)) {
+        if (++spins == (1u << 22)) watchdog_report(bar, parity);
+    }
+    acc += clock64() - t0;
 }
 
 template <int BN>
 struct Cfg {
+    // K_c = 128: one promotion chunk = 2 stages of 64 k. TMEM: 4 A stages (2 chunks of hi/lo,
+    // 64 columns each) + accumulator slots; N is covered by 2 part-MMAs of widths H0 + H1 = BN so
+    // that the drain of one part overlaps the MMAs of the other.
+    static constexpr int KC = 2;                           // stages per promotion chunk
+    static constexpr int NCH = 2;                          // chunk slots (TMEM A + Omega smem)
+    static constexpr int NQ = 2;
+    static constexpr int W = ((BN / 2) + 15) / 16 * 16;    // H0
+    static constexpr int WLAST = BN - W;                   // H1
+    static constexpr int NPH = 1;                          // parts per epilogue group
+    static constexpr int SB = NCH * KC;                    // TMEM A stage slots
+    static constexpr int ABASE = kTmemCols - SB * kAStageCols;
+    static constexpr int NSLOT_fit = ABASE / W;
+    static constexpr int NSLOT = NSLOT_fit > 4 ? 4 : NSLOT_fit;
+    static constexpr int SO = NCH * KC;                    // Omega smem stages
     static constexpr int kOmStageBytes = BN * kBK * 2;
-    static constexpr int SB = 2;
-    static constexpr int kBarBytes = 256;
-    static constexpr int SA_fit = (kSmemLimit - 1024 - kBarBytes - SB * (kHLStageBytes + kOmStageBytes)) / kA32StageBytes;
-    static constexpr int SA = SA_fit > 4 ? 4 : SA_fit;
-    static constexpr int kSmemBytes = 1024 + SA * kA32StageBytes + SB * (kHLStageBytes + kOmStageBytes) + kBarBytes;
-    static constexpr uint32_t kTmemCols = tmem_cols_for(2 * BN);
-    static constexpr int C = BN / 2;     // accumulator columns per epilogue thread
-    static_assert(BN % 16 == 0 && BN >= 16 && BN <= 256, "UMMA N for M=128");
-    static_assert(SA >= 2, "smem");
-    static_assert(kSmemBytes <= kSmemLimit, "smem");
+    static constexpr int kBarBytes = 512;
+    static constexpr int SA_fit = (kSmemLimit - 1024 - kBarBytes - SO * kOmStageBytes) / kA32StageBytes;
+    static constexpr int SA = SA_fit > 6 ? 6 : SA_fit;
+    static constexpr int kSmemBytes = 1024 + SA * kA32StageBytes + SO * kOmStageBytes + kBarBytes;
+    static_assert(BN % 16 == 0 && BN >= 32 && BN <= 256, "BN");
+    static_assert(WLAST >= 16 && WLAST % 16 == 0 && W <= 128, "UMMA N parts for M=128");
+    static_assert(NSLOT >= NQ, "TMEM accumulator slots");
+    static_assert(SA >= 2 && kSmemBytes <= kSmemLimit, "smem");
 };
 
 __device__ __forceinline__ void tile_coords(int tile, const KParams& p, int& m_blk, int& s, int& n_blk) {
@@ -87,7 +134,42 @@ __device__ __forceinline__ void advance(uint32_t& stage, uint32_t& phase, uint32
     if (++stage == n) { stage = 0; phase ^= 1u; }
 }
 
-template <int BN>
+// D[tmem] (+)= A[tmem] * B[smem]  (A operand from tensor memory, "TS" form)
+__device__ __forceinline__ void mma_f16_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t bdesc, uint32_t idesc,
+                                           uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}\n"
+        ::"r"(tmem_d), "r"(tmem_a), "l"(bdesc), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+
+// D[tmem] = A[tmem] * B[smem] + D * 2^-11  (scale-input-d = 11, sm_100a)
+__device__ __forceinline__ void mma_f16_ts_scale11(uint32_t tmem_d, uint32_t tmem_a, uint64_t bdesc, uint32_t idesc) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, 1, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p, 11;\n\t}\n"
+        ::"r"(tmem_d), "r"(tmem_a), "l"(bdesc), "r"(idesc)
+        : "memory");
+}
+
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&r)[16]) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], "
+        "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};"
+        ::"r"(taddr), "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]),
+          "r"(r[8]), "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15])
+        : "memory");
+}
+
+__device__ __forceinline__ void tmem_st8(uint32_t taddr, const uint32_t (&r)[8]) {
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};"
+                 ::"r"(taddr), "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7])
+                 : "memory");
+}
+
 __device__ __forceinline__ void tmem_ld8(uint32_t taddr, float (&v)[8]) {
     uint32_t r[8];
     asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
@@ -97,108 +179,241 @@ __device__ __forceinline__ void tmem_ld8(uint32_t taddr, float (&v)[8]) {
     for (int i = 0; i < 8; ++i) v[i] = __uint_as_float(r[i]);
 }
 
+// (a, b) += (c, d) with one add.rn.f32x2 (IEEE RN per lane; FADD2 on sm_100)
+__device__ __forceinline__ void add2_rn(float& a, float& b, float c, float d) {
+    asm("{\n\t.reg .b64 x, y;\n\t"
+        "mov.b64 x, {%0, %1};\n\t"
+        "mov.b64 y, {%2, %3};\n\t"
+        "add.rn.f32x2 x, x, y;\n\t"
+        "mov.b64 {%0, %1}, x;\n\t}\n"
+        : "+f"(a), "+f"(b)
+        : "f"(c), "f"(d));
+}
+
+// RN promotion adds: packed add.rn.f32x2 (FADD2) by default; -DSHG_EPI_SCALAR for add.rn.f32.
+#ifdef SHG_EPI_SCALAR
+#define ADD_PAIR(a, b, c, d) do { (a) = __fadd_rn((a), (c)); (b) = __fadd_rn((b), (d)); } while (0)
+#else
+#define ADD_PAIR(a, b, c, d) add2_rn((a), (b), (c), (d))
+#endif
+
 template <int BN>
 __global__ void __launch_bounds__(kThreads, 1)
 shgemm_sm100_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
                     const KParams p) {
     using CF = Cfg<BN>;
-    constexpr int SA = CF::SA, SB = CF::SB, C = CF::C;
+    constexpr int SA = CF::SA, SB = CF::SB, SO = CF::SO, NQ = CF::NQ, W = CF::W, WLAST = CF::WLAST;
+    constexpr int NPH = CF::NPH, NSLOT = CF::NSLOT, ABASE = CF::ABASE;
     constexpr int kOm = CF::kOmStageBytes;
 
     extern __shared__ uint8_t smem_raw[];
     const uint32_t raw_addr = smem_u32(smem_raw);
     uint8_t* base = smem_raw + ((1024u - (raw_addr & 1023u)) & 1023u);
     uint8_t* a32 = base;
-    uint8_t* hl = a32 + SA * kA32StageBytes;
-    uint8_t* om = hl + SB * kHLStageBytes;
-    uint64_t* bars = reinterpret_cast<uint64_t*>(om + SB * kOm);
-    uint64_t* a_full = bars;
-    uint64_t* a_empty = a_full + SA;
-    uint64_t* hl_full = a_empty + SA;
-    uint64_t* om_full = hl_full + SB;
-    uint64_t* b_empty = om_full + SB;
-    uint64_t* acc_full = b_empty + SB;
-    uint64_t* acc_empty = acc_full + 2;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
+    uint8_t* om = a32 + SA * kA32StageBytes;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(om + SO * kOm);
+    constexpr int NCH = CF::NCH, KC = CF::KC;
+    uint64_t* a_full = bars;                 // TMA A landed                        (count 1 + tx)
+    uint64_t* a_empty = a_full + SA;         // splitters done reading              (count 8)
+    uint64_t* ch_ready = a_empty + SA;       // chunk hi/lo in TMEM + Omega in smem (count 8 + 1 + tx)
+    uint64_t* ch_empty = ch_ready + NCH;     // MMAs done with the chunk slot       (tcgen05.commit)
+    uint64_t* acc_full = ch_empty + NCH;     // D slot complete                     (tcgen05.commit)
+    uint64_t* acc_empty = acc_full + NSLOT;  // D slot drained               (count 4)
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + NSLOT);
 
     const uint32_t warp = warp_id();
     const uint32_t lane = threadIdx.x & 31u;
 
     if (threadIdx.x == 0) {
-        for (int i = 0; i < SA; ++i) { mbar_init(&a_full[i], 1); mbar_init(&a_empty[i], 4); }
-        for (int i = 0; i < SB; ++i) {
-            mbar_init(&hl_full[i], 4); mbar_init(&om_full[i], 1); mbar_init(&b_empty[i], 1);
-        }
-        for (int i = 0; i < 2; ++i) { mbar_init(&acc_full[i], 1); mbar_init(&acc_empty[i], 8); }
+        for (int i = 0; i < SA; ++i) { mbar_init(&a_full[i], 1); mbar_init(&a_empty[i], kNumSplitWarps); }
+        for (int i = 0; i < NCH; ++i) { mbar_init(&ch_ready[i], kNumSplitWarps + 1); mbar_init(&ch_empty[i], 1); }
+        for (int i = 0; i < NSLOT; ++i) { mbar_init(&acc_full[i], 1); mbar_init(&acc_empty[i], 4); }
         fence_mbar_init();
     }
     if (warp == kWarpProdA && lane == 0) {
         tma_prefetch_desc(&mapA);
         tma_prefetch_desc(&mapB);
     }
-    if (warp == kWarpMMA) tmem_alloc<CF::kTmemCols>(tmem_slot);
+    if (warp == kWarpMMA) tmem_alloc<kTmemCols>(tmem_slot);
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
 
     const int num_tiles = p.m_tiles * p.splits * p.n_tiles;
+    const long long t_kernel0 = clock64();
 
-    if (warp < 4) {
-        // ============================================================ splitter (Eqs 14-15)
-        asm volatile("setmaxnreg.dec.sync.aligned.u32 64;");
-        const int t = threadIdx.x;                       // 0..127
-        const int w = t >> 5, l = t & 31;
-        const int r = 32 * w + 8 * (l >> 3) + (l & 7);   // tile row owned by this thread
-        const int rx = r & 7;                            // SW128 XOR term of this row
-        uint32_t sa = 0, pa = 0, sb = 0, pb = 0;
+    if (warp < kNumSplitWarps) {
+        // ============================================================ splitter (Eqs 14-15) -> TMEM
+        asm volatile("setmaxnreg.dec.sync.aligned.u32 56;");
+        const int q = static_cast<int>(warp & 3u);        // TMEM lane quarter = rows 32q..32q+31
+        const int kh = static_cast<int>(warp >> 2);       // k half of the stage: 32kh .. 32kh+31
+        const int r = 32 * q + static_cast<int>(lane);    // tile row owned by this thread
+        const int rx = r & 7;                             // SW128 XOR term of this row
+        const uint32_t lane_addr = static_cast<uint32_t>(32 * q) << 16;
+        uint32_t sa = 0, pa = 0, cs = 0, pc = 0;
+        long long w_a = 0, w_b = 0, stages = 0;
+        const long long t_begin = clock64();
+        const bool skip_math = (p.dbg & 2u) != 0;
         for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
             int m_blk, s, n_blk, kb0, kb1;
             tile_coords(tile, p, m_blk, s, n_blk);
             kb_range(s, p, kb0, kb1);
-            for (int kb = kb0; kb < kb1; ++kb) {
-                mbar_wait(&a_full[sa], pa);
-                mbar_wait(&b_empty[sb], pb ^ 1u);
-                const uint8_t* src = a32 + sa * kA32StageBytes + r * 128;
-                uint8_t* dhi = hl + sb * kHLStageBytes + r * 128;
-                uint8_t* dlo = dhi + kHLStageBytes / 2;
+            for (int kb = kb0; kb < kb1; kb += KC) {
+                const int nst = (kb1 - kb) < KC ? (kb1 - kb) : KC;
 #pragma unroll
-                for (int c = 0; c < 8; ++c) {            // FP16 16-B chunk c = k 8c .. 8c+7
-                    const uint8_t* box = src + (c >> 2) * (kA32StageBytes / 2);
-                    const int f0 = ((2 * (c & 3)) ^ rx) * 16;
-                    const int f1 = ((2 * (c & 3) + 1) ^ rx) * 16;
-                    const float4 x0 = *reinterpret_cast<const float4*>(box + f0);
-                    const float4 x1 = *reinterpret_cast<const float4*>(box + f1);
-                    uint4 h, lo;
-                    split8(x0, x1, h, lo);
-                    const int dc = (c ^ rx) * 16;
-                    *reinterpret_cast<uint4*>(dhi + dc) = h;
-                    *reinterpret_cast<uint4*>(dlo + dc) = lo;
+                for (int t = 0; t < KC; ++t) {
+                    if (t < nst) {
+                        ++stages;
+                        // (1) read and split this thread's 32 k of its row (overlaps the MMAs that
+                        //     still use the chunk slot about to be overwritten)
+                        mbar_wait_prof(&a_full[sa], pa, w_a);
+                        uint32_t hi[16], lo[16];
+                        if (!skip_math) {
+                            const uint8_t* src = a32 + sa * kA32StageBytes + kh * (kA32StageBytes / 2) + r * 128;
+#pragma unroll
+                            for (int c = 0; c < 4; ++c) {        // 8 k per chunk of the row
+                                const float4 x0 = *reinterpret_cast<const float4*>(src + (((2 * c) ^ rx) * 16));
+                                const float4 x1 = *reinterpret_cast<const float4*>(src + (((2 * c + 1) ^ rx) * 16));
+                                split2_x2(x0.x, x0.y, hi[4 * c + 0], lo[4 * c + 0]);
+                                split2_x2(x0.z, x0.w, hi[4 * c + 1], lo[4 * c + 1]);
+                                split2_x2(x1.x, x1.y, hi[4 * c + 2], lo[4 * c + 2]);
+                                split2_x2(x1.z, x1.w, hi[4 * c + 3], lo[4 * c + 3]);
+                            }
+                        }
+                        __syncwarp();
+                        if (lane == 0) mbar_arrive(&a_empty[sa]);
+                        advance(sa, pa, SA);
+                        // (2) hand hi/lo to the tensor cores through TMEM
+                        if (t == 0) {
+                            mbar_wait_prof(&ch_empty[cs], pc ^ 1u, w_b);
+                            tc_fence_after();
+                        }
+                        if (!skip_math) {
+                            const uint32_t col = tmem_base + lane_addr + ABASE + (cs * KC + t) * kAStageCols + kh * 16;
+                            tmem_st16(col, hi);
+                            tmem_st16(col + 32, lo);
+                        }
+                    }
                 }
-                fence_proxy_async_smem();
+                tmem_st_wait();
+                tc_fence_before();
                 __syncwarp();
-                if (l == 0) {
-                    mbar_arrive(&hl_full[sb]);
-                    mbar_arrive(&a_empty[sa]);
-                }
-                advance(sa, pa, SA);
-                advance(sb, pb, SB);
+                if (lane == 0) mbar_arrive(&ch_ready[cs]);
+                advance(cs, pc, NCH);
             }
         }
-    } else if (warp < 8) {
-        asm volatile("setmaxnreg.dec.sync.aligned.u32 64;");
+        if (p.prof && threadIdx.x == 0) {
+            long long* pr = p.prof + blockIdx.x * kProfSlots;
+            pr[kProfSplitAFull] = w_a;
+            pr[kProfSplitBEmpty] = w_b;
+            pr[kProfSplitBusy] = clock64() - t_begin - w_a - w_b;
+            pr[kProfStages] = stages;
+        }
+    } else if (warp < kEpiWarp0 + 8) {
+        // ============================================================ RN promotion + epilogue
+        asm volatile("setmaxnreg.inc.sync.aligned.u32 168;");
+        const int q = static_cast<int>(warp & 3u);                       // TMEM lane quarter (warp_id % 4)
+        const int h = static_cast<int>((warp - kEpiWarp0) >> 2);         // epilogue group: parts h, h+2, ...
+        const uint32_t lane_addr = static_cast<uint32_t>(32 * q) << 16;
+        uint32_t stage = 0;
+        long long w_full = 0, t_store = 0;
+        const bool skip_ld = (p.dbg & 1u) != 0;
+        for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+            int m_blk, s, n_blk, kb0, kb1;
+            tile_coords(tile, p, m_blk, s, n_blk);
+            kb_range(s, p, kb0, kb1);
+            float acc[NPH * W];
+#pragma unroll
+            for (int i = 0; i < NPH * W; ++i) acc[i] = 0.0f;
+            for (int kb = kb0; kb < kb1; kb += CF::KC, ++stage) {   // one promotion per K_c chunk
+#pragma unroll
+                for (int j = 0; j < NPH; ++j) {
+                    const int part = h + 2 * j;
+                    const int width = (part == NQ - 1) ? WLAST : W;
+                    const uint32_t g = stage * NQ + part;
+                    const uint32_t slot = g % NSLOT;
+                    mbar_wait_prof(&acc_full[slot], (g / NSLOT) & 1u, w_full);
+                    tc_fence_after();
+                    const uint32_t taddr = tmem_base + lane_addr + slot * W;
+                    if (!skip_ld) {
+#pragma unroll
+                        for (int c = 0; c < W; c += 16) {
+                            if (c < width) {
+                                float v[2][8];
+#pragma unroll
+                                for (int u = 0; u < 2; ++u)
+                                    if (c + 8 * u < width) tmem_ld8(taddr + c + 8 * u, v[u]);
+                                tmem_ld_wait();
+#pragma unroll
+                                for (int u = 0; u < 2; ++u)
+#pragma unroll
+                                    for (int i = 0; i < 8; i += 2)
+                                        if (c + 8 * u < width)
+                                            ADD_PAIR(acc[j * W + c + 8 * u + i], acc[j * W + c + 8 * u + i + 1],
+                                                     v[u][i], v[u][i + 1]);
+                            }
+                        }
+                    }
+                    tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&acc_empty[slot]);
+                }
+            }
+            // ---- store the tile rows owned by this thread (its parts' columns)
+            const long long ts0 = clock64();
+            const int64_t row = static_cast<int64_t>(m_blk) * kBM + 32 * q + static_cast<int>(lane);
+            if (row < p.m) {
+#pragma unroll
+                for (int j = 0; j < NPH; ++j) {
+                    const int part = h + 2 * j;
+                    const int width = (part == NQ - 1) ? WLAST : W;
+                    const int64_t col0 = static_cast<int64_t>(n_blk) * BN + part * W;
+                    if (col0 >= p.n) continue;
+                    float* dst = p.out + static_cast<int64_t>(s) * p.split_stride + row * p.ldo_out + col0;
+                    const int64_t valid = (p.n - col0) < width ? (p.n - col0) : width;
+                    bool bad = false;
+                    if (p.vec_store && valid == width) {
+#pragma unroll
+                        for (int i = 0; i < W; i += 4)
+                            if (i < width)
+                                *reinterpret_cast<float4*>(dst + i) =
+                                    make_float4(acc[j * W + i], acc[j * W + i + 1], acc[j * W + i + 2], acc[j * W + i + 3]);
+                    } else {
+#pragma unroll
+                        for (int i = 0; i < W; ++i)
+                            if (i < valid) dst[i] = acc[j * W + i];
+                    }
+                    if (p.nonfinite) {
+#pragma unroll
+                        for (int i = 0; i < W; ++i)
+                            if (i < valid && !isfinite(acc[j * W + i])) bad = true;
+                        if (bad) atomicOr(p.nonfinite, 1);
+                    }
+                }
+            }
+            t_store += clock64() - ts0;
+        }
+        if (p.prof && warp == kEpiWarp0 && lane == 0) {
+            long long* pr = p.prof + blockIdx.x * kProfSlots;
+            pr[kProfEpiAccFull] = w_full;
+            pr[kProfEpiStore] = t_store;
+        }
+    } else {
+        asm volatile("setmaxnreg.dec.sync.aligned.u32 32;");
         if (warp == kWarpProdA) {
             // ======================================================== A stager (TMA, FP32)
             if (elect_one()) {
                 const uint64_t pol = policy_evict_first();
                 uint32_t sa = 0, pa = 0;
+                long long w = 0;
                 for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
                     int m_blk, s, n_blk, kb0, kb1;
                     tile_coords(tile, p, m_blk, s, n_blk);
                     kb_range(s, p, kb0, kb1);
                     const int m0 = m_blk * kBM;
                     for (int kb = kb0; kb < kb1; ++kb) {
-                        mbar_wait(&a_empty[sa], pa ^ 1u);
+                        mbar_wait_prof(&a_empty[sa], pa ^ 1u, w);
                         mbar_arrive_expect_tx(&a_full[sa], kA32StageBytes);
                         const int64_t kk = static_cast<int64_t>(kb) * kBK;
                         const int c0 = static_cast<int>(kk % p.k_inner);
@@ -209,128 +424,99 @@ shgemm_sm100_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_const
                         advance(sa, pa, SA);
                     }
                 }
+                if (p.prof) p.prof[blockIdx.x * kProfSlots + kProfProdAEmpty] = w;
             }
         } else if (warp == kWarpProdB) {
             // ======================================================== Omega stager (TMA, FP16)
             if (elect_one()) {
                 const uint64_t pol = policy_evict_last();
-                uint32_t sb = 0, pb = 0;
+                uint32_t cs = 0, pc = 0;
+                long long w = 0;
                 for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
                     int m_blk, s, n_blk, kb0, kb1;
                     tile_coords(tile, p, m_blk, s, n_blk);
                     kb_range(s, p, kb0, kb1);
                     const int n0 = n_blk * BN;
-                    for (int kb = kb0; kb < kb1; ++kb) {
-                        mbar_wait(&b_empty[sb], pb ^ 1u);
-                        mbar_arrive_expect_tx(&om_full[sb], kOm);
-                        tma_load_2d(om + sb * kOm, &mapB, &om_full[sb], kb * kBK, n0, pol);
-                        advance(sb, pb, SB);
+                    for (int kb = kb0; kb < kb1; kb += KC) {
+                        const int nst = (kb1 - kb) < KC ? (kb1 - kb) : KC;
+                        mbar_wait_prof(&ch_empty[cs], pc ^ 1u, w);
+                        mbar_arrive_expect_tx(&ch_ready[cs], static_cast<uint32_t>(nst * kOm));
+                        for (int t = 0; t < nst; ++t)
+                            tma_load_2d(om + (cs * KC + t) * kOm, &mapB, &ch_ready[cs], (kb + t) * kBK, n0, pol);
+                        advance(cs, pc, NCH);
                     }
                 }
+                if (p.prof) p.prof[blockIdx.x * kProfSlots + kProfProdBEmpty] = w;
             }
         } else if (warp == kWarpMMA) {
-            // ======================================================== MMA issuer (tcgen05)
-            constexpr uint32_t idesc = idesc_f16_f32(kBM, BN);
-            uint32_t sb = 0, pb = 0, buf = 0, pacc = 0;
+            // ======================================================== MMA issuer (tcgen05, A from TMEM)
+            uint32_t cs = 0, pc = 0, g = 0;
+            long long w_acc = 0, w_hl = 0, w_om = 0;
+            const bool skip_mma = (p.dbg & 4u) != 0;
             for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
                 int m_blk, s, n_blk, kb0, kb1;
                 tile_coords(tile, p, m_blk, s, n_blk);
                 kb_range(s, p, kb0, kb1);
-                for (int kb = kb0; kb < kb1; ++kb) {
-                    mbar_wait(&acc_empty[buf], pacc ^ 1u);
-                    mbar_wait(&hl_full[sb], pb);
-                    mbar_wait(&om_full[sb], pb);
-                    tc_fence_after();
-                    if (elect_one()) {
-                        const uint32_t d = tmem_base + buf * BN;
-                        const uint64_t ahi = sw128_kmajor_desc(smem_u32(hl + sb * kHLStageBytes));
-                        const uint64_t alo = sw128_kmajor_desc(smem_u32(hl + sb * kHLStageBytes + kHLStageBytes / 2));
-                        const uint64_t bd = sw128_kmajor_desc(smem_u32(om + sb * kOm));
-                        // D := lo . Omega   (4 x K=16; +32 B per step inside the 128-B swizzle row)
+                for (int kb = kb0; kb < kb1; kb += KC) {
+                    const int nst = (kb1 - kb) < KC ? (kb1 - kb) : KC;   // stages in this chunk
+                    mbar_wait_prof(&ch_ready[cs], pc, w_hl);
+                    const uint32_t a_base = tmem_base + ABASE + cs * KC * kAStageCols;
+                    const uint64_t b_base = sw128_kmajor_desc(smem_u32(om + cs * KC * kOm));
 #pragma unroll
-                        for (int j = 0; j < 4; ++j) mma_f16_ss(d, alo + 2 * j, bd + 2 * j, idesc, j > 0 ? 1u : 0u);
-                        // D := hi . Omega + D * 2^-11, then accumulate the rest of hi
-                        mma_f16_ss_scaled<11>(d, ahi, bd, idesc);
+                    for (int part = 0; part < NQ; ++part, ++g) {
+                        const uint32_t slot = g % NSLOT;
+                        mbar_wait_prof(&acc_empty[slot], ((g / NSLOT) & 1u) ^ 1u, w_acc);
+                        tc_fence_after();
+                        if (elect_one()) {
+                            if (!skip_mma) {
+                                const uint32_t d = tmem_base + slot * W;
+                                const uint32_t idesc = idesc_f16_f32(kBM, part == NQ - 1 ? WLAST : W);
+                                const uint64_t b = b_base + static_cast<uint64_t>((part * W * 128) >> 4);
+                                // D := sum over the chunk's stages of lo . Omega  (Eq 16's dA_low term)
 #pragma unroll
-                        for (int j = 1; j < 4; ++j) mma_f16_ss(d, ahi + 2 * j, bd + 2 * j, idesc, 1u);
-                        tc_commit(&b_empty[sb]);
-                        tc_commit(&acc_full[buf]);
+                                for (int t = 0; t < KC; ++t)
+                                    if (t < nst)
+#pragma unroll
+                                        for (int j = 0; j < 4; ++j)
+                                            mma_f16_ts(d, a_base + t * kAStageCols + 32 + 8 * j,
+                                                       b + static_cast<uint64_t>((t * kOm) >> 4) + 2 * j, idesc,
+                                                       (t > 0 || j > 0) ? 1u : 0u);
+                                // D := hi . Omega + D * 2^-11 (first step), then the rest of hi
+#pragma unroll
+                                for (int t = 0; t < KC; ++t)
+                                    if (t < nst)
+#pragma unroll
+                                        for (int j = 0; j < 4; ++j) {
+                                            const uint32_t a = a_base + t * kAStageCols + 8 * j;
+                                            const uint64_t bb = b + static_cast<uint64_t>((t * kOm) >> 4) + 2 * j;
+                                            if (t == 0 && j == 0) mma_f16_ts_scale11(d, a, bb, idesc);
+                                            else mma_f16_ts(d, a, bb, idesc, 1u);
+                                        }
+                            }
+                            tc_commit(&acc_full[slot]);
+                        }
+                        __syncwarp();
                     }
+                    if (elect_one()) tc_commit(&ch_empty[cs]);
                     __syncwarp();
-                    advance(sb, pb, SB);
-                    advance(buf, pacc, 2);
+                    advance(cs, pc, NCH);
                 }
             }
-        }
-    } else {
-        // ============================================================ RN promotion + epilogue
-        asm volatile("setmaxnreg.inc.sync.aligned.u32 192;");
-        const int q = static_cast<int>(warp & 3u);           // TMEM lane quarter (warp_id % 4)
-        const int h = static_cast<int>((warp - kEpiWarp0) >> 2);  // column half
-        const uint32_t lane_base = static_cast<uint32_t>(32 * q) << 16;
-        uint32_t buf = 0, pacc = 0;
-        for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
-            int m_blk, s, n_blk, kb0, kb1;
-            tile_coords(tile, p, m_blk, s, n_blk);
-            kb_range(s, p, kb0, kb1);
-            float acc[C];
-#pragma unroll
-            for (int i = 0; i < C; ++i) acc[i] = 0.0f;
-            for (int kb = kb0; kb < kb1; ++kb) {
-                mbar_wait(&acc_full[buf], pacc);
-                tc_fence_after();
-                const uint32_t taddr = tmem_base + lane_base + buf * BN + h * C;
-#pragma unroll
-                for (int c = 0; c < C; c += 32) {
-                    constexpr int kMax = 32;
-                    float v[4][8];
-#pragma unroll
-                    for (int u = 0; u < 4; ++u)
-                        if (c + 8 * u < C) tmem_ld8<BN>(taddr + c + 8 * u, v[u]);
-                    tmem_ld_wait();
-#pragma unroll
-                    for (int u = 0; u < 4; ++u)
-#pragma unroll
-                        for (int i = 0; i < 8; ++i)
-                            if (c + 8 * u < C) acc[c + 8 * u + i] = __fadd_rn(acc[c + 8 * u + i], v[u][i]);
-                    (void)kMax;
-                }
-                tc_fence_before();
-                __syncwarp();
-                if (lane == 0) mbar_arrive(&acc_empty[buf]);
-                advance(buf, pacc, 2);
-            }
-            // ---- store the tile rows owned by this thread
-            const int64_t row = static_cast<int64_t>(m_blk) * kBM + 32 * q + static_cast<int>(lane);
-            const int64_t col0 = static_cast<int64_t>(n_blk) * BN + h * C;
-            if (row < p.m && col0 < p.n) {
-                float* dst = p.out + static_cast<int64_t>(s) * p.split_stride + row * p.ldo_out + col0;
-                const int64_t valid = p.n - col0;
-                bool bad = false;
-                if (p.vec_store && valid >= C) {
-#pragma unroll
-                    for (int i = 0; i < C; i += 4)
-                        *reinterpret_cast<float4*>(dst + i) = make_float4(acc[i], acc[i + 1], acc[i + 2], acc[i + 3]);
-                } else {
-#pragma unroll
-                    for (int i = 0; i < C; ++i)
-                        if (i < valid) dst[i] = acc[i];
-                }
-                if (p.nonfinite) {
-#pragma unroll
-                    for (int i = 0; i < C; ++i)
-                        if (i < valid && !isfinite(acc[i])) bad = true;
-                    if (bad) atomicOr(p.nonfinite, 1);
-                }
+            if (p.prof && lane == 0) {
+                long long* pr = p.prof + blockIdx.x * kProfSlots;
+                pr[kProfMmaAccEmpty] = w_acc;
+                pr[kProfMmaHlFull] = w_hl;
+                pr[kProfMmaOmFull] = w_om;
             }
         }
     }
 
     tc_fence_before();
     __syncthreads();
+    if (p.prof && threadIdx.x == 0) p.prof[blockIdx.x * kProfSlots + kProfTotal] = clock64() - t_kernel0;
     if (warp == kWarpMMA) {
         tc_fence_after();
-        tmem_dealloc<CF::kTmemCols>(tmem_base);
+        tmem_dealloc<kTmemCols>(tmem_base);
     }
 }
 
