@@ -99,6 +99,13 @@ shg_status_t shgemm_ex(int64_t m, int64_t n, int64_t k, const float *A, int64_t 
                        int64_t ldo, float *Y, int64_t ldc, const shg_tune_t *tune, void *workspace,
                        size_t workspace_bytes, int *nonfinite_flag, shg_stream_t stream);
 
+/* shgemm_ex for an M-major A ("A transposed"): element (i, l) of A is At[l * ldat + i], i.e. At is
+ * the k x m row-major transpose of A, ldat >= m (fast path: At 16-B aligned, ldat % 4 == 0). This
+ * is how project() reads the last-mode unfolding of a C-order tensor in place. */
+shg_status_t shgemm_at(int64_t m, int64_t n, int64_t k, const float *At, int64_t ldat, const uint16_t *Omega,
+                       int64_t ldo, float *Y, int64_t ldc, const shg_tune_t *tune, void *workspace,
+                       size_t workspace_bytes, int *nonfinite_flag, shg_stream_t stream);
+
 /* Bytes of split-K workspace shgemm_ex needs for (m, n, k) with `tune` (NULL = heuristics). */
 size_t shg_workspace_size(int64_t m, int64_t n, int64_t k, const shg_tune_t *tune);
 

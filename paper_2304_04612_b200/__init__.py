@@ -66,6 +66,7 @@ def lib():
             L.project.argtypes = [vp, i32, vp, i32, i64, u64, i32, vp, i64, vp, sz, vp]
             L.shg_project_workspace_size.argtypes = [i32, vp, i32, i64]
             L.shg_project_workspace_size.restype = sz
+            L.shgemm_at.argtypes = [i64, i64, i64, vp, i64, vp, i64, vp, i64, ctypes.POINTER(Tune), vp, sz, vp, vp]
             L.shgemm_host.argtypes = [i64, i64, i64, vp, i64, vp, i64, vp, i64, i64, vp, sz, vp]
             L.shg_host_workspace_size.argtypes = [i64, i64, i64]
             L.shg_host_workspace_size.restype = sz
@@ -78,7 +79,7 @@ def lib():
             L.shg_probe_umma.argtypes = [vp, vp, i32, vp, i32, i32, vp, vp]
             L.shg_probe_mma_rate.argtypes = [i32, i32, i32, i32, vp, i32, vp]
             L.shg_probe_mma_rate.restype = i32
-            for name in ("shgemm", "shgemm_ex", "shgemm_host", "shg_plan", "gen_omega_f16", "gen_omega_f16_ex", "project",
+            for name in ("shgemm", "shgemm_ex", "shgemm_at", "shgemm_host", "shg_plan", "gen_omega_f16", "gen_omega_f16_ex", "project",
                          "shg_debug_split", "shg_synth_f32", "shg_probe_umma"):
                 getattr(L, name).restype = i32
             _lib = L
@@ -165,6 +166,26 @@ def shgemm(A: torch.Tensor, Omega: torch.Tensor, out: torch.Tensor | None = None
     ws_bytes = 0 if workspace is None else workspace.numel() * workspace.element_size()
     _check(lib().shgemm_ex(m, n, k, _p(A), lda, _p(Omega), ldo, _p(out), ldc, _tune(tune), _p(workspace),
                            ws_bytes, _p(nonfinite), _stream(stream)), "shgemm_ex")
+    return out
+
+
+def shgemm_at(At: torch.Tensor, Omega: torch.Tensor, out: torch.Tensor | None = None, tune=None,
+              nonfinite: torch.Tensor | None = None, workspace: torch.Tensor | None = None, stream=None):
+    """Y = A . Omega for an M-major A given as its transpose At (k, m) float32 row-major."""
+    k, m = At.shape
+    k2, n = Omega.shape
+    if k2 != k or At.dtype != torch.float32 or Omega.dtype != torch.float16:
+        raise ValueError("shape/dtype mismatch")
+    if m and k and At.stride(1) != 1:
+        raise ValueError("At must be row-major")
+    if k and n and Omega.stride(0) != 1:
+        raise ValueError("Omega must be column-major (stride(0) == 1)")
+    if out is None:
+        out = torch.empty((m, n), dtype=torch.float32, device=At.device)
+    ws_bytes = 0 if workspace is None else workspace.numel() * workspace.element_size()
+    _check(lib().shgemm_at(m, n, k, _p(At), At.stride(0) if k > 1 else max(m, 1), _p(Omega),
+                           Omega.stride(1) if n > 1 else max(k, 1), _p(out), out.stride(0) if m > 1 else max(n, 1),
+                           _tune(tune), _p(workspace), ws_bytes, _p(nonfinite), _stream(stream)), "shgemm_at")
     return out
 
 

@@ -170,7 +170,7 @@ Plan make_plan(int64_t m, int64_t n, int64_t k, bool fast_ok, const shg_tune_t* 
 
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 
-template <int BN>
+template <int BN, bool MMAJOR>
 shg_status_t launch_tc(const CUtensorMap& mapA, const CUtensorMap& mapB, const shg::KParams& kp, int grid,
                        cudaStream_t stream) {
     using CF = shg::Cfg<BN>;
@@ -179,20 +179,36 @@ shg_status_t launch_tc(const CUtensorMap& mapA, const CUtensorMap& mapB, const s
     cudaGetDevice(&dev);
     cudaError_t attr_err = cudaSuccess;
     std::call_once(flags[std::min(std::max(dev, 0), 63)], [&]() {
-        attr_err = cudaFuncSetAttribute(shg::shgemm_sm100_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        CF::kSmemBytes);
+        attr_err = cudaFuncSetAttribute(shg::shgemm_sm100_kernel<BN, MMAJOR>,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, CF::kSmemBytes);
     });
     if (attr_err != cudaSuccess) return cuda_fail(attr_err, "cudaFuncSetAttribute");
-    shg::shgemm_sm100_kernel<BN><<<grid, shg::kThreads, CF::kSmemBytes, stream>>>(mapA, mapB, kp);
+    shg::shgemm_sm100_kernel<BN, MMAJOR><<<grid, shg::kThreads, CF::kSmemBytes, stream>>>(mapA, mapB, kp);
     g_launches.fetch_add(1, std::memory_order_relaxed);
     SHG_CUDA(cudaGetLastError());
     return SHG_OK;
 }
 
-shg_status_t dispatch_tc(int bn, const CUtensorMap& a, const CUtensorMap& b, const shg::KParams& kp, int grid,
-                         cudaStream_t s) {
+shg_status_t dispatch_tc(int bn, bool mmajor, const CUtensorMap& a, const CUtensorMap& b, const shg::KParams& kp,
+                         int grid, cudaStream_t s) {
     if (!valid_bn(bn)) return SHG_ERR_INVALID_VALUE;
-    SHG_BN_SWITCH(bn, return launch_tc<BN_>(a, b, kp, grid, s))
+    if (mmajor) {
+        SHG_BN_SWITCH(bn, return (launch_tc<BN_, true>(a, b, kp, grid, s)))
+    }
+    SHG_BN_SWITCH(bn, return (launch_tc<BN_, false>(a, b, kp, grid, s)))
+}
+
+// M-major A (element (i, l) at A[l * lda + i]): 2-D map {M, K}, box {32 rows, 64 k}
+bool encode_a_mmajor(CUtensorMap* map, const float* A, int64_t M, int64_t K, int64_t lda) {
+    EncodeFn fn = encode_fn();
+    if (!fn) return false;
+    cuuint64_t dims[2] = {static_cast<cuuint64_t>(M), static_cast<cuuint64_t>(K)};
+    cuuint64_t strides[1] = {static_cast<cuuint64_t>(lda) * 4};
+    cuuint32_t box[2] = {32, 64};
+    cuuint32_t estr[2] = {1, 1};
+    return fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(A), dims, strides, box, estr,
+              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
 int grid_for(int64_t work, int threads) {
@@ -201,10 +217,12 @@ int grid_for(int64_t work, int threads) {
 }
 
 // Generic A view used by shgemm (plain matrix) and project (unfoldings):
-// element (row, kk) at A[(kk / S) * slab + row * row_stride + kk % S].
+// K-major : element (row, kk) at A[(kk / S) * slab + row * row_stride + kk % S];
+// M-major : element (row, kk) at A[kk * row_stride + row]   (S = k, P = 1, slab unused).
 struct AView {
     const float* A;
     int64_t S, P, row_stride, slab;
+    bool mmajor = false;
 };
 
 shg_status_t run_shgemm(int64_t m, int64_t n, int64_t k, const AView& av, const uint16_t* Om, int64_t ldo,
@@ -220,18 +238,21 @@ shg_status_t run_shgemm(int64_t m, int64_t n, int64_t k, const AView& av, const 
     const bool plain = (av.P == 1 && av.S == k);
     const bool fast_ok = aligned16(av.A) && aligned16(Om) && (av.row_stride % 4 == 0) && (av.slab % 4 == 0) &&
                          (ldo % 8 == 0) && (plain || av.S % shg::kBK == 0) && encode_fn() != nullptr &&
-                         k < (int64_t(1) << 31) && av.S < (int64_t(1) << 31);
+                         k < (int64_t(1) << 31) && av.S < (int64_t(1) << 31) && m < (int64_t(1) << 31);
     Plan pl = make_plan(m, n, k, fast_ok, tune, d.sms);
     if (pl.path == 1) {
         if (!plain) return SHG_ERR_INVALID_VALUE;  // callers materialise non-plain views first
-        shg::shgemm_simt_kernel<<<grid_for(m * n, 256), 256, 0, stream>>>(m, n, k, av.A, av.row_stride, Om, ldo, Y,
+        const int64_t sa_row = av.mmajor ? 1 : av.row_stride, sa_col = av.mmajor ? av.row_stride : 1;
+        shg::shgemm_simt_kernel<<<grid_for(m * n, 256), 256, 0, stream>>>(m, n, k, av.A, sa_row, sa_col, Om, ldo, Y,
                                                                          ldc, nonfinite);
         g_launches.fetch_add(1, std::memory_order_relaxed);
         SHG_CUDA(cudaGetLastError());
         return SHG_OK;
     }
     CUtensorMap mapA, mapB;
-    if (!encode_a(&mapA, av.A, av.S, m, av.P, av.row_stride, av.slab)) {
+    const bool enc_ok = av.mmajor ? encode_a_mmajor(&mapA, av.A, m, k, av.row_stride)
+                                  : encode_a(&mapA, av.A, av.S, m, av.P, av.row_stride, av.slab);
+    if (!enc_ok) {
         std::snprintf(g_err, sizeof(g_err), "cuTensorMapEncodeTiled(A) failed");
         return SHG_ERR_CUDA;
     }
@@ -269,7 +290,7 @@ shg_status_t run_shgemm(int64_t m, int64_t n, int64_t k, const AView& av, const 
         kp.vec_store = (aligned16(Y) && ldc % 4 == 0) ? 1 : 0;
         kp.nonfinite = nonfinite;
     }
-    shg_status_t st = dispatch_tc(pl.bn, mapA, mapB, kp, pl.grid, stream);
+    shg_status_t st = dispatch_tc(pl.bn, av.mmajor, mapA, mapB, kp, pl.grid, stream);
     if (st != SHG_OK) return st;
     if (pl.splits > 1) {
         shg::splitk_reduce_kernel<<<grid_for(m * n, 256), 256, 0, stream>>>(kp.out, pl.splits, m, n, pl.ld_ws,
@@ -387,6 +408,19 @@ shg_status_t shgemm(int64_t m, int64_t n, int64_t k, const float* A, int64_t lda
     return shgemm_ex(m, n, k, A, lda, Omega, ldo, Y, ldc, nullptr, nullptr, 0, nullptr, stream);
 }
 
+shg_status_t shgemm_at(int64_t m, int64_t n, int64_t k, const float* At, int64_t ldat, const uint16_t* Omega,
+                       int64_t ldo, float* Y, int64_t ldc, const shg_tune_t* tune, void* workspace,
+                       size_t workspace_bytes, int* nonfinite_flag, shg_stream_t stream) {
+    if (m < 0 || n < 0 || k < 0) return SHG_ERR_INVALID_VALUE;
+    if (m == 0 || n == 0) return SHG_OK;
+    if (!Y || ldc < n) return SHG_ERR_INVALID_VALUE;
+    if (k > 0 && (!At || !Omega || ldat < m || ldo < k)) return SHG_ERR_INVALID_VALUE;
+    if (tune && tune->bn > 0 && !valid_bn(tune->bn)) return SHG_ERR_INVALID_VALUE;
+    AView av{At, k, 1, ldat, 0, true};
+    return run_shgemm(m, n, k, av, Omega, ldo, Y, ldc, tune, workspace, workspace_bytes, nonfinite_flag,
+                      reinterpret_cast<cudaStream_t>(stream));
+}
+
 size_t shg_workspace_size(int64_t m, int64_t n, int64_t k, const shg_tune_t* tune) {
     if (m <= 0 || n <= 0 || k <= 0) return 0;
     const Plan pl = make_plan(m, n, k, true, tune, std::max(1, dev_info().sms));
@@ -424,7 +458,7 @@ size_t shg_project_workspace_size(int ndim, const int64_t* dims, int mode, int64
     const int64_t M = dims[mode];
     const int64_t ldo = (K + 7) / 8 * 8;
     size_t bytes = static_cast<size_t>((n * ldo * 2 + 255) / 256 * 256);
-    const bool needs_copy = !(mode == 0 || (S % shg::kBK == 0 && S % 4 == 0));
+    const bool needs_copy = !(mode == 0 || S == 1 || (S % shg::kBK == 0 && S % 4 == 0));
     if (needs_copy) bytes += static_cast<size_t>((M * ((K + 3) / 4 * 4) * 4 + 255) / 256 * 256);
     bytes += shg_workspace_size(M, n, K, nullptr);
     return bytes;
@@ -465,24 +499,18 @@ shg_status_t project(const float* A, int ndim, const int64_t* dims, int mode, in
     } else if (S % shg::kBK == 0 && S % 4 == 0) {
         // A[p][r][s] -> unfold[r][p*S + s]: 3-D view {S, M, P}, row stride S, slab stride M*S
         av = AView{A, S, P, S, M * S};
+    } else if (S == 1) {
+        // last mode: unfold[r][c] = A[c * M + r], i.e. the M-major view of a (K x M) row-major
+        // matrix — read in place by the M-major stager (no transpose copy)
+        av = AView{A, K, 1, M, 0, true};
     } else {
-        // materialise the unfolding (last mode: (P x M) row-major -> M x P, i.e. a transpose)
-        // TODO(M-major stager): read the last-mode unfolding in place
+        // middle mode with S % 64 != 0: materialise the unfolding slab by slab (S-wide row blocks)
         float* T = reinterpret_cast<float*>(ws + off);
         const int64_t ldt = (K + 3) / 4 * 4;
         off += static_cast<size_t>((M * ldt * 4 + 255) / 256 * 256);
-        if (S == 1) {
-            dim3 blk(32, 8);
-            shg::transpose_f32_kernel<<<grid_for(((P + 31) / 32) * ((M + 31) / 32) * 256, 256), blk, 0, s>>>(
-                A, P, M, M, T, ldt);
-            g_launches.fetch_add(1, std::memory_order_relaxed);
-            SHG_CUDA(cudaGetLastError());
-        } else {
-            // general middle mode with S % 64 != 0: copy slab by slab (p) as S-wide row blocks
-            for (int64_t p = 0; p < P; ++p) {
-                SHG_CUDA(cudaMemcpy2DAsync(T + p * S, ldt * 4, A + p * M * S, S * 4, S * 4, M,
-                                           cudaMemcpyDeviceToDevice, s));
-            }
+        for (int64_t p = 0; p < P; ++p) {
+            SHG_CUDA(cudaMemcpy2DAsync(T + p * S, ldt * 4, A + p * M * S, S * 4, S * 4, M,
+                                       cudaMemcpyDeviceToDevice, s));
         }
         av = AView{T, K, 1, ldt, ldt * M};
     }

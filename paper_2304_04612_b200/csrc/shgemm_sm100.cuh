@@ -125,9 +125,17 @@ __device__ __forceinline__ void tile_coords(int tile, const KParams& p, int& m_b
     n_blk = rem - s * p.n_tiles;
 }
 
+// Split s covers the contiguous k-block range [s*num_kb/S, (s+1)*num_kb/S); loops run over the
+// local iteration index it in [0, count) and map it to the global k-block with kb_global.
+// (An interleaved assignment, k-block s + it*S, was measured slower on 4-MB-strided rows.)
 __device__ __forceinline__ void kb_range(int s, const KParams& p, int& lo, int& hi) {
-    lo = static_cast<int>((static_cast<int64_t>(s) * p.num_kb) / p.splits);
-    hi = static_cast<int>((static_cast<int64_t>(s + 1) * p.num_kb) / p.splits);
+    lo = 0;
+    hi = static_cast<int>((static_cast<int64_t>(s + 1) * p.num_kb) / p.splits -
+                          (static_cast<int64_t>(s) * p.num_kb) / p.splits);
+}
+
+__device__ __forceinline__ int kb_global(int it, int s, const KParams& p) {
+    return static_cast<int>((static_cast<int64_t>(s) * p.num_kb) / p.splits) + it;
 }
 
 __device__ __forceinline__ void advance(uint32_t& stage, uint32_t& phase, uint32_t n) {
@@ -197,7 +205,13 @@ __device__ __forceinline__ void add2_rn(float& a, float& b, float c, float d) {
 #define ADD_PAIR(a, b, c, d) add2_rn((a), (b), (c), (d))
 #endif
 
-template <int BN>
+// MMAJOR = false: A is K-major (row-major m x k, or a 3-D K-major view of an unfolding); each stage
+//                 is two TMA boxes of 32 k x 128 rows.
+// MMAJOR = true : A is M-major (element (i, l) at A[l * lda + i], e.g. the last-mode unfolding of a
+//                 C-order tensor); each stage is four TMA boxes of 32 rows x 64 k, and the splitter
+//                 gathers its row's k values with conflict-free 32-bit loads (one 128-B smem row per
+//                 warp instruction) — no transpose copy.
+template <int BN, bool MMAJOR>
 __global__ void __launch_bounds__(kThreads, 1)
 shgemm_sm100_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
                     const KParams p) {
@@ -269,7 +283,21 @@ shgemm_sm100_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_const
                         //     still use the chunk slot about to be overwritten)
                         mbar_wait_prof(&a_full[sa], pa, w_a);
                         uint32_t hi[16], lo[16];
-                        if (!skip_math) {
+                        if (!skip_math && MMAJOR) {
+                            // box r/32 holds rows 32*(r/32).. as 64 k-rows of 128 B (SW128); this
+                            // thread's column is r%32: 16-B chunk (r%32)/4, word r%4
+                            const uint8_t* box = a32 + sa * kA32StageBytes + (r >> 5) * (kA32StageBytes / 4);
+                            const int cidx = (r & 31) >> 2;
+                            const int word = (r & 3) * 4;
+#pragma unroll
+                            for (int i = 0; i < 16; ++i) {       // k pairs 32kh + 2i, +1
+                                const int k0 = 32 * kh + 2 * i;
+                                const float a0 = *reinterpret_cast<const float*>(box + k0 * 128 + ((cidx ^ (k0 & 7)) << 4) + word);
+                                const float a1 =
+                                    *reinterpret_cast<const float*>(box + (k0 + 1) * 128 + ((cidx ^ ((k0 + 1) & 7)) << 4) + word);
+                                split2_x2(a0, a1, hi[i], lo[i]);
+                            }
+                        } else if (!skip_math) {
                             const uint8_t* src = a32 + sa * kA32StageBytes + kh * (kA32StageBytes / 2) + r * 128;
 #pragma unroll
                             for (int c = 0; c < 4; ++c) {        // 8 k per chunk of the row
@@ -415,12 +443,20 @@ shgemm_sm100_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_const
                     for (int kb = kb0; kb < kb1; ++kb) {
                         mbar_wait_prof(&a_empty[sa], pa ^ 1u, w);
                         mbar_arrive_expect_tx(&a_full[sa], kA32StageBytes);
-                        const int64_t kk = static_cast<int64_t>(kb) * kBK;
+                        const int64_t kk = static_cast<int64_t>(kb_global(kb, s, p)) * kBK;
                         const int c0 = static_cast<int>(kk % p.k_inner);
                         const int c2 = static_cast<int>(kk / p.k_inner);
                         uint8_t* dst = a32 + sa * kA32StageBytes;
-                        tma_load_3d(dst, &mapA, &a_full[sa], c0, m0, c2, pol);
-                        tma_load_3d(dst + kA32StageBytes / 2, &mapA, &a_full[sa], c0 + 32, m0, c2, pol);
+                        if (MMAJOR) {
+                            // 2-D map {M (inner), K}: four boxes of 32 rows x 64 k
+#pragma unroll
+                            for (int b = 0; b < 4; ++b)
+                                tma_load_2d(dst + b * (kA32StageBytes / 4), &mapA, &a_full[sa], m0 + 32 * b,
+                                            static_cast<int>(kk), pol);
+                        } else {
+                            tma_load_3d(dst, &mapA, &a_full[sa], c0, m0, c2, pol);
+                            tma_load_3d(dst + kA32StageBytes / 2, &mapA, &a_full[sa], c0 + 32, m0, c2, pol);
+                        }
                         advance(sa, pa, SA);
                     }
                 }
@@ -442,7 +478,8 @@ shgemm_sm100_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_const
                         mbar_wait_prof(&ch_empty[cs], pc ^ 1u, w);
                         mbar_arrive_expect_tx(&ch_ready[cs], static_cast<uint32_t>(nst * kOm));
                         for (int t = 0; t < nst; ++t)
-                            tma_load_2d(om + (cs * KC + t) * kOm, &mapB, &ch_ready[cs], (kb + t) * kBK, n0, pol);
+                            tma_load_2d(om + (cs * KC + t) * kOm, &mapB, &ch_ready[cs], kb_global(kb + t, s, p) * kBK,
+                                        n0, pol);
                         advance(cs, pc, NCH);
                     }
                 }

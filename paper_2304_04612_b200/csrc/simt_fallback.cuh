@@ -9,14 +9,16 @@
 
 namespace shg {
 
-__global__ void shgemm_simt_kernel(int64_t m, int64_t n, int64_t k, const float* __restrict__ A, int64_t lda,
-                                   const uint16_t* __restrict__ Om, int64_t ldo, float* __restrict__ Y,
+// A element (i, l) at A[i * sa_row + l * sa_col] (row-major: sa_row = lda, sa_col = 1;
+// M-major: sa_row = 1, sa_col = lda).
+__global__ void shgemm_simt_kernel(int64_t m, int64_t n, int64_t k, const float* __restrict__ A, int64_t sa_row,
+                                   int64_t sa_col, const uint16_t* __restrict__ Om, int64_t ldo, float* __restrict__ Y,
                                    int64_t ldc, int* nonfinite) {
     const int64_t total = m * n;
     for (int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; t < total;
          t += static_cast<int64_t>(gridDim.x) * blockDim.x) {
         const int64_t i = t / n, j = t - (t / n) * n;
-        const float* a = A + i * lda;
+        const float* a = A + i * sa_row;
         const uint16_t* w = Om + j * ldo;
         float acc = 0.0f;
         for (int64_t k0 = 0; k0 < k; k0 += 64) {
@@ -24,7 +26,7 @@ __global__ void shgemm_simt_kernel(int64_t m, int64_t n, int64_t k, const float*
             float s_hi = 0.0f, s_lo = 0.0f;
             for (int64_t l = k0; l < k1; ++l) {
                 uint32_t h, lo;
-                split2(a[l], 0.0f, h, lo);
+                split2(a[l * sa_col], 0.0f, h, lo);
                 const float hf = __half2float(__ushort_as_half(static_cast<uint16_t>(h & 0xFFFFu)));
                 const float lf = __half2float(__ushort_as_half(static_cast<uint16_t>(lo & 0xFFFFu)));
                 const float wf = __half2float(__ushort_as_half(w[l]));

@@ -1,0 +1,148 @@
+"""RandNLA harness on the GPU (SURVEY §2 A7 / A25, §8d "Pipelines").
+
+Randomized SVD (Alg 1) and RP-HOSVD (Alg 2). The paper uses
+SHGEMM for the random projection only (Alg 1 line 1; Alg 2 line 2) and cuBLAS/cuSOLVER for
+everything else; so does this harness: the projection goes through the C ABI (`shgemm` /
+`project`), QR/SVD/other products are torch.linalg / torch.matmul calls (cuSOLVER / cuBLAS FP32,
+TF32 disabled). `projection="sgemm"` is the FP32 baseline of the paper's speedup figures (P:712:
+"the random matrix is FP16 when using SHGEMM, otherwise FP32"): the same Gaussian stream kept in
+FP32 (OMEGA_SPEC §6 values before FP16 rounding) and a cuBLAS SGEMM. Per-line device times are
+recorded with CUDA events (the Fig 8 / Fig 9 breakdowns).
+"""
+from __future__ import annotations
+
+import contextlib
+
+import torch
+
+from . import gen_omega, project, project_workspace_size, shgemm, synth
+
+
+@contextlib.contextmanager
+def _fp32_matmul():
+    prev = torch.backends.cuda.matmul.allow_tf32
+    torch.backends.cuda.matmul.allow_tf32 = False
+    try:
+        yield
+    finally:
+        torch.backends.cuda.matmul.allow_tf32 = prev
+
+
+class _Timer:
+    def __init__(self, enabled=True):
+        self.enabled = enabled
+        self.marks = []
+
+    def mark(self, name):
+        if self.enabled:
+            e = torch.cuda.Event(enable_timing=True)
+            e.record()
+            self.marks.append((name, e))
+
+    def result(self):
+        if not self.enabled or len(self.marks) < 2:
+            return {}
+        torch.cuda.synchronize()
+        out = {}
+        for (name, e0), (_, e1) in zip(self.marks[:-1], self.marks[1:]):
+            out[name] = out.get(name, 0.0) + e0.elapsed_time(e1)
+        out["total"] = self.marks[0][1].elapsed_time(self.marks[-1][1])
+        return out
+
+
+def _qr_pos(Y):
+    Q, R = torch.linalg.qr(Y)
+    d = torch.sign(torch.diagonal(R))
+    d = torch.where(d == 0, torch.ones_like(d), d)
+    return Q * d[None, :]
+
+
+def omega_fp32(k: int, n: int, seed: int = 0, stream_id: int = 0, device="cuda") -> torch.Tensor:
+    """FP32 Gaussian k x n (column-major view): the SAME counter-based draws as gen_omega's FP16 Omega
+    (OMEGA_SPEC §2-3 addressing, §6 FP32 output) before the RN16 rounding, so the SGEMM baseline
+    and SHGEMM project with the same random matrix up to its FP16 rounding."""
+    return synth("gauss", seed, stream_id, n, k, device=device).t()
+
+
+def rsvd(A: torch.Tensor, p: int, s: int = 10, seed: int = 0, dist="gaussian", projection="shgemm",
+         timing: bool = False):
+    """Alg 1: Y = A Omega; Q = QR(Y); B = Q^T A; (U', S, V) = tSVD(B, p); U = Q U'."""
+    m, n = A.shape
+    nhat = p + s
+    t = _Timer(timing)
+    with _fp32_matmul():
+        t.mark("1_projection")
+        if projection == "shgemm":
+            Om = gen_omega(n, nhat, seed=seed, dist=dist, device=A.device)
+            Y = shgemm(A, Om)
+        elif projection == "sgemm":
+            Om = omega_fp32(n, nhat, seed=seed, device=A.device)
+            Y = A @ Om
+        else:
+            raise ValueError(projection)
+        t.mark("2_qr")
+        Q = _qr_pos(Y)
+        t.mark("3_QtA")
+        B = Q.t() @ A
+        t.mark("4_svd")
+        Uh, S, Vt = torch.linalg.svd(B, full_matrices=False)
+        t.mark("5_QU")
+        U = Q @ Uh[:, :p]
+        t.mark("end")
+    return {"U": U, "S": S[:p], "V": Vt[:p].t(), "Q": Q, "times_ms": t.result()}
+
+
+def reconstruction_error(A, U, S, V) -> float:
+    """||A - U diag(S) V^T||_F / ||A||_F, evaluated in FP64 on the device."""
+    A64 = A.double()
+    R = A64 - (U.double() * S.double()[None, :]) @ V.double().t()
+    return float(torch.linalg.norm(R) / torch.linalg.norm(A64))
+
+
+def unfold(T, mode):
+    return torch.movedim(T, mode, 0).reshape(T.shape[mode], -1)
+
+
+def mode_product(T, M, mode):
+    """T x_mode M with M (I_mode x J): contracts M^T . unfold_mode(T) (reading R14)."""
+    out = torch.tensordot(T, M, dims=([mode], [0]))
+    return torch.movedim(out, -1, mode)
+
+
+def rp_hosvd(T: torch.Tensor, ranks, seed: int = 0, dist="gaussian", projection="shgemm", timing=False):
+    """Alg 2: for each mode W = A'_(i) Omega_(i) (project, stream_id = mode), Q_i = QR(W);
+    g = A x_1 Q_1^T ... x_N Q_N^T."""
+    t = _Timer(timing)
+    Qs = []
+    ws = None
+    if projection == "shgemm":   # one persistent scratch buffer (Omega_(i) + split-K partials) for all modes
+        nbytes = max(project_workspace_size(list(T.shape), i, J) for i, J in enumerate(ranks))
+        ws = torch.empty(nbytes, dtype=torch.uint8, device=T.device)
+    with _fp32_matmul():
+        for i, J in enumerate(ranks):
+            t.mark("2_projection")
+            if projection == "shgemm":
+                W = project(T, i, J, seed=seed, dist=dist, workspace=ws)
+            elif projection == "sgemm":
+                Ui = unfold(T, i)
+                Om = omega_fp32(Ui.shape[1], J, seed=seed, stream_id=i, device=T.device)
+                W = Ui @ Om
+            else:
+                raise ValueError(projection)
+            t.mark("3_qr")
+            Qs.append(_qr_pos(W))
+        t.mark("5_core")
+        g = T
+        for i, Q in enumerate(Qs):
+            g = mode_product(g, Q, i)
+        t.mark("end")
+    return {"core": g, "Q": Qs, "times_ms": t.result()}
+
+
+def hosvd_error(T, core, Qs) -> float:
+    """||A - g x_1 Q_1 ... x_N Q_N||_F / ||A||_F in FP64."""
+    R = core.double()
+    for i, Q in enumerate(Qs):
+        R = mode_product(R, Q.double().t(), i)
+    T64 = T.double()
+    return float(torch.linalg.norm(T64 - R) / torch.linalg.norm(T64))

@@ -144,3 +144,38 @@ def cauchy_like(N: int, seed: int) -> np.ndarray:
 
 def small_int_matrix(m: int, n: int, seed: int, lim: int = 8) -> np.ndarray:
     return rng(seed).integers(-lim, lim + 1, size=(m, n)).astype(np.float32)
+
+
+def spectrum_matrix_torch(s, seed: int, device="cuda"):
+    """Same construction as spectrum_matrix(method='hadamard') with torch on `device` (FP64 math,
+    FP32 result) for the large RSVD input (16384^2): A = P1 (H/sqrtN) D1 diag(s) D2 (H/sqrtN) P2^T."""
+    import torch
+    s = torch.as_tensor(np.asarray(s), dtype=torch.float64, device=device)
+    N = s.shape[0]
+    assert N & (N - 1) == 0
+    g = rng(seed)
+    d1 = torch.as_tensor(g.choice([-1.0, 1.0], N), device=device)
+    d2 = torch.as_tensor(g.choice([-1.0, 1.0], N), device=device)
+    p1 = torch.as_tensor(np.argsort(g.permutation(N)), device=device)
+    p2 = torch.as_tensor(np.argsort(g.permutation(N)), device=device)
+
+    def fwht_rows(X):
+        n = X.shape[0]
+        h = 1
+        while h < n:
+            Xv = X.view(n // (2 * h), 2, h, -1)
+            a = Xv[:, 0].clone()
+            b = Xv[:, 1]
+            Xv[:, 0] = a + b
+            Xv[:, 1] = a - b
+            h *= 2
+        return X
+
+    M = torch.diag(s * d2)
+    M = fwht_rows(M) / np.sqrt(N)
+    M = M.t().contiguous()
+    M = M[:, p2]
+    M = d1[:, None] * M
+    A = fwht_rows(M) / np.sqrt(N)
+    A = A[p1]
+    return A.to(torch.float32).contiguous()

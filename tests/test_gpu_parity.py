@@ -300,3 +300,28 @@ def test_project_all_modes(shg, orc, dims):
         U = np.ascontiguousarray(pl.unfold(T, mode))
         om = orc.omega_f16(U.shape[1], n, seed=3, stream_id=mode)
         check_bars(orc, U, om, W)
+
+
+# ------------------------------------------------------------------------------------------ M-major A
+@pytest.mark.parametrize("m,k,n,tune", [(300, 1000, 50, None), (128, 4096, 256, None), (1000, 777, 272, None),
+                                        (77, 3000, 64, {"split_k": 5}), (200, 300, 40, {"force_simt": 1})])
+def test_shgemm_at_mmajor(shg, orc, m, k, n, tune):
+    """A given M-major (At = A^T row-major): the last-mode unfolding path of project()."""
+    A = synth.gaussian(m, k, seed=m + 3 * k)
+    At = torch.from_numpy(np.ascontiguousarray(A.T)).cuda()
+    Om = shg.gen_omega(k, n, seed=6)
+    Y = to_np(shg.shgemm_at(At, Om, tune=tune))
+    check_bars(orc, A, omega_bits(Om), Y)
+
+
+def test_project_fast_paths_large(shg, orc):
+    """Modes 0 (K-major), 1 (3-D K-major view, S = 256) and 2 (M-major, in place) on a tensor big
+    enough for the tensor-core path with split-K."""
+    from oracle import pipelines as pl
+    dims = (96, 128, 256)
+    T = synth.gaussian(int(np.prod(dims)), 1, seed=12).reshape(dims)
+    Tt = cuda(T)
+    for mode in range(3):
+        W = to_np(shg.project(Tt, mode, 48, seed=9))
+        U = np.ascontiguousarray(pl.unfold(T, mode))
+        check_bars(orc, U, orc.omega_f16(U.shape[1], 48, seed=9, stream_id=mode), W)

@@ -1,0 +1,84 @@
+"""GPU RandNLA harness vs the CPU oracle pipelines (north_star: RSVD and RP-HOSVD reconstruction
+errors within 1e-4 relative of the FP32 oracle pipeline; readings R10, R12-R15 of DESIGN.md)."""
+import numpy as np
+import pytest
+
+import synth
+from gpu_common import omega_bits, to_np
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def shg():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2304_04612_b200 import _build
+    _build.build()
+    import paper_2304_04612_b200 as m
+    return m
+
+
+@pytest.fixture(scope="module")
+def pl(shg):
+    from paper_2304_04612_b200 import pipelines
+    return pipelines
+
+
+def test_fp32_baseline_omega_rounds_to_fp16_omega(shg, pl):
+    Om16 = shg.gen_omega(3000, 40, seed=7, stream_id=2)
+    Om32 = pl.omega_fp32(3000, 40, seed=7, stream_id=2)
+    assert torch.equal(Om32.half(), Om16)
+
+
+@pytest.mark.parametrize("kind", ["linear", "exp"])
+@pytest.mark.parametrize("projection", ["shgemm", "sgemm"])
+def test_rsvd_matches_oracle_pipeline(shg, pl, kind, projection):
+    from oracle import pipelines as opl
+    N, p, s, s_p = 512, 22, 10, 1e-2
+    A = synth.spectrum_matrix(synth.spectrum(kind, N, p, s_p), seed=3)
+    r = pl.rsvd(torch.from_numpy(A).cuda(), p, s, seed=4, projection=projection)
+    e_gpu = pl.reconstruction_error(torch.from_numpy(A).cuda(), r["U"], r["S"], r["V"])
+    e_or = opl.rsvd(A, p, s, seed=4, precision="f32")["residual"]
+    floor = synth.eckart_young_floor(kind, N, p, s_p) / float(np.linalg.norm(A.astype(np.float64)))
+    assert e_gpu >= floor * (1 - 1e-5)
+    assert abs(e_gpu - e_or) <= 1e-4 * e_or, (e_gpu, e_or)
+
+
+def test_rsvd_exact_rank(shg, pl):
+    rng = np.random.default_rng(0)
+    A = (rng.standard_normal((600, 20)) @ rng.standard_normal((20, 500))).astype(np.float32)
+    r = pl.rsvd(torch.from_numpy(A).cuda(), 20, 10, seed=1)
+    assert pl.reconstruction_error(torch.from_numpy(A).cuda(), r["U"], r["S"], r["V"]) <= 1e-5
+
+
+def test_rp_hosvd_matches_oracle_pipeline(shg, pl):
+    from oracle import pipelines as opl
+    T = synth.alg3_tensor((64, 48, 40), (16, 16, 16), pad=4, seed=5, noise=1e-2)
+    r = pl.rp_hosvd(torch.from_numpy(T).cuda(), (16, 16, 16), seed=2)
+    e_gpu = pl.hosvd_error(torch.from_numpy(T).cuda(), r["core"], r["Q"])
+    e_or = opl.rp_hosvd(T, (16, 16, 16), seed=2, precision="f32")["residual"]
+    assert e_gpu > 1e-3
+    assert abs(e_gpu - e_or) <= 1e-4 * e_or, (e_gpu, e_or)
+    T0 = synth.alg3_tensor((64, 48, 40), (16, 16, 16), pad=4, seed=5)
+    r0 = pl.rp_hosvd(torch.from_numpy(T0).cuda(), (16, 16, 16), seed=2)
+    assert pl.hosvd_error(torch.from_numpy(T0).cuda(), r0["core"], r0["Q"]) <= 1e-5
+
+
+def test_rsvd_config2_full_size(shg, pl):
+    """BASELINE config 2: RSVD of a 16384^2 FP32 matrix with a prescribed spectrum, rank 256 + 16.
+    GPU pipeline vs the oracle FP32 pipeline on the same input and Omega; Eckart-Young floor."""
+    from oracle import pipelines as opl
+    N, p, s, s_p = 16384, 256, 16, 1e-2
+    sig = synth.spectrum("exp", N, p, s_p)
+    A = synth.spectrum_matrix_torch(sig, seed=1)
+    r = pl.rsvd(A, p, s, seed=0, timing=True)
+    e_gpu = pl.reconstruction_error(A, r["U"], r["S"], r["V"])
+    A_h = to_np(A)
+    del A, r
+    torch.cuda.empty_cache()
+    e_or = opl.rsvd(A_h, p, s, seed=0, precision="f32")["residual"]
+    floor = synth.eckart_young_floor("exp", N, p, s_p) / float(np.linalg.norm(A_h.astype(np.float64)))
+    assert e_gpu >= floor * (1 - 1e-4)
+    assert abs(e_gpu - e_or) <= 1e-4 * e_or, (e_gpu, e_or)
