@@ -12,14 +12,17 @@
 //                 packed f32x2 arithmetic, and write hi and lo straight into TENSOR MEMORY with
 //                 tcgen05.st — the MMA takes A from TMEM, so hi/lo never touch shared memory
 //                 (measured: smem bandwidth was the bound with an smem A operand).
-//  * Omega      : TMA streams the 64 x BN FP16 tile (K-major SW128) into an SB-deep smem ring.
-//  * MMA        : one thread issues, per 64-k stage and per N-half (H0 + H1 = BN columns),
-//                 4 lo MMAs (D := lo.Omega) then 4 hi MMAs, the first with scale-input-d = 11
+//  * Omega      : TMA streams the 64 x BN FP16 tiles (K-major SW128) of a chunk into smem.
+//  * Chunks     : K_c = 128 = 2 stages; a chunk slot = 2 TMEM A stages + 2 Omega smem stages, with
+//                 ONE ready barrier (8 splitter arrivals + the Omega TMA bytes) and ONE empty
+//                 barrier (tcgen05.commit) — every mbarrier wait costs ~90 cycles on the MMA thread.
+//  * MMA        : one thread issues, per chunk and per N-part (H0 + H1 = BN columns), 8 lo MMAs
+//                 (D := sum lo.Omega) then 8 hi MMAs, the first with scale-input-d = 11
 //                 (D := hi.Omega + D * 2^-11), so D holds hi.Omega + 2^-11 lo.Omega (Eq 16) for
-//                 the stage. D half-accumulators rotate through NSLOT TMEM slots.
-//  * Promotion  : 8 epilogue warps (4 lane quarters x 2 N-halves) tcgen05.ld each finished D and
+//                 the chunk. Part accumulators rotate through NSLOT TMEM slots.
+//  * Promotion  : 8 epilogue warps (4 lane quarters x 2 N-parts) tcgen05.ld each finished D and
 //                 add it with RN (add.rn.f32x2) into register accumulators: the RZ-avoidance of
-//                 PAPER.md:587 applied per K_c = 64 chunk (and to lo as well: reading c4-2).
+//                 PAPER.md:587 applied per K_c = 128 chunk (and to lo as well: reading R2).
 //  * Epilogue   : after the last stage, the RN accumulators are written to Y (row-major) with
 //                 128-bit stores, masked on ragged edges; split-K tiles write to a workspace
 //                 plane that splitk_reduce_kernel sums in fixed order.
