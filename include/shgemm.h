@@ -67,9 +67,10 @@ typedef struct {
     int32_t max_ctas;    /* persistent grid size cap; 0 = number of SMs */
     int32_t force_simt;  /* 1 = force the CUDA-core fallback (tests) */
     /* Diagnostics only (results are WRONG when debug_flags != 0): bit0 skip the TMEM->register
-     * promotion loads, bit1 skip the splitter arithmetic, bit2 skip the MMAs. */
+     * promotion loads, bit1 skip the splitter arithmetic, bit2 skip the MMAs, bit3 skip the Omega
+     * loads. */
     int32_t debug_flags;
-    int32_t reserved;
+    int32_t pair;        /* CTA pairs (tcgen05.mma.cta_group::2): 0 auto (BN >= 128 and m > 128), 1 on, 2 off */
     /* Diagnostics: device int64[grid * 16] per-CTA wait-cycle counters (layout in
      * csrc/shgemm_sm100.cuh, enum ProfSlot), or NULL. */
     int64_t *prof;
@@ -80,6 +81,7 @@ typedef struct {
     int32_t path;        /* 0 = tcgen05 mainloop, 1 = SIMT fallback, 2 = trivial (no GEMM) */
     int32_t bn, n_tiles, m_tiles, split_k, grid, stages_a, stages_b, smem_bytes;
     int32_t kernels;     /* kernel launches one call makes */
+    int32_t cta_pair;    /* 1 if the mainloop runs as CTA pairs (cluster of 2, cta_group::2) */
     int64_t workspace_bytes;
 } shg_plan_t;
 
@@ -197,6 +199,10 @@ shg_status_t shg_probe_umma(const uint16_t *A, const uint16_t *B, int n, const f
  * accumulators; out[cta] (device floats) = cycles per MMA. */
 shg_status_t shg_probe_mma_rate(int n, int iters, int ts, int lsu_warps, float *out, int grid,
                                 shg_stream_t stream);
+
+/* Same for tcgen05.mma.cta_group::2 (clusters of 2 CTAs, M = 256, n % 32 == 0): out[cluster] =
+ * cycles per pair-MMA instruction (256 x n x 16 MACs on two SMs). */
+shg_status_t shg_probe_mma2_rate(int n, int iters, int ts, float *out, int clusters, shg_stream_t stream);
 
 #ifdef __cplusplus
 }

@@ -35,7 +35,7 @@ class SHGError(RuntimeError):
 
 class Tune(ctypes.Structure):
     _fields_ = [("bn", ctypes.c_int32), ("split_k", ctypes.c_int32), ("max_ctas", ctypes.c_int32),
-                ("force_simt", ctypes.c_int32), ("debug_flags", ctypes.c_int32), ("reserved", ctypes.c_int32),
+                ("force_simt", ctypes.c_int32), ("debug_flags", ctypes.c_int32), ("pair", ctypes.c_int32),
                 ("prof", ctypes.c_void_p)]
 
 
@@ -43,7 +43,7 @@ class Plan(ctypes.Structure):
     _fields_ = [("path", ctypes.c_int32), ("bn", ctypes.c_int32), ("n_tiles", ctypes.c_int32),
                 ("m_tiles", ctypes.c_int32), ("split_k", ctypes.c_int32), ("grid", ctypes.c_int32),
                 ("stages_a", ctypes.c_int32), ("stages_b", ctypes.c_int32), ("smem_bytes", ctypes.c_int32),
-                ("kernels", ctypes.c_int32), ("workspace_bytes", ctypes.c_int64)]
+                ("kernels", ctypes.c_int32), ("cta_pair", ctypes.c_int32), ("workspace_bytes", ctypes.c_int64)]
 
 
 def lib():
@@ -79,6 +79,8 @@ def lib():
             L.shg_probe_umma.argtypes = [vp, vp, i32, vp, i32, i32, vp, vp]
             L.shg_probe_mma_rate.argtypes = [i32, i32, i32, i32, vp, i32, vp]
             L.shg_probe_mma_rate.restype = i32
+            L.shg_probe_mma2_rate.argtypes = [i32, i32, i32, vp, i32, vp]
+            L.shg_probe_mma2_rate.restype = i32
             for name in ("shgemm", "shgemm_ex", "shgemm_at", "shgemm_host", "shg_plan", "gen_omega_f16", "gen_omega_f16_ex", "project",
                          "shg_debug_split", "shg_synth_f32", "shg_probe_umma"):
                 getattr(L, name).restype = i32

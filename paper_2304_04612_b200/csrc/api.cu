@@ -87,13 +87,13 @@ bool encode_a(CUtensorMap* map, const float* A, int64_t S, int64_t M, int64_t P,
               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-// Omega (column-major k x n == n rows of ldo halves): dims {k, n}, box {64, bn}
-bool encode_b(CUtensorMap* map, const uint16_t* Om, int64_t k, int64_t n, int64_t ldo, int bn) {
+// Omega (column-major k x n == n rows of ldo halves): dims {k, n}, box {64 k, rows}
+bool encode_b(CUtensorMap* map, const uint16_t* Om, int64_t k, int64_t n, int64_t ldo, int rows) {
     EncodeFn fn = encode_fn();
     if (!fn) return false;
     cuuint64_t dims[2] = {static_cast<cuuint64_t>(k), static_cast<cuuint64_t>(n)};
     cuuint64_t strides[1] = {static_cast<cuuint64_t>(ldo) * 2};
-    cuuint32_t box[2] = {64, static_cast<cuuint32_t>(bn)};
+    cuuint32_t box[2] = {64, static_cast<cuuint32_t>(rows)};
     cuuint32_t estr[2] = {1, 1};
     return fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, const_cast<uint16_t*>(Om), dims, strides, box, estr,
               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -116,13 +116,25 @@ constexpr int kBNs[] = {32, 64, 96, 128, 144, 160, 192, 224, 256};
         default: { constexpr int BN_ = 256; EXPR; }              \
     }
 
-int smem_for_bn(int bn) { SHG_BN_SWITCH(bn, return shg::Cfg<BN_>::kSmemBytes) }
-int sa_for_bn(int bn) { SHG_BN_SWITCH(bn, return shg::Cfg<BN_>::SA) }
-int sb_for_bn(int bn) { SHG_BN_SWITCH(bn, return shg::Cfg<BN_>::SO) }
+// CTA pairs (cta_group::2) are instantiated for BN >= 128, where Omega traffic matters
+constexpr bool pair_ok(int bn) { return bn >= 128; }
+
+template <int B> using CfgPair = shg::Cfg<B, true>;
+template <int B> using CfgSingle = shg::Cfg<B, false>;
+#define SHG_CFG_FIELD(bn, pair, FIELD)                                                                    \
+    if (pair) { SHG_BN_SWITCH(bn, return CfgPair<BN_>::FIELD) }                                           \
+    SHG_BN_SWITCH(bn, return CfgSingle<BN_>::FIELD)
+
+int smem_for(int bn, bool pair) { SHG_CFG_FIELD(bn, pair, kSmemBytes) }
+int sa_for(int bn, bool pair) { SHG_CFG_FIELD(bn, pair, SA) }
+int so_for(int bn, bool pair) { SHG_CFG_FIELD(bn, pair, SO) }
+int r0_for(int bn, bool pair) { SHG_CFG_FIELD(bn, pair, R0) }
+int r1_for(int bn, bool pair) { SHG_CFG_FIELD(bn, pair, R1) }
 
 struct Plan {
     int path = 0;  // 0 tc, 1 simt, 2 trivial
     int bn = 0, n_tiles = 0, m_tiles = 0, splits = 1, grid = 0, num_kb = 0;
+    bool pair = false;
     int64_t ws_bytes = 0, ld_ws = 0;
 };
 
@@ -145,22 +157,28 @@ Plan make_plan(int64_t m, int64_t n, int64_t k, bool fast_ok, const shg_tune_t* 
         pl.bn = 256;
         for (int b : kBNs) if (b >= need) { pl.bn = b; break; }
     }
-    pl.m_tiles = static_cast<int>((m + shg::kBM - 1) / shg::kBM);
+    // CTA pair: halves Omega's L2->SMEM traffic per SM (the power-cap lever at BN >= 128); needs > 128 rows
+    const int pair_mode = tune ? tune->pair : 0;   // 0 auto, 1 force on, 2 force off
+    pl.pair = pair_ok(pl.bn) && ((pair_mode == 0 && m > shg::kBM) || pair_mode == 1);
+    const int tile_m = pl.pair ? 2 * shg::kBM : shg::kBM;
+    const int slots = pl.pair ? std::max(1, sms / 2) : sms;     // concurrent tiles
+    pl.m_tiles = static_cast<int>((m + tile_m - 1) / tile_m);
     pl.num_kb = static_cast<int>((k + shg::kBK - 1) / shg::kBK);
     const int64_t mn_tiles = static_cast<int64_t>(pl.m_tiles) * pl.n_tiles;
     int splits = 1;
     if (tune && tune->split_k > 0) {
         splits = tune->split_k;
-    } else if (mn_tiles < sms) {
+    } else if (mn_tiles < slots) {
         // fill the SMs with k-splits, keeping >= 4 k-blocks (256 k) per split
-        splits = static_cast<int>(std::max<int64_t>(1, sms / mn_tiles));
+        splits = static_cast<int>(std::max<int64_t>(1, slots / mn_tiles));
         splits = static_cast<int>(std::min<int64_t>(splits, std::max<int64_t>(1, pl.num_kb / 4)));
     }
     splits = std::max(1, std::min(splits, pl.num_kb));
     pl.splits = splits;
     const int64_t tiles = mn_tiles * splits;
-    const int cap = (tune && tune->max_ctas > 0) ? tune->max_ctas : sms;
-    pl.grid = static_cast<int>(std::min<int64_t>(tiles, cap));
+    int cap = (tune && tune->max_ctas > 0) ? tune->max_ctas : sms;
+    if (pl.pair) cap = std::max(2, cap / 2 * 2);
+    pl.grid = static_cast<int>(std::min<int64_t>(tiles * (pl.pair ? 2 : 1), cap));
     if (splits > 1) {
         pl.ld_ws = (n + 3) / 4 * 4;
         pl.ws_bytes = static_cast<int64_t>(splits) * m * pl.ld_ws * 4;
@@ -170,32 +188,68 @@ Plan make_plan(int64_t m, int64_t n, int64_t k, bool fast_ok, const shg_tune_t* 
 
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 
-template <int BN, bool MMAJOR>
-shg_status_t launch_tc(const CUtensorMap& mapA, const CUtensorMap& mapB, const shg::KParams& kp, int grid,
-                       cudaStream_t stream) {
-    using CF = shg::Cfg<BN>;
+template <int BN, bool MMAJOR, bool PAIR>
+shg_status_t launch_tc(const CUtensorMap& mapA, const CUtensorMap& mapB0, const CUtensorMap& mapB1,
+                       const shg::KParams& kp, int grid, cudaStream_t stream) {
+    using CF = shg::Cfg<BN, PAIR>;
+    auto kern = shg::shgemm_sm100_kernel<BN, MMAJOR, PAIR>;
     static std::once_flag flags[64];
     int dev = 0;
     cudaGetDevice(&dev);
     cudaError_t attr_err = cudaSuccess;
     std::call_once(flags[std::min(std::max(dev, 0), 63)], [&]() {
-        attr_err = cudaFuncSetAttribute(shg::shgemm_sm100_kernel<BN, MMAJOR>,
-                                        cudaFuncAttributeMaxDynamicSharedMemorySize, CF::kSmemBytes);
+        attr_err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, CF::kSmemBytes);
     });
     if (attr_err != cudaSuccess) return cuda_fail(attr_err, "cudaFuncSetAttribute");
-    shg::shgemm_sm100_kernel<BN, MMAJOR><<<grid, shg::kThreads, CF::kSmemBytes, stream>>>(mapA, mapB, kp);
+    if constexpr (!PAIR) {
+        // plain launch: a cluster-dimension attribute (even 1x1x1) takes a slower launch path
+        kern<<<grid, shg::kThreads, CF::kSmemBytes, stream>>>(mapA, mapB0, mapB1, kp);
+        g_launches.fetch_add(1, std::memory_order_relaxed);
+        SHG_CUDA(cudaGetLastError());
+        return SHG_OK;
+    }
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(shg::kThreads);
+    cfg.dynamicSmemBytes = CF::kSmemBytes;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = PAIR ? 2 : 1;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    SHG_CUDA(cudaLaunchKernelEx(&cfg, kern, mapA, mapB0, mapB1, kp));
     g_launches.fetch_add(1, std::memory_order_relaxed);
-    SHG_CUDA(cudaGetLastError());
     return SHG_OK;
 }
 
-shg_status_t dispatch_tc(int bn, bool mmajor, const CUtensorMap& a, const CUtensorMap& b, const shg::KParams& kp,
-                         int grid, cudaStream_t s) {
-    if (!valid_bn(bn)) return SHG_ERR_INVALID_VALUE;
-    if (mmajor) {
-        SHG_BN_SWITCH(bn, return (launch_tc<BN_, true>(a, b, kp, grid, s)))
+template <bool MMAJOR, bool PAIR>
+shg_status_t dispatch_bn(int bn, const CUtensorMap& a, const CUtensorMap& b0, const CUtensorMap& b1,
+                         const shg::KParams& kp, int grid, cudaStream_t s) {
+    if constexpr (PAIR) {
+        switch (bn) {
+            case 128: return launch_tc<128, MMAJOR, true>(a, b0, b1, kp, grid, s);
+            case 144: return launch_tc<144, MMAJOR, true>(a, b0, b1, kp, grid, s);
+            case 160: return launch_tc<160, MMAJOR, true>(a, b0, b1, kp, grid, s);
+            case 192: return launch_tc<192, MMAJOR, true>(a, b0, b1, kp, grid, s);
+            case 224: return launch_tc<224, MMAJOR, true>(a, b0, b1, kp, grid, s);
+            case 256: return launch_tc<256, MMAJOR, true>(a, b0, b1, kp, grid, s);
+            default: return SHG_ERR_INVALID_VALUE;
+        }
+    } else {
+        SHG_BN_SWITCH(bn, return (launch_tc<BN_, MMAJOR, false>(a, b0, b1, kp, grid, s)))
     }
-    SHG_BN_SWITCH(bn, return (launch_tc<BN_, false>(a, b, kp, grid, s)))
+}
+
+shg_status_t dispatch_tc(int bn, bool mmajor, bool pair, const CUtensorMap& a, const CUtensorMap& b0,
+                         const CUtensorMap& b1, const shg::KParams& kp, int grid, cudaStream_t s) {
+    if (!valid_bn(bn) || (pair && !pair_ok(bn))) return SHG_ERR_INVALID_VALUE;
+    if (mmajor) return pair ? dispatch_bn<true, true>(bn, a, b0, b1, kp, grid, s)
+                            : dispatch_bn<true, false>(bn, a, b0, b1, kp, grid, s);
+    return pair ? dispatch_bn<false, true>(bn, a, b0, b1, kp, grid, s)
+                : dispatch_bn<false, false>(bn, a, b0, b1, kp, grid, s);
 }
 
 // M-major A (element (i, l) at A[l * lda + i]): 2-D map {M, K}, box {32 rows, 64 k}
@@ -249,14 +303,16 @@ shg_status_t run_shgemm(int64_t m, int64_t n, int64_t k, const AView& av, const 
         SHG_CUDA(cudaGetLastError());
         return SHG_OK;
     }
-    CUtensorMap mapA, mapB;
+    CUtensorMap mapA, mapB0, mapB1;
     const bool enc_ok = av.mmajor ? encode_a_mmajor(&mapA, av.A, m, k, av.row_stride)
                                   : encode_a(&mapA, av.A, av.S, m, av.P, av.row_stride, av.slab);
     if (!enc_ok) {
         std::snprintf(g_err, sizeof(g_err), "cuTensorMapEncodeTiled(A) failed");
         return SHG_ERR_CUDA;
     }
-    if (!encode_b(&mapB, Om, k, n, ldo, pl.bn)) {
+    // pair: one box per N-part half (R0 / R1 rows); single CTA: one box of all BN rows (mapB0)
+    const int rows0 = pl.pair ? r0_for(pl.bn, true) : pl.bn;
+    if (!encode_b(&mapB0, Om, k, n, ldo, rows0) || !encode_b(&mapB1, Om, k, n, ldo, r1_for(pl.bn, pl.pair))) {
         std::snprintf(g_err, sizeof(g_err), "cuTensorMapEncodeTiled(Omega) failed");
         return SHG_ERR_CUDA;
     }
@@ -290,7 +346,7 @@ shg_status_t run_shgemm(int64_t m, int64_t n, int64_t k, const AView& av, const 
         kp.vec_store = (aligned16(Y) && ldc % 4 == 0) ? 1 : 0;
         kp.nonfinite = nonfinite;
     }
-    shg_status_t st = dispatch_tc(pl.bn, av.mmajor, mapA, mapB, kp, pl.grid, stream);
+    shg_status_t st = dispatch_tc(pl.bn, av.mmajor, pl.pair, mapA, mapB0, mapB1, kp, pl.grid, stream);
     if (st != SHG_OK) return st;
     if (pl.splits > 1) {
         shg::splitk_reduce_kernel<<<grid_for(m * n, 256), 256, 0, stream>>>(kp.out, pl.splits, m, n, pl.ld_ws,
@@ -436,9 +492,10 @@ shg_status_t shg_plan(int64_t m, int64_t n, int64_t k, const shg_tune_t* tune, s
     out->bn = pl.bn; out->n_tiles = pl.n_tiles; out->m_tiles = pl.m_tiles; out->split_k = pl.splits;
     out->grid = pl.grid;
     if (pl.path == 0) {
-        out->stages_a = sa_for_bn(pl.bn);
-        out->stages_b = sb_for_bn(pl.bn);
-        out->smem_bytes = smem_for_bn(pl.bn);
+        out->stages_a = sa_for(pl.bn, pl.pair);
+        out->stages_b = so_for(pl.bn, pl.pair);
+        out->smem_bytes = smem_for(pl.bn, pl.pair);
+        out->cta_pair = pl.pair ? 1 : 0;
         out->kernels = pl.splits > 1 ? 2 : 1;
     } else {
         out->kernels = pl.path == 1 ? 1 : (k == 0 && m > 0 && n > 0 ? 0 : 0);

@@ -186,3 +186,80 @@ extern "C" shg_status_t shg_probe_mma_rate(int n, int iters, int ts, int lsu_war
     shg::probe_mma_rate_kernel<<<grid, 256, smem, reinterpret_cast<cudaStream_t>(stream)>>>(n, iters, ts, lsu_warps, out, nacc);
     return cudaGetLastError() == cudaSuccess ? SHG_OK : SHG_ERR_CUDA;
 }
+
+// ------------------------------------------------------------------ cta_group::2 MMA rate
+// Clusters of 2 CTAs; the leader issues `iters` tcgen05.mma.cta_group::2.kind::f16 with M = 256
+// (128 rows per CTA), N = n, K = 16, A from TMEM (ts) or smem, B halves (n/2 rows) in each CTA's
+// smem. out[cluster] = cycles per MMA instruction (each does 256 x n x 16 MACs on two SMs).
+namespace shg {
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128, 1)
+probe_mma2_rate_kernel(int n, int iters, int ts, float* out) {
+    extern __shared__ uint8_t smem_raw[];
+    const uint32_t raw_addr = smem_u32(smem_raw);
+    uint8_t* base = smem_raw + ((1024u - (raw_addr & 1023u)) & 1023u);
+    uint8_t* sA = base;                  // 128 rows x 128 B
+    uint8_t* sB = base + 16384;          // up to 128 rows x 128 B (n/2 rows)
+    uint64_t* bar = reinterpret_cast<uint64_t*>(base + 32768);
+    uint32_t* tslot = reinterpret_cast<uint32_t*>(bar + 1);
+    uint32_t rank;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(rank));
+    const uint32_t warp = warp_id();
+    for (int i = threadIdx.x; i < 32768 / 16; i += blockDim.x)
+        reinterpret_cast<uint4*>(base)[i] = make_uint4(0x3C003C00u, 0x3C003C00u, 0, 0);
+    fence_proxy_async_smem();
+    if (threadIdx.x == 0) { mbar_init(bar, 1); fence_mbar_init(); }
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tslot)) : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+    }
+    tc_fence_before();
+    asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+    tc_fence_after();
+    const uint32_t tbase = *tslot;
+    if (rank == 0 && warp == 0) {
+        if (elect_one()) {
+            const uint32_t idesc = idesc_f16_f32(256, static_cast<uint32_t>(n));
+            const uint64_t ad = sw128_kmajor_desc(smem_u32(sA));
+            const uint64_t bd = sw128_kmajor_desc(smem_u32(sB));
+            const long long t0 = clock64();
+            for (int i = 0; i < iters; ++i) {
+                const uint32_t j = static_cast<uint32_t>(i & 3);
+                if (ts) {
+                    asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, 1, 0;\n\t"
+                                 "tcgen05.mma.cta_group::2.kind::f16 [%0], [%1], %2, %3, p;\n\t}\n"
+                                 ::"r"(tbase), "r"(tbase + 448 + 8 * j), "l"(bd + 2 * j), "r"(idesc) : "memory");
+                } else {
+                    asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, 1, 0;\n\t"
+                                 "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}\n"
+                                 ::"r"(tbase), "l"(ad + 2 * j), "l"(bd + 2 * j), "r"(idesc) : "memory");
+                }
+            }
+            asm volatile("tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;"
+                         ::"r"(smem_u32(bar)), "h"(static_cast<uint16_t>(3)) : "memory");
+            mbar_wait(bar, 0);
+            const long long t1 = clock64();
+            uint32_t cid;
+            asm volatile("mov.u32 %0, %%clusterid.x;" : "=r"(cid));
+            out[cid] = static_cast<float>(t1 - t0) / static_cast<float>(iters);
+        }
+        __syncwarp();
+    } else if (rank == 1 && threadIdx.x == 0) {
+        mbar_wait(bar, 0);
+    }
+    tc_fence_before();
+    asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+    if (warp == 0) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;" ::"r"(tbase) : "memory");
+    }
+}
+}  // namespace shg
+
+extern "C" shg_status_t shg_probe_mma2_rate(int n, int iters, int ts, float* out, int clusters, shg_stream_t stream) {
+    if (!out || n < 32 || n > 256 || (n % 32) || iters < 1 || clusters < 1) return SHG_ERR_INVALID_VALUE;
+    const int smem = 1024 + 32768 + 64;
+    cudaError_t e = cudaFuncSetAttribute(shg::probe_mma2_rate_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return SHG_ERR_CUDA;
+    shg::probe_mma2_rate_kernel<<<2 * clusters, 128, smem, reinterpret_cast<cudaStream_t>(stream)>>>(n, iters, ts, out);
+    return cudaGetLastError() == cudaSuccess ? SHG_OK : SHG_ERR_CUDA;
+}

@@ -6,16 +6,16 @@
 // The A100 design (WMMA, RN add after every f_k = 8 mma) is prior art, not the
 // blueprint; this kernel re-derives it for tcgen05:
 //
-//  * A stager   : TMA (3-D map, SWIZZLE_128B) streams 128 x 64 FP32 tiles into an SA-deep smem ring.
+//  * A stager   : TMA streams 128 x 64 FP32 tiles (K-major: 3-D map, or M-major: 2-D map) into an
+//                 SA-deep smem ring (SWIZZLE_128B).
 //  * Splitter   : 8 warps (2 per TMEM lane quarter, one per 32-k half) read their rows of the FP32
-//                 tile (conflict-free LDS.128 through the swizzle), apply split2 (Eqs 14-15) with
-//                 packed f32x2 arithmetic, and write hi and lo straight into TENSOR MEMORY with
-//                 tcgen05.st — the MMA takes A from TMEM, so hi/lo never touch shared memory
-//                 (measured: smem bandwidth was the bound with an smem A operand).
-//  * Omega      : TMA streams the 64 x BN FP16 tiles (K-major SW128) of a chunk into smem.
+//                 tile (conflict-free shared loads through the swizzle), apply split2 (Eqs 14-15)
+//                 with packed f32x2 arithmetic, and write hi and lo straight into TENSOR MEMORY with
+//                 tcgen05.st — the MMA takes A from TMEM, so hi/lo never touch shared memory.
+//  * Omega      : TMA streams the 64-k Omega tiles (K-major SW128) of a chunk into smem.
 //  * Chunks     : K_c = 128 = 2 stages; a chunk slot = 2 TMEM A stages + 2 Omega smem stages, with
-//                 ONE ready barrier (8 splitter arrivals + the Omega TMA bytes) and ONE empty
-//                 barrier (tcgen05.commit) — every mbarrier wait costs ~90 cycles on the MMA thread.
+//                 ONE ready barrier (splitter arrivals + the Omega TMA bytes) and ONE empty barrier
+//                 (tcgen05.commit) — every mbarrier wait costs ~90 cycles on the MMA thread.
 //  * MMA        : one thread issues, per chunk and per N-part (H0 + H1 = BN columns), 8 lo MMAs
 //                 (D := sum lo.Omega) then 8 hi MMAs, the first with scale-input-d = 11
 //                 (D := hi.Omega + D * 2^-11), so D holds hi.Omega + 2^-11 lo.Omega (Eq 16) for
@@ -23,11 +23,15 @@
 //  * Promotion  : 8 epilogue warps (4 lane quarters x 2 N-parts) tcgen05.ld each finished D and
 //                 add it with RN (add.rn.f32x2) into register accumulators: the RZ-avoidance of
 //                 PAPER.md:587 applied per K_c = 128 chunk (and to lo as well: reading R2).
-//  * Epilogue   : after the last stage, the RN accumulators are written to Y (row-major) with
-//                 128-bit stores, masked on ragged edges; split-K tiles write to a workspace
-//                 plane that splitk_reduce_kernel sums in fixed order.
+//  * Epilogue   : after the last chunk, the RN accumulators are written to Y (row-major) with
+//                 128-bit stores, masked on ragged edges; split-K tiles write to a workspace plane
+//                 that splitk_reduce_kernel sums in fixed order.
+//  * PAIR       : optional CTA pair (cluster of 2, tcgen05.mma.cta_group::2, M = 256): each CTA
+//                 splits its own 128 rows and holds HALF of every Omega part tile, the leader issues
+//                 the MMAs for both — Omega's L2->SMEM traffic per SM halves (measured: Omega
+//                 traffic costs ~1/3 of the clock under the 1000 W power cap).
 //
-// One CTA per SM (smem-bound), persistent over tiles (m-block, k-split, n-block), n fastest.
+// One CTA (or CTA pair) per SM (pair), persistent over tiles (m-block, k-split, n-block), n fastest.
 #pragma once
 #include <cstdint>
 #include <cstdio>
@@ -37,9 +41,9 @@
 
 namespace shg {
 
-constexpr int kBM = 128;                          // UMMA M (cta_group::1)
+constexpr int kBM = 128;                          // rows per CTA (UMMA M per CTA)
 constexpr int kBK = 64;                           // k per stage: one 128-B swizzle row of FP16
-constexpr int kA32StageBytes = kBM * kBK * 4;     // 32 KB (two 16 KB TMA boxes of 32 FP32 columns)
+constexpr int kA32StageBytes = kBM * kBK * 4;     // 32 KB
 constexpr int kNumSplitWarps = 8;                 // warps 0..7
 constexpr int kEpiWarp0 = 8;                      // warps 8..15
 constexpr int kWarpProdA = 16, kWarpMMA = 17, kWarpProdB = 18;   // warp 19 idle
@@ -49,18 +53,20 @@ constexpr int kThreads = 640;
 constexpr int kSmemLimit = 232448;                // max dynamic smem per block on sm_100
 constexpr int kTmemCols = 512;
 constexpr int kAStageCols = 64;                   // hi 32 + lo 32 columns (2 FP16 per 32-bit column)
+constexpr uint32_t kPeerBitMask = 0xFEFFFFFFu;    // shared::cluster address of the even CTA's copy
 
 struct KParams {
     int64_t m, n, k;
     int64_t k_inner;        // S: contiguous k run of the A view (k for a plain matrix)
     int32_t num_kb;         // ceil(k / 64)
-    int32_t m_tiles, n_tiles, splits;
+    int32_t m_tiles, n_tiles, splits;   // m_tiles counts 128-row (single) or 256-row (pair) tiles
     float* out;             // Y, or the split-K workspace when splits > 1
     int64_t ldo_out;        // leading dimension of out (elements)
     int64_t split_stride;   // elements between split planes (workspace)
     int32_t vec_store;      // out rows 16-B aligned and ldo_out % 4 == 0
     int* nonfinite;         // optional flag (set to 1 on any non-finite output)
-    uint32_t dbg;           // diagnostics: bit0 skip promotion loads, bit1 skip split math, bit2 skip MMAs
+    uint32_t dbg;           // diagnostics: bit0 skip promotion loads, bit1 skip split math, bit2 skip MMAs,
+                            //              bit3 skip the Omega TMA (results are wrong when dbg != 0)
     long long* prof;        // diagnostics: per-CTA wait-cycle counters [gridDim.x][16] (ProfSlot)
 };
 
@@ -84,38 +90,78 @@ __device__ __forceinline__ void watchdog_report(uint64_t* bar, uint32_t parity) 
     asm volatile("trap;");
 }
 
+// try_wait with cluster-scope acquire (barriers that receive arrivals from the peer CTA)
+__device__ __forceinline__ bool mbar_try_wait_cluster(uint64_t* bar, uint32_t parity) {
+    uint32_t ok;
+    asm volatile(
+        "{\n\t.reg .pred P;\n\t"
+        "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, P;\n\t}\n"
+        : "=r"(ok) : "r"(smem_u32(bar)), "r"(parity) : "memory");
+    return ok != 0;
+}
+
+// CLUSTER selects acquire.cluster. The pair path does NOT use it: its remote arrivals are relaxed
+// (they carry no data) and acquire.cluster emits CCTL.IVALL (an L1 invalidate) on every success.
+template <bool CLUSTER = false>
 __device__ __forceinline__ void mbar_wait_prof(uint64_t* bar, uint32_t parity, long long& acc) {
     const long long t0 = clock64();
     uint32_t spins = 0;
-    while (!mbar_try_wait(bar, parity)) {
+    while (!(CLUSTER ? mbar_try_wait_cluster(bar, parity) : mbar_try_wait(bar, parity))) {
         if (++spins == (1u << 22)) watchdog_report(bar, parity);
     }
     acc += clock64() - t0;
 }
 
-template <int BN>
+// arrive on the copy of `bar` (a local smem address) in CTA `cta` of the cluster. RELAXED: the only
+// data these arrivals publish is tensor memory, already ordered by tcgen05.wait::st /
+// tcgen05.fence::before_thread_sync; a .release.cluster arrive would emit MEMBAR.ALL.GPU (measured
+// ~1000 cycles per handoff on the MMA thread's critical path).
+__device__ __forceinline__ void mbar_arrive_cluster(uint64_t* bar, uint32_t cta) {
+    asm volatile(
+        "{\n\t.reg .b32 ra;\n\t"
+        "mapa.shared::cluster.u32 ra, %0, %1;\n\t"
+        "mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [ra];\n\t}\n"
+        ::"r"(smem_u32(bar)), "r"(cta) : "memory");
+}
+
+__device__ __forceinline__ uint32_t cluster_ctarank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+
+__device__ __forceinline__ void cluster_sync_all() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
+template <int BN, bool PAIR>
 struct Cfg {
     // K_c = 128: one promotion chunk = 2 stages of 64 k. TMEM: 4 A stages (2 chunks of hi/lo,
-    // 64 columns each) + accumulator slots; N is covered by 2 part-MMAs of widths H0 + H1 = BN so
+    // 64 columns each) + accumulator slots; N is covered by 2 part-MMAs of widths W + WLAST = BN so
     // that the drain of one part overlaps the MMAs of the other.
     static constexpr int KC = 2;                           // stages per promotion chunk
     static constexpr int NCH = 2;                          // chunk slots (TMEM A + Omega smem)
     static constexpr int NQ = 2;
-    static constexpr int W = ((BN / 2) + 15) / 16 * 16;    // H0
-    static constexpr int WLAST = BN - W;                   // H1
+    static constexpr int W = ((BN / 2) + 15) / 16 * 16;    // width of part 0
+    static constexpr int WLAST = BN - W;                   // width of part 1
     static constexpr int NPH = 1;                          // parts per epilogue group
     static constexpr int SB = NCH * KC;                    // TMEM A stage slots
     static constexpr int ABASE = kTmemCols - SB * kAStageCols;
     static constexpr int NSLOT_fit = ABASE / W;
     static constexpr int NSLOT = NSLOT_fit > 4 ? 4 : NSLOT_fit;
     static constexpr int SO = NCH * KC;                    // Omega smem stages
-    static constexpr int kOmStageBytes = BN * kBK * 2;
+    static constexpr int R0 = PAIR ? W / 2 : W;            // Omega rows of part 0 held by this CTA
+    static constexpr int R1 = PAIR ? WLAST / 2 : WLAST;    // Omega rows of part 1 held by this CTA
+    static constexpr int kOmStageBytes = (R0 + R1) * kBK * 2;
+    static constexpr int kTileM = PAIR ? 2 * kBM : kBM;   // rows per (pair) tile
     static constexpr int kBarBytes = 512;
     static constexpr int SA_fit = (kSmemLimit - 1024 - kBarBytes - SO * kOmStageBytes) / kA32StageBytes;
     static constexpr int SA = SA_fit > 6 ? 6 : SA_fit;
     static constexpr int kSmemBytes = 1024 + SA * kA32StageBytes + SO * kOmStageBytes + kBarBytes;
     static_assert(BN % 16 == 0 && BN >= 32 && BN <= 256, "BN");
-    static_assert(WLAST >= 16 && WLAST % 16 == 0 && W <= 128, "UMMA N parts for M=128");
+    static_assert(WLAST >= 16 && WLAST % 16 == 0 && W <= 128, "UMMA N parts");
+    static_assert(!PAIR || (R0 % 8 == 0 && R1 % 8 == 0), "pair halves must be whole 8-row core groups");
     static_assert(NSLOT >= NQ, "TMEM accumulator slots");
     static_assert(SA >= 2 && kSmemBytes <= kSmemLimit, "smem");
 };
@@ -145,25 +191,73 @@ __device__ __forceinline__ void advance(uint32_t& stage, uint32_t& phase, uint32
     if (++stage == n) { stage = 0; phase ^= 1u; }
 }
 
-// D[tmem] (+)= A[tmem] * B[smem]  (A operand from tensor memory, "TS" form)
+// D[tmem] (+)= A[tmem] * B[smem]  (A operand from tensor memory, "TS" form), 1 CTA or CTA pair
+template <bool PAIR>
 __device__ __forceinline__ void mma_f16_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t bdesc, uint32_t idesc,
                                            uint32_t accumulate) {
-    asm volatile(
-        "{\n\t.reg .pred p;\n\t"
-        "setp.ne.b32 p, %4, 0;\n\t"
-        "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}\n"
-        ::"r"(tmem_d), "r"(tmem_a), "l"(bdesc), "r"(idesc), "r"(accumulate)
-        : "memory");
+    if constexpr (PAIR) {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "setp.ne.b32 p, %4, 0;\n\t"
+            "tcgen05.mma.cta_group::2.kind::f16 [%0], [%1], %2, %3, p;\n\t}\n"
+            ::"r"(tmem_d), "r"(tmem_a), "l"(bdesc), "r"(idesc), "r"(accumulate)
+            : "memory");
+    } else {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "setp.ne.b32 p, %4, 0;\n\t"
+            "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}\n"
+            ::"r"(tmem_d), "r"(tmem_a), "l"(bdesc), "r"(idesc), "r"(accumulate)
+            : "memory");
+    }
 }
 
 // D[tmem] = A[tmem] * B[smem] + D * 2^-11  (scale-input-d = 11, sm_100a)
+template <bool PAIR>
 __device__ __forceinline__ void mma_f16_ts_scale11(uint32_t tmem_d, uint32_t tmem_a, uint64_t bdesc, uint32_t idesc) {
-    asm volatile(
-        "{\n\t.reg .pred p;\n\t"
-        "setp.ne.b32 p, 1, 0;\n\t"
-        "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p, 11;\n\t}\n"
-        ::"r"(tmem_d), "r"(tmem_a), "l"(bdesc), "r"(idesc)
-        : "memory");
+    if constexpr (PAIR) {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "setp.ne.b32 p, 1, 0;\n\t"
+            "tcgen05.mma.cta_group::2.kind::f16 [%0], [%1], %2, %3, p, 11;\n\t}\n"
+            ::"r"(tmem_d), "r"(tmem_a), "l"(bdesc), "r"(idesc)
+            : "memory");
+    } else {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "setp.ne.b32 p, 1, 0;\n\t"
+            "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p, 11;\n\t}\n"
+            ::"r"(tmem_d), "r"(tmem_a), "l"(bdesc), "r"(idesc)
+            : "memory");
+    }
+}
+
+// completion of this thread's prior tcgen05 ops -> one arrive on `bar` (in both CTAs of a pair)
+template <bool PAIR>
+__device__ __forceinline__ void commit_to(uint64_t* bar) {
+    if constexpr (PAIR) {
+        asm volatile(
+            "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;"
+            ::"r"(smem_u32(bar)), "h"(static_cast<uint16_t>(3)) : "memory");
+    } else {
+        tc_commit(bar);
+    }
+}
+
+// Omega tile load; in a pair the transaction bytes land on the leader's (even CTA's) barrier
+template <bool PAIR>
+__device__ __forceinline__ void tma_load_omega(void* smem_dst, const CUtensorMap* map, uint64_t* bar, int32_t c0,
+                                               int32_t c1, uint64_t policy) {
+    if constexpr (PAIR) {
+        asm volatile(
+            "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+            " [%0], [%1, {%3, %4}], [%2], %5;"
+            ::"r"(smem_u32(smem_dst)), "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar) & kPeerBitMask),
+              "r"(c0), "r"(c1), "l"(policy)
+            : "memory");
+    } else {
+        tma_load_2d(smem_dst, map, bar, c0, c1, policy);
+    }
 }
 
 __device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&r)[16]) {
@@ -173,12 +267,6 @@ __device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&r)[16
         ::"r"(taddr), "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]),
           "r"(r[8]), "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15])
         : "memory");
-}
-
-__device__ __forceinline__ void tmem_st8(uint32_t taddr, const uint32_t (&r)[8]) {
-    asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};"
-                 ::"r"(taddr), "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7])
-                 : "memory");
 }
 
 __device__ __forceinline__ void tmem_ld8(uint32_t taddr, float (&v)[8]) {
@@ -214,14 +302,17 @@ __device__ __forceinline__ void add2_rn(float& a, float& b, float c, float d) {
 //                 C-order tensor); each stage is four TMA boxes of 32 rows x 64 k, and the splitter
 //                 gathers its row's k values with conflict-free 32-bit loads (one 128-B smem row per
 //                 warp instruction) — no transpose copy.
-template <int BN, bool MMAJOR>
+// PAIR          : CTA pair (launch with cluster dims (2,1,1)); see the header comment.
+template <int BN, bool MMAJOR, bool PAIR>
 __global__ void __launch_bounds__(kThreads, 1)
-shgemm_sm100_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
-                    const KParams p) {
-    using CF = Cfg<BN>;
-    constexpr int SA = CF::SA, SB = CF::SB, SO = CF::SO, NQ = CF::NQ, W = CF::W, WLAST = CF::WLAST;
+shgemm_sm100_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB0,
+                    const __grid_constant__ CUtensorMap mapB1, const KParams p) {
+    using CF = Cfg<BN, PAIR>;
+    constexpr int SA = CF::SA, NQ = CF::NQ, W = CF::W, WLAST = CF::WLAST;
     constexpr int NPH = CF::NPH, NSLOT = CF::NSLOT, ABASE = CF::ABASE;
     constexpr int kOm = CF::kOmStageBytes;
+    constexpr int NCH = CF::NCH, KC = CF::KC;
+    constexpr int SO = CF::SO;
 
     extern __shared__ uint8_t smem_raw[];
     const uint32_t raw_addr = smem_u32(smem_raw);
@@ -229,31 +320,46 @@ shgemm_sm100_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_const
     uint8_t* a32 = base;
     uint8_t* om = a32 + SA * kA32StageBytes;
     uint64_t* bars = reinterpret_cast<uint64_t*>(om + SO * kOm);
-    constexpr int NCH = CF::NCH, KC = CF::KC;
     uint64_t* a_full = bars;                 // TMA A landed                        (count 1 + tx)
     uint64_t* a_empty = a_full + SA;         // splitters done reading              (count 8)
-    uint64_t* ch_ready = a_empty + SA;       // chunk hi/lo in TMEM + Omega in smem (count 8 + 1 + tx)
+    uint64_t* ch_ready = a_empty + SA;       // chunk hi/lo in TMEM + Omega in smem (leader: count 8|16 + 1|2 + tx)
     uint64_t* ch_empty = ch_ready + NCH;     // MMAs done with the chunk slot       (tcgen05.commit)
     uint64_t* acc_full = ch_empty + NCH;     // D slot complete                     (tcgen05.commit)
-    uint64_t* acc_empty = acc_full + NSLOT;  // D slot drained               (count 4)
+    uint64_t* acc_empty = acc_full + NSLOT;  // D slot drained                      (leader: count 4|8)
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + NSLOT);
 
     const uint32_t warp = warp_id();
     const uint32_t lane = threadIdx.x & 31u;
+    const uint32_t crank = PAIR ? cluster_ctarank() : 0u;      // 0 = leader (issues the MMAs)
+    const int cta_of_tile = PAIR ? static_cast<int>(blockIdx.x >> 1) : static_cast<int>(blockIdx.x);
+    const int tile_stride = PAIR ? static_cast<int>(gridDim.x >> 1) : static_cast<int>(gridDim.x);
+    constexpr int kPair = PAIR ? 2 : 1;
 
     if (threadIdx.x == 0) {
         for (int i = 0; i < SA; ++i) { mbar_init(&a_full[i], 1); mbar_init(&a_empty[i], kNumSplitWarps); }
-        for (int i = 0; i < NCH; ++i) { mbar_init(&ch_ready[i], kNumSplitWarps + 1); mbar_init(&ch_empty[i], 1); }
-        for (int i = 0; i < NSLOT; ++i) { mbar_init(&acc_full[i], 1); mbar_init(&acc_empty[i], 4); }
+        for (int i = 0; i < NCH; ++i) {
+            mbar_init(&ch_ready[i], kPair * (kNumSplitWarps + 1));
+            mbar_init(&ch_empty[i], 1);
+        }
+        for (int i = 0; i < NSLOT; ++i) { mbar_init(&acc_full[i], 1); mbar_init(&acc_empty[i], 4 * kPair); }
         fence_mbar_init();
     }
     if (warp == kWarpProdA && lane == 0) {
         tma_prefetch_desc(&mapA);
-        tma_prefetch_desc(&mapB);
+        tma_prefetch_desc(&mapB0);
+        tma_prefetch_desc(&mapB1);
     }
-    if (warp == kWarpMMA) tmem_alloc<kTmemCols>(tmem_slot);
+    if (warp == kWarpMMA) {
+        if constexpr (PAIR) {
+            asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;"
+                         ::"r"(smem_u32(tmem_slot)), "n"(kTmemCols) : "memory");
+            asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+        } else {
+            tmem_alloc<kTmemCols>(tmem_slot);
+        }
+    }
     tc_fence_before();
-    __syncthreads();
+    if constexpr (PAIR) cluster_sync_all(); else __syncthreads();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
 
@@ -265,14 +371,14 @@ shgemm_sm100_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_const
         asm volatile("setmaxnreg.dec.sync.aligned.u32 56;");
         const int q = static_cast<int>(warp & 3u);        // TMEM lane quarter = rows 32q..32q+31
         const int kh = static_cast<int>(warp >> 2);       // k half of the stage: 32kh .. 32kh+31
-        const int r = 32 * q + static_cast<int>(lane);    // tile row owned by this thread
+        const int r = 32 * q + static_cast<int>(lane);    // tile row (of this CTA) owned by this thread
         const int rx = r & 7;                             // SW128 XOR term of this row
         const uint32_t lane_addr = static_cast<uint32_t>(32 * q) << 16;
         uint32_t sa = 0, pa = 0, cs = 0, pc = 0;
         long long w_a = 0, w_b = 0, stages = 0;
         const long long t_begin = clock64();
         const bool skip_math = (p.dbg & 2u) != 0;
-        for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+        for (int tile = cta_of_tile; tile < num_tiles; tile += tile_stride) {
             int m_blk, s, n_blk, kb0, kb1;
             tile_coords(tile, p, m_blk, s, n_blk);
             kb_range(s, p, kb0, kb1);
@@ -330,7 +436,10 @@ shgemm_sm100_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_const
                 tmem_st_wait();
                 tc_fence_before();
                 __syncwarp();
-                if (lane == 0) mbar_arrive(&ch_ready[cs]);
+                if (lane == 0) {
+                    if constexpr (PAIR) mbar_arrive_cluster(&ch_ready[cs], 0u);
+                    else mbar_arrive(&ch_ready[cs]);
+                }
                 advance(cs, pc, NCH);
             }
         }
@@ -350,7 +459,7 @@ shgemm_sm100_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_const
         uint32_t stage = 0;
         long long w_full = 0, t_store = 0;
         const bool skip_ld = (p.dbg & 1u) != 0;
-        for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+        for (int tile = cta_of_tile; tile < num_tiles; tile += tile_stride) {
             int m_blk, s, n_blk, kb0, kb1;
             tile_coords(tile, p, m_blk, s, n_blk);
             kb_range(s, p, kb0, kb1);
@@ -388,12 +497,16 @@ shgemm_sm100_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_const
                     }
                     tc_fence_before();
                     __syncwarp();
-                    if (lane == 0) mbar_arrive(&acc_empty[slot]);
+                    if (lane == 0) {
+                        if constexpr (PAIR) mbar_arrive_cluster(&acc_empty[slot], 0u);
+                        else mbar_arrive(&acc_empty[slot]);
+                    }
                 }
             }
             // ---- store the tile rows owned by this thread (its parts' columns)
             const long long ts0 = clock64();
-            const int64_t row = static_cast<int64_t>(m_blk) * kBM + 32 * q + static_cast<int>(lane);
+            const int64_t row = static_cast<int64_t>(m_blk) * CF::kTileM + static_cast<int64_t>(crank) * kBM + 32 * q +
+                                static_cast<int>(lane);
             if (row < p.m) {
 #pragma unroll
                 for (int j = 0; j < NPH; ++j) {
@@ -433,16 +546,16 @@ shgemm_sm100_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_const
     } else {
         asm volatile("setmaxnreg.dec.sync.aligned.u32 32;");
         if (warp == kWarpProdA) {
-            // ======================================================== A stager (TMA, FP32)
+            // ======================================================== A stager (TMA, FP32, own rows)
             if (elect_one()) {
                 const uint64_t pol = policy_evict_first();
                 uint32_t sa = 0, pa = 0;
                 long long w = 0;
-                for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+                for (int tile = cta_of_tile; tile < num_tiles; tile += tile_stride) {
                     int m_blk, s, n_blk, kb0, kb1;
                     tile_coords(tile, p, m_blk, s, n_blk);
                     kb_range(s, p, kb0, kb1);
-                    const int m0 = m_blk * kBM;
+                    const int m0 = m_blk * CF::kTileM + static_cast<int>(crank) * kBM;
                     for (int kb = kb0; kb < kb1; ++kb) {
                         mbar_wait_prof(&a_empty[sa], pa ^ 1u, w);
                         mbar_arrive_expect_tx(&a_full[sa], kA32StageBytes);
@@ -467,11 +580,13 @@ shgemm_sm100_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_const
             }
         } else if (warp == kWarpProdB) {
             // ======================================================== Omega stager (TMA, FP16)
+            // per stage and per N-part one box: part 0 rows [n0 + crank*R0, +R0), part 1 rows
+            // [n0 + W + crank*R1, +R1) (pair: each CTA holds its half of every part)
             if (elect_one()) {
                 const uint64_t pol = policy_evict_last();
                 uint32_t cs = 0, pc = 0;
                 long long w = 0;
-                for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+                for (int tile = cta_of_tile; tile < num_tiles; tile += tile_stride) {
                     int m_blk, s, n_blk, kb0, kb1;
                     tile_coords(tile, p, m_blk, s, n_blk);
                     kb_range(s, p, kb0, kb1);
@@ -479,21 +594,37 @@ shgemm_sm100_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_const
                     for (int kb = kb0; kb < kb1; kb += KC) {
                         const int nst = (kb1 - kb) < KC ? (kb1 - kb) : KC;
                         mbar_wait_prof(&ch_empty[cs], pc ^ 1u, w);
-                        mbar_arrive_expect_tx(&ch_ready[cs], static_cast<uint32_t>(nst * kOm));
-                        for (int t = 0; t < nst; ++t)
-                            tma_load_2d(om + (cs * KC + t) * kOm, &mapB, &ch_ready[cs], kb_global(kb + t, s, p) * kBK,
-                                        n0, pol);
+                        const bool skip = (p.dbg & 8u) != 0;      // diagnostics: stale Omega (power study)
+                        if (crank == 0) {
+                            mbar_arrive_expect_tx(&ch_ready[cs], skip ? 0u : static_cast<uint32_t>(kPair * nst * kOm));
+                        } else {
+                            mbar_arrive_cluster(&ch_ready[cs], 0u);
+                        }
+                        if (!skip) {
+                            for (int t = 0; t < nst; ++t) {
+                                uint8_t* dst = om + (cs * KC + t) * kOm;
+                                const int kcoord = kb_global(kb + t, s, p) * kBK;
+                                if constexpr (PAIR) {
+                                    tma_load_omega<PAIR>(dst, &mapB0, &ch_ready[cs], kcoord,
+                                                         n0 + static_cast<int>(crank) * CF::R0, pol);
+                                    tma_load_omega<PAIR>(dst + CF::R0 * 128, &mapB1, &ch_ready[cs], kcoord,
+                                                         n0 + W + static_cast<int>(crank) * CF::R1, pol);
+                                } else {   // the two parts are contiguous rows: one box of BN rows (mapB0)
+                                    tma_load_omega<PAIR>(dst, &mapB0, &ch_ready[cs], kcoord, n0, pol);
+                                }
+                            }
+                        }
                         advance(cs, pc, NCH);
                     }
                 }
                 if (p.prof) p.prof[blockIdx.x * kProfSlots + kProfProdBEmpty] = w;
             }
-        } else if (warp == kWarpMMA) {
+        } else if (warp == kWarpMMA && crank == 0) {
             // ======================================================== MMA issuer (tcgen05, A from TMEM)
             uint32_t cs = 0, pc = 0, g = 0;
             long long w_acc = 0, w_hl = 0, w_om = 0;
             const bool skip_mma = (p.dbg & 4u) != 0;
-            for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+            for (int tile = cta_of_tile; tile < num_tiles; tile += tile_stride) {
                 int m_blk, s, n_blk, kb0, kb1;
                 tile_coords(tile, p, m_blk, s, n_blk);
                 kb_range(s, p, kb0, kb1);
@@ -510,17 +641,17 @@ shgemm_sm100_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_const
                         if (elect_one()) {
                             if (!skip_mma) {
                                 const uint32_t d = tmem_base + slot * W;
-                                const uint32_t idesc = idesc_f16_f32(kBM, part == NQ - 1 ? WLAST : W);
-                                const uint64_t b = b_base + static_cast<uint64_t>((part * W * 128) >> 4);
+                                const uint32_t idesc = idesc_f16_f32(CF::kTileM, part == NQ - 1 ? WLAST : W);
+                                const uint64_t b = b_base + static_cast<uint64_t>(((part ? CF::R0 : 0) * 128) >> 4);
                                 // D := sum over the chunk's stages of lo . Omega  (Eq 16's dA_low term)
 #pragma unroll
                                 for (int t = 0; t < KC; ++t)
                                     if (t < nst)
 #pragma unroll
                                         for (int j = 0; j < 4; ++j)
-                                            mma_f16_ts(d, a_base + t * kAStageCols + 32 + 8 * j,
-                                                       b + static_cast<uint64_t>((t * kOm) >> 4) + 2 * j, idesc,
-                                                       (t > 0 || j > 0) ? 1u : 0u);
+                                            mma_f16_ts<PAIR>(d, a_base + t * kAStageCols + 32 + 8 * j,
+                                                             b + static_cast<uint64_t>((t * kOm) >> 4) + 2 * j, idesc,
+                                                             (t > 0 || j > 0) ? 1u : 0u);
                                 // D := hi . Omega + D * 2^-11 (first step), then the rest of hi
 #pragma unroll
                                 for (int t = 0; t < KC; ++t)
@@ -529,15 +660,15 @@ shgemm_sm100_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_const
                                         for (int j = 0; j < 4; ++j) {
                                             const uint32_t a = a_base + t * kAStageCols + 8 * j;
                                             const uint64_t bb = b + static_cast<uint64_t>((t * kOm) >> 4) + 2 * j;
-                                            if (t == 0 && j == 0) mma_f16_ts_scale11(d, a, bb, idesc);
-                                            else mma_f16_ts(d, a, bb, idesc, 1u);
+                                            if (t == 0 && j == 0) mma_f16_ts_scale11<PAIR>(d, a, bb, idesc);
+                                            else mma_f16_ts<PAIR>(d, a, bb, idesc, 1u);
                                         }
                             }
-                            tc_commit(&acc_full[slot]);
+                            commit_to<PAIR>(&acc_full[slot]);
                         }
                         __syncwarp();
                     }
-                    if (elect_one()) tc_commit(&ch_empty[cs]);
+                    if (elect_one()) commit_to<PAIR>(&ch_empty[cs]);
                     __syncwarp();
                     advance(cs, pc, NCH);
                 }
@@ -552,11 +683,16 @@ shgemm_sm100_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_const
     }
 
     tc_fence_before();
-    __syncthreads();
+    if constexpr (PAIR) cluster_sync_all(); else __syncthreads();
     if (p.prof && threadIdx.x == 0) p.prof[blockIdx.x * kProfSlots + kProfTotal] = clock64() - t_kernel0;
     if (warp == kWarpMMA) {
         tc_fence_after();
-        tmem_dealloc<kTmemCols>(tmem_base);
+        if constexpr (PAIR) {
+            asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "n"(kTmemCols)
+                         : "memory");
+        } else {
+            tmem_dealloc<kTmemCols>(tmem_base);
+        }
     }
 }
 

@@ -209,7 +209,8 @@ def test_shgemm_bars(shg, orc, m, k, n, kind):
     check_bars(orc, A, om, Y)
 
 
-@pytest.mark.parametrize("tune", [{"force_simt": 1}, {"split_k": 3}, {"bn": 64}, {"max_ctas": 3}])
+@pytest.mark.parametrize("tune", [{"force_simt": 1}, {"split_k": 3}, {"bn": 64}, {"max_ctas": 3}, {"pair": 1},
+                                  {"pair": 2}, {"pair": 1, "bn": 144}, {"pair": 1, "split_k": 2, "max_ctas": 6}])
 def test_shgemm_tunables(shg, orc, tune):
     m, k, n = 400, 1500, 100
     A = synth.gaussian(m, k, seed=2)
@@ -325,3 +326,17 @@ def test_project_fast_paths_large(shg, orc):
         W = to_np(shg.project(Tt, mode, 48, seed=9))
         U = np.ascontiguousarray(pl.unfold(T, mode))
         check_bars(orc, U, orc.omega_f16(U.shape[1], 48, seed=9, stream_id=mode), W)
+
+
+@pytest.mark.parametrize("m,k,n,mmajor", [(129, 700, 200, False), (1000, 4096, 256, False), (700, 1024, 144, True),
+                                          (4096, 512, 128, True)])
+def test_cta_pair_mode(shg, orc, m, k, n, mmajor):
+    """tcgen05.mma.cta_group::2 mainloop (cluster of 2, Omega halves per CTA) incl. ragged pair tiles."""
+    A = synth.gaussian(m, k, seed=m + n)
+    Om = shg.gen_omega(k, n, seed=4)
+    assert shg.plan(m, n, k, {"pair": 1})["cta_pair"] == 1
+    if mmajor:
+        Y = to_np(shg.shgemm_at(torch.from_numpy(np.ascontiguousarray(A.T)).cuda(), Om, tune={"pair": 1}))
+    else:
+        Y = to_np(shg.shgemm(cuda(A), Om, tune={"pair": 1}))
+    check_bars(orc, A, omega_bits(Om), Y)
