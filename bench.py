@@ -234,12 +234,20 @@ def main():
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
+    ndev = max(1, torch.cuda.device_count())
+    local = int(os.environ.get("LOCAL_RANK", "0")) % ndev
     torch.cuda.set_device(local)
     dist = None
+    backend = None
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        # one rank per GPU over NCCL (the driver's launch); more ranks than GPUs (a functional test of
+        # the sharded path on one device) cannot share a GPU under NCCL, so that case uses gloo.
+        backend = "nccl" if world <= ndev else "gloo"
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group("gloo")
 
     m_total, k, n, desc = CONFIGS[args.config]
     # row sharding: rank g owns rows [g*ceil(m/G), min(m, (g+1)*ceil(m/G)))
@@ -298,7 +306,7 @@ def main():
     gemm_ms = statistics.mean(ev[i][1].elapsed_time(ev[i][2]) for i in range(args.steps))
     gen_ms = statistics.mean(ev[i][0].elapsed_time(ev[i][1]) for i in range(args.steps))
     if dist:
-        t = torch.tensor([total_ms], device="cuda")
+        t = torch.tensor([total_ms], device="cuda" if backend == "nccl" else "cpu")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         total_ms = float(t.item())
     ms_per_step = total_ms / args.steps
@@ -349,6 +357,7 @@ def main():
                "data": "synthetic",
                "config": {"workload": args.config, "description": desc, "m": m_total, "k": k, "n": n,
                           "rows_per_gpu": per, "parallelism": f"row-shard x{world} (no collective on the data path)",
+                          "dist_backend": backend,
                           "l2": "inputs larger than L2 (A is %.1f GiB per GPU), no flush" % (4.0 * m * k / 2 ** 30),
                           "plan": shg.plan(m, n, k)},
                "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,

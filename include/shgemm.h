@@ -71,6 +71,11 @@ typedef struct {
      * loads. */
     int32_t debug_flags;
     int32_t pair;        /* CTA pairs (tcgen05.mma.cta_group::2): 0 auto (BN >= 128 and m > 128), 1 on, 2 off */
+    int32_t a_box;       /* row-major A staging: 0 auto (2 if k % 32 == 0 and lda >= 2 MiB, else 1), 1 two TMA boxes of
+                            {32 k, 128 rows} per stage (128 B per row visit), 2 one box of
+                            {2 x 32 k, 128 rows} (256 B per row visit; needs k % 32 == 0, else
+                            SHG_ERR_INVALID_VALUE). Ignored for M-major A (shgemm_at). */
+    int32_t reserved;
     /* Diagnostics: device int64[grid * 16] per-CTA wait-cycle counters (layout in
      * csrc/shgemm_sm100.cuh, enum ProfSlot), or NULL. */
     int64_t *prof;
@@ -169,6 +174,18 @@ shg_status_t shg_debug_split(const float *a, int64_t count, uint16_t *hi, uint16
  * A[i*lda + l] = synth(seed, stream_id, global row row0 + i, column l), 0 <= i < m, 0 <= l < k. */
 shg_status_t shg_synth_f32(int kind, uint64_t seed, uint32_t stream_id, int64_t m, int64_t k, int64_t row0,
                            float *A, int64_t lda, shg_stream_t stream);
+
+/* TMA read-bandwidth probe (diagnostics): `grid` CTAs stream the full 128-row
+ * m-blocks of A (device, m x k FP32, row stride lda) into shared memory with TMA only, in the
+ * mainloop's tile order (m-block major, `splits` contiguous k ranges). Box per load:
+ *   layout 0: 2-D {box_k, box_rows}, no swizzle (box_k <= 256, multiple of 4)
+ *   layout 1: 2-D {32, box_rows}, 128-B swizzle (the mainloop's A box)
+ *   layout 2: 3-D {32, box_k/32, box_rows} over dims {32, k/32, m}, 128-B swizzle
+ * box_k * box_rows * 4 <= 32768, 128 % box_rows == 0. Adds the bytes loaded to *bytes_out (device
+ * u64). Time it with events on `stream`. */
+shg_status_t shg_probe_tma_read(const float *A, int64_t m, int64_t k, int64_t lda, int layout, int box_k,
+                                int box_rows, int splits, int grid, unsigned long long *bytes_out,
+                                shg_stream_t stream);
 
 /* Number of kernels this library has launched in this process (monotonic). */
 uint64_t shg_launch_count(void);

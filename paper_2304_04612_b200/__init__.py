@@ -36,6 +36,7 @@ class SHGError(RuntimeError):
 class Tune(ctypes.Structure):
     _fields_ = [("bn", ctypes.c_int32), ("split_k", ctypes.c_int32), ("max_ctas", ctypes.c_int32),
                 ("force_simt", ctypes.c_int32), ("debug_flags", ctypes.c_int32), ("pair", ctypes.c_int32),
+                ("a_box", ctypes.c_int32), ("reserved", ctypes.c_int32),
                 ("prof", ctypes.c_void_p)]
 
 
@@ -72,6 +73,7 @@ def lib():
             L.shg_host_workspace_size.restype = sz
             L.shg_debug_split.argtypes = [vp, i64, vp, vp, vp]
             L.shg_synth_f32.argtypes = [i32, u64, u32, i64, i64, i64, vp, i64, vp]
+            L.shg_probe_tma_read.argtypes = [vp, i64, i64, i64, i32, i32, i32, i32, i32, vp, vp]
             L.shg_launch_count.restype = u64
             L.shg_last_error.restype = ctypes.c_char_p
             L.shg_device_supported.restype = i32

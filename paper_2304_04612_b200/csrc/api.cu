@@ -13,6 +13,7 @@
 
 #include "../../include/shgemm.h"
 #include "omega.cuh"
+#include "probe_tma.cuh"
 #include "shgemm_sm100.cuh"
 #include "simt_fallback.cuh"
 #include "split.cuh"
@@ -83,6 +84,24 @@ bool encode_a(CUtensorMap* map, const float* A, int64_t S, int64_t M, int64_t P,
     cuuint32_t box[3] = {32, 128, 1};
     cuuint32_t estr[3] = {1, 1, 1};
     return fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(A), dims, strides, box, estr,
+              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+// Same view as a 4-D map {32, S/32, M, P} (S % 32 == 0), box {32, 2, 128, 1}: TMA walks the box
+// row by row, 256 B per row visit (twice encode_a's 128 B). Measured with shg_probe_tma_read on a
+// 1024 x 2^20 matrix: 4.5 TB/s for 128-B row visits vs 7.1 TB/s for 256-B (6.4 vs 7.1 at 256-KB
+// row strides) — each row visit costs a DRAM page / TLB lookup, so fewer, longer visits stream
+// faster (profiles/r01_tma_probe.jsonl).
+bool encode_a_rowpair(CUtensorMap* map, const float* A, int64_t S, int64_t M, int64_t P, int64_t row_stride_el,
+                      int64_t slab_stride_el) {
+    EncodeFn fn = encode_fn();
+    if (!fn || S % 32) return false;
+    cuuint64_t dims[4] = {32, static_cast<cuuint64_t>(S / 32), static_cast<cuuint64_t>(M), static_cast<cuuint64_t>(P)};
+    cuuint64_t strides[3] = {128, static_cast<cuuint64_t>(row_stride_el) * 4, static_cast<cuuint64_t>(slab_stride_el) * 4};
+    cuuint32_t box[4] = {32, 2, 128, 1};
+    cuuint32_t estr[4] = {1, 1, 1, 1};
+    return fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, const_cast<float*>(A), dims, strides, box, estr,
               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
@@ -304,7 +323,15 @@ shg_status_t run_shgemm(int64_t m, int64_t n, int64_t k, const AView& av, const 
         return SHG_OK;
     }
     CUtensorMap mapA, mapB0, mapB1;
+    // K-major A stage layout: 256-B row visits (encode_a_rowpair) when rows are >= 2 MiB apart, i.e.
+    // every row of a 128-row box sits in its own 2-MiB page (measured on 1024 x 2^20: 1.24 -> 0.79
+    // ms); at shorter strides the two-box layout measured 3-15% faster (profiles/r01_ab_abox.jsonl)
+    const int a_box = tune ? tune->a_box : 0;     // 0 auto, 1 128-B row visits, 2 256-B row visits
+    const bool rowpair_ok = !av.mmajor && av.S % 32 == 0;
+    const bool rowpair = rowpair_ok && (a_box == 2 || (a_box == 0 && av.row_stride * 4 >= (int64_t(2) << 20)));
+    if (a_box == 2 && !rowpair_ok) return SHG_ERR_INVALID_VALUE;
     const bool enc_ok = av.mmajor ? encode_a_mmajor(&mapA, av.A, m, k, av.row_stride)
+                        : rowpair ? encode_a_rowpair(&mapA, av.A, av.S, m, av.P, av.row_stride, av.slab)
                                   : encode_a(&mapA, av.A, av.S, m, av.P, av.row_stride, av.slab);
     if (!enc_ok) {
         std::snprintf(g_err, sizeof(g_err), "cuTensorMapEncodeTiled(A) failed");
@@ -321,6 +348,7 @@ shg_status_t run_shgemm(int64_t m, int64_t n, int64_t k, const AView& av, const 
     kp.k_inner = av.S;
     kp.num_kb = pl.num_kb;
     kp.m_tiles = pl.m_tiles; kp.n_tiles = pl.n_tiles; kp.splits = pl.splits;
+    kp.a_rowpair = rowpair ? 1 : 0;
     kp.dbg = tune ? static_cast<uint32_t>(tune->debug_flags) : 0u;
     kp.prof = tune ? reinterpret_cast<long long*>(tune->prof) : nullptr;
     void* own_ws = nullptr;
@@ -633,6 +661,49 @@ shg_status_t shgemm_host(int64_t m, int64_t n, int64_t k, const float* A_host, i
         SHG_CUDA(cudaStreamWaitEvent(us, hs.ev_done[b], 0));
     }
     if (own) SHG_CUDA(cudaFreeAsync(own, us));
+    return SHG_OK;
+}
+
+shg_status_t shg_probe_tma_read(const float* A, int64_t m, int64_t k, int64_t lda, int layout, int box_k,
+                                int box_rows, int splits, int grid, unsigned long long* bytes_out,
+                                shg_stream_t stream) {
+    if (!A || !bytes_out || m < 128 || k < 32 || lda < k || layout < 0 || layout > 2 || box_rows < 1 ||
+        box_rows > 128 || 128 % box_rows || box_k < 1 || splits < 1 || grid < 1)
+        return SHG_ERR_INVALID_VALUE;
+    if (static_cast<int64_t>(box_k) * box_rows * 4 > shg::kProbeStageBytes) return SHG_ERR_INVALID_VALUE;
+    if ((layout != 0 && (box_k % 32)) || (layout == 0 && (box_k > 256 || box_k % 4)) || (layout == 1 && box_k != 32))
+        return SHG_ERR_INVALID_VALUE;
+    if (layout == 2 && (box_k / 32 > 256 || k % 32)) return SHG_ERR_INVALID_VALUE;
+    EncodeFn fn = encode_fn();
+    if (!fn) return SHG_ERR_CUDA;
+    CUtensorMap map;
+    CUresult r;
+    if (layout == 2) {
+        cuuint64_t dims[3] = {32, static_cast<cuuint64_t>(k / 32), static_cast<cuuint64_t>(m)};
+        cuuint64_t strides[2] = {128, static_cast<cuuint64_t>(lda) * 4};
+        cuuint32_t box[3] = {32, static_cast<cuuint32_t>(box_k / 32), static_cast<cuuint32_t>(box_rows)};
+        cuuint32_t estr[3] = {1, 1, 1};
+        r = fn(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(A), dims, strides, box, estr,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    } else {
+        cuuint64_t dims[2] = {static_cast<cuuint64_t>(k), static_cast<cuuint64_t>(m)};
+        cuuint64_t strides[1] = {static_cast<cuuint64_t>(lda) * 4};
+        cuuint32_t box[2] = {static_cast<cuuint32_t>(box_k), static_cast<cuuint32_t>(box_rows)};
+        cuuint32_t estr[2] = {1, 1};
+        r = fn(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(A), dims, strides, box, estr,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, layout == 1 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
+               CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    }
+    if (r != CUDA_SUCCESS) return SHG_ERR_INVALID_VALUE;
+    const int smem = shg::kProbeStages * shg::kProbeStageBytes + 1024 + 64;
+    SHG_CUDA(cudaFuncSetAttribute(shg::probe_tma_read_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    const int m_tiles = static_cast<int>(m / 128);
+    const int num_ks = static_cast<int>(k / box_k);
+    shg::probe_tma_read_kernel<<<grid, 32, smem, reinterpret_cast<cudaStream_t>(stream)>>>(
+        map, layout, box_k, box_rows, m_tiles, splits, num_ks, bytes_out);
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    SHG_CUDA(cudaGetLastError());
     return SHG_OK;
 }
 

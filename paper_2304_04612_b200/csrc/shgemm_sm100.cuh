@@ -60,6 +60,9 @@ struct KParams {
     int64_t k_inner;        // S: contiguous k run of the A view (k for a plain matrix)
     int32_t num_kb;         // ceil(k / 64)
     int32_t m_tiles, n_tiles, splits;   // m_tiles counts 128-row (single) or 256-row (pair) tiles
+    int32_t a_rowpair;      // K-major A stage layout: 0 = two boxes {32 k, 128 rows} (k-half major,
+                            // 128 B fetched per row visit), 1 = one 4-D box {32, 2, 128 rows, 1}
+                            // (row major, 256 B per row visit; needs k_inner % 32 == 0)
     float* out;             // Y, or the split-K workspace when splits > 1
     int64_t ldo_out;        // leading dimension of out (elements)
     int64_t split_stride;   // elements between split planes (workspace)
@@ -372,7 +375,9 @@ shgemm_sm100_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_const
         const int q = static_cast<int>(warp & 3u);        // TMEM lane quarter = rows 32q..32q+31
         const int kh = static_cast<int>(warp >> 2);       // k half of the stage: 32kh .. 32kh+31
         const int r = 32 * q + static_cast<int>(lane);    // tile row (of this CTA) owned by this thread
-        const int rx = r & 7;                             // SW128 XOR term of this row
+        // this thread's 128-B line of the stage and its SW128 XOR term (line index & 7)
+        const int a_line = p.a_rowpair ? 2 * r + kh : kh * kBM + r;
+        const int rx = a_line & 7;
         const uint32_t lane_addr = static_cast<uint32_t>(32 * q) << 16;
         uint32_t sa = 0, pa = 0, cs = 0, pc = 0;
         long long w_a = 0, w_b = 0, stages = 0;
@@ -407,7 +412,7 @@ shgemm_sm100_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_const
                                 split2_x2(a0, a1, hi[i], lo[i]);
                             }
                         } else if (!skip_math) {
-                            const uint8_t* src = a32 + sa * kA32StageBytes + kh * (kA32StageBytes / 2) + r * 128;
+                            const uint8_t* src = a32 + sa * kA32StageBytes + a_line * 128;
 #pragma unroll
                             for (int c = 0; c < 4; ++c) {        // 8 k per chunk of the row
                                 const float4 x0 = *reinterpret_cast<const float4*>(src + (((2 * c) ^ rx) * 16));
@@ -569,6 +574,9 @@ shgemm_sm100_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_const
                             for (int b = 0; b < 4; ++b)
                                 tma_load_2d(dst + b * (kA32StageBytes / 4), &mapA, &a_full[sa], m0 + 32 * b,
                                             static_cast<int>(kk), pol);
+                        } else if (p.a_rowpair) {
+                            // 4-D map {32, S/32, M, P}: one box of 128 rows x (2 x 32 k), row major
+                            tma_load_4d(dst, &mapA, &a_full[sa], 0, c0 >> 5, m0, c2, pol);
                         } else {
                             tma_load_3d(dst, &mapA, &a_full[sa], c0, m0, c2, pol);
                             tma_load_3d(dst + kA32StageBytes / 2, &mapA, &a_full[sa], c0 + 32, m0, c2, pol);

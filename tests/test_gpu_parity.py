@@ -210,7 +210,8 @@ def test_shgemm_bars(shg, orc, m, k, n, kind):
 
 
 @pytest.mark.parametrize("tune", [{"force_simt": 1}, {"split_k": 3}, {"bn": 64}, {"max_ctas": 3}, {"pair": 1},
-                                  {"pair": 2}, {"pair": 1, "bn": 144}, {"pair": 1, "split_k": 2, "max_ctas": 6}])
+                                  {"pair": 2}, {"pair": 1, "bn": 144}, {"pair": 1, "split_k": 2, "max_ctas": 6},
+                                  {"a_box": 1}, {"a_box": 1, "pair": 1}, {"a_box": 1, "split_k": 4}])
 def test_shgemm_tunables(shg, orc, tune):
     m, k, n = 400, 1500, 100
     A = synth.gaussian(m, k, seed=2)
@@ -340,3 +341,17 @@ def test_cta_pair_mode(shg, orc, m, k, n, mmajor):
     else:
         Y = to_np(shg.shgemm(cuda(A), Om, tune={"pair": 1}))
     check_bars(orc, A, omega_bits(Om), Y)
+
+
+
+@pytest.mark.parametrize("m,k,n,tune", [(160, 1 << 19, 24, None), (200, 1 << 16, 40, {"a_box": 2}), (300, 4096 + 32, 144, {"a_box": 2, "pair": 1}),
+                                        (129, 96, 64, {"a_box": 2}), (300, 4096 + 32, 144, {"a_box": 1, "pair": 1})])
+def test_a_box_layouts(shg, orc, m, k, n, tune):
+    """Both row-major A staging layouts (two {32 k, 128 rows} boxes, or one {2 x 32 k, 128 rows}
+    row-major box, auto-selected for rows >= 2 MiB apart) incl. a k % 64 == 32 tail; a_box 2
+    without k % 32 == 0 is rejected."""
+    A = synth.gaussian(m, k, seed=k + m)
+    om, Y = _run(shg, A, k, n, tune=tune)
+    check_bars(orc, A, om, Y)
+    with pytest.raises(shg.SHGError):
+        shg.shgemm(cuda(synth.gaussian(64, 100, seed=1)), shg.gen_omega(100, 16), tune={"a_box": 2})

@@ -19,3 +19,12 @@ for sk in (0, 9, 18, 36):
     print(json.dumps(dict(mode='0-shgemm', split_k=sk, plan=shg.plan(1024, 64, 1 << 20, {'split_k': sk} if sk else None)['split_k'], ms=ms, gbs=4.0 * 2**30 / ms / 1e6)), flush=True)
 ms = t_ms(lambda: shg.gen_omega(1 << 20, 64))
 print(json.dumps(dict(gen_omega_2e20x64_ms=ms)))
+res = {}
+variants = [('auto', None), ('sk36', {'split_k': 36}), ('sk74', {'split_k': 74}), ('abox1', {'a_box': 1}),
+            ('abox2_sk36', {'a_box': 2, 'split_k': 36})]
+for rnd in range(3):
+    for name, tune in variants:
+        res.setdefault(name, []).append(t_ms(lambda: shg.shgemm(A, Om, tune=tune), reps=3))
+for name, tune in variants:
+    ms = sorted(res[name])[1]
+    print(json.dumps(dict(mode='0-shgemm', variant=name, split_k=shg.plan(1024, 64, 1 << 20, tune)['split_k'], ms=ms, gbs=4.0 * 2**30 / ms / 1e6)), flush=True)
