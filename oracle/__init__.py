@@ -61,7 +61,10 @@ def lib():
             L.orc_omega_element.restype = ctypes.c_uint16
             L.orc_omega_f16.argtypes = [i64, i64, u64, u32, i64, ctypes.c_int, i64, vp, i64]
             L.orc_split.argtypes = [vp, i64, vp, vp]
-            for name in ("orc_gemm_y64", "orc_gemm_y32", "orc_gemm_ysplit64"):
+            L.orc_split_tf32.argtypes = [vp, i64, vp, vp]
+            L.orc_f32_to_tf32_rn.argtypes = [ctypes.c_float]
+            L.orc_f32_to_tf32_rn.restype = u32
+            for name in ("orc_gemm_y64", "orc_gemm_y32", "orc_gemm_ysplit64", "orc_gemm_ysplit64_tf32"):
                 getattr(L, name).argtypes = [i64, vp, i64, i64, vp, i64, vp, i64, vp, i64]
             L.orc_gauss_f32.argtypes = [u64, u32, u64, u64]
             L.orc_gauss_f32.restype = ctypes.c_float
@@ -156,6 +159,20 @@ def split(a: np.ndarray):
     return hi, lo
 
 
+def split_tf32(a: np.ndarray):
+    """Eqs 14-15 with toLow = TF32 (SHGEMM-TF32). Returns (hi_bits, lo_bits) as uint32
+    FP32 bit patterns (low 13 bits zero)."""
+    a = np.ascontiguousarray(a, dtype=np.float32).reshape(-1)
+    hi = np.empty(a.size, dtype=np.uint32)
+    lo = np.empty(a.size, dtype=np.uint32)
+    lib().orc_split_tf32(_ptr(a), a.size, _ptr(hi), _ptr(lo))
+    return hi, lo
+
+
+def f32_to_tf32_bits(x: float) -> int:
+    return int(lib().orc_f32_to_tf32_rn(float(x)))
+
+
 # --------------------------------------------------------------------------- Ω
 def sparse_threshold(dist: int, k_total: int) -> int:
     return int(lib().orc_sparse_threshold(int(dist), int(k_total)))
@@ -212,6 +229,11 @@ def gemm_y32(A, omega_bits, rows=None) -> np.ndarray:
 def gemm_ysplit64(A, omega_bits, rows=None) -> np.ndarray:
     """Eq 16 in FP64: sum_l (hi + lo 2^-11) w."""
     return _gemm(lib().orc_gemm_ysplit64, np.float64, A, omega_bits, rows)
+
+
+def gemm_ysplit64_tf32(A, omega_bits, rows=None) -> np.ndarray:
+    """Eq 16 in FP64 with the TF32 split of SHGEMM-TF32."""
+    return _gemm(lib().orc_gemm_ysplit64_tf32, np.float64, A, omega_bits, rows)
 
 
 def relative_error(C, C_ref) -> float:

@@ -16,6 +16,9 @@
  *   orc_gemm_y32        naive single-precision GEMM (the "SGEMM" comparator of P:613):
  *                       acc = fmaf(A[i][l], Ω[l][j], acc), sequential in l
  *   orc_gemm_ysplit64   Eq 16 evaluated exactly in FP64: sum_l (hi + lo*2^-11) * Ω[l][j]
+ *   orc_f32_to_tf32_rn  RN ties-to-even to TF32 (e8m10), as FP32 bits with 13 zero low bits
+ *   orc_split_tf32      Eqs 14-15 with toLow = TF32: the SHGEMM-TF32 variant of P:494-498
+ *   orc_gemm_ysplit64_tf32  Eq 16 in FP64 with the TF32 hi/lo
  *   orc_unif_f32 / orc_gauss_f32   counter-based synthetic-input generator (same Philox, §6 of
  *                       OMEGA_SPEC), fp32 outputs, for regenerating sampled rows of device-made inputs
  *
@@ -245,6 +248,35 @@ void orc_split(const float *a, int64_t count, uint16_t *hi, uint16_t *lo) {
     }
 }
 
+/* ------------------------------------------------------------------ TF32 (SHGEMM-TF32) */
+/* RN ties-to-even of an FP32 value to TF32 = e8m10: the sign and 8-bit exponent are kept,
+ * the 23-bit fraction is rounded to its top 10 bits. On the FP32 encoding this is: drop the low 13
+ * bits, and add one unit of bit 13 when the dropped part exceeds half of it, or equals half and
+ * the kept part is odd. The carry may run into the exponent (correct: the next binade, or +-inf
+ * from the largest finite binade). Infinities pass through; NaNs stay NaN (quiet bit set). */
+uint32_t orc_f32_to_tf32_rn(float f) {
+    uint32_t x = f2u(f);
+    uint32_t sign = x & 0x80000000u, ax = x & 0x7FFFFFFFu;
+    if (ax > 0x7F800000u) return x | 0x00400000u;          /* NaN */
+    if (ax == 0x7F800000u) return x;                       /* inf */
+    uint32_t dropped = ax & 0x1FFFu, kept = ax & ~0x1FFFu;
+    if (dropped > 0x1000u || (dropped == 0x1000u && (kept & 0x2000u))) kept += 0x2000u;
+    return sign | kept;
+}
+
+/* Eqs 14-15 with toLow = TF32: hi = RN_tf32(a), lo = RN_tf32((a - hi) * 2^11).
+ * a - hi is exact (hi is a rounding of a to fewer bits of the same binade or the next one up) and
+ * x 2^11 is an exact exponent shift, except at the TF32 overflow edge (hi = +-inf, lo = -+inf). */
+void orc_split_tf32(const float *a, int64_t count, uint32_t *hi, uint32_t *lo) {
+    for (int64_t t = 0; t < count; ++t) {
+        uint32_t h = orc_f32_to_tf32_rn(a[t]);
+        float resid = a[t] - u2f(h);
+        float scaled = resid * 2048.0f;
+        hi[t] = h;
+        lo[t] = orc_f32_to_tf32_rn(scaled);
+    }
+}
+
 /* ------------------------------------------------------------------ GEMMs (A row-major m x k, Ω column-major) */
 /* Ω as a k x n row-major fp32/fp64 copy so the inner loop over j is contiguous. */
 static float *omega_rows_f32(int64_t k, int64_t n, const uint16_t *omega, int64_t ldo) {
@@ -320,6 +352,32 @@ void orc_gemm_ysplit64(int64_t nrows, const int64_t *rows, int64_t n, int64_t k,
                 uint16_t h, lo;
                 orc_split(&a[l], 1, &h, &lo);
                 double rec = (double)orc_f16_to_f32(h) + (double)orc_f16_to_f32(lo) * (1.0 / 2048.0);
+                const float *wl = w + l * n;
+                for (int64_t j = 0; j < n; ++j) acc[j] = acc[j] + rec * (double)wl[j];
+            }
+            for (int64_t j = 0; j < n; ++j) Y[r * ldy + j] = acc[j];
+        }
+        free(acc);
+    }
+    free(w);
+}
+
+/* Eq 16 in FP64 with the TF32 split (SHGEMM-TF32) */
+void orc_gemm_ysplit64_tf32(int64_t nrows, const int64_t *rows, int64_t n, int64_t k,
+                       const float *A, int64_t lda, const uint16_t *omega, int64_t ldo,
+                       double *Y, int64_t ldy) {
+    float *w = omega_rows_f32(k, n, omega, ldo);
+    #pragma omp parallel
+    {
+        double *acc = (double *)malloc(sizeof(double) * (size_t)(n > 0 ? n : 1));
+        #pragma omp for schedule(dynamic, 4)
+        for (int64_t r = 0; r < nrows; ++r) {
+            const float *a = A + (rows ? rows[r] : r) * lda;
+            for (int64_t j = 0; j < n; ++j) acc[j] = 0.0;
+            for (int64_t l = 0; l < k; ++l) {
+                uint32_t h, lo;
+                orc_split_tf32(&a[l], 1, &h, &lo);
+                double rec = (double)u2f(h) + (double)u2f(lo) * (1.0 / 2048.0);
                 const float *wl = w + l * n;
                 for (int64_t j = 0; j < n; ++j) acc[j] = acc[j] + rec * (double)wl[j];
             }

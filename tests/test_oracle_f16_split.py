@@ -18,7 +18,7 @@ def f16c(orc):
     libdir = os.path.dirname(orc.build())
     if not os.path.exists(out) or os.path.getmtime(out) < os.path.getmtime(src):
         subprocess.run(["gcc", "-O2", "-mf16c", "-fopenmp", "-fPIC", "-shared", "-o", out, src,
-                        "-L" + libdir, "-loracle", "-Wl,-rpath," + libdir], check=True)
+                        "-L" + libdir, "-loracle", "-lm", "-Wl,-rpath," + libdir], check=True)
     orc.lib()  # make sure liboracle is loaded globally first
     ctypes.CDLL(orc.build(), mode=ctypes.RTLD_GLOBAL)
     L = ctypes.CDLL(out)
