@@ -60,6 +60,13 @@ typedef enum {
     SHG_DIST_VERYSPARSE = 3   /* s = sqrt(k) (Li et al.), k = rows of the full Omega */
 } shg_dist_t;
 
+/* Tensor-core kind of the SHGEMM ("two kinds of SGEMM"). */
+typedef enum {
+    SHG_TC_FP16 = 0,  /* SHGEMM-FP16: toLow = FP16 (Eqs 14-17); |A| < 65520 (FP16 range) */
+    SHG_TC_TF32 = 1   /* SHGEMM-TF32: toLow = TF32 (e8m10): the full FP32 exponent range, Omega
+                         widened exactly to TF32; half the FP16 tensor-core rate */
+} shg_tc_t;
+
 /* Tunables for shgemm_ex. Zero-initialise for the heuristics. */
 typedef struct {
     int32_t bn;          /* N tile (multiple of 16, <= 256); 0 = heuristic */
@@ -75,7 +82,8 @@ typedef struct {
                             {32 k, 128 rows} per stage (128 B per row visit), 2 one box of
                             {2 x 32 k, 128 rows} (256 B per row visit; needs k % 32 == 0, else
                             SHG_ERR_INVALID_VALUE). Ignored for M-major A (shgemm_at). */
-    int32_t reserved;
+    int32_t tc;          /* shg_tc_t: SHG_TC_FP16 (0, default) or SHG_TC_TF32; selects the kernel, not a
+                            tuning: the results differ (TF32 keeps |a| >= 65520 finite) */
     /* Diagnostics: device int64[grid * 16] per-CTA wait-cycle counters (layout in
      * csrc/shgemm_sm100.cuh, enum ProfSlot), or NULL. */
     int64_t *prof;
@@ -87,6 +95,7 @@ typedef struct {
     int32_t bn, n_tiles, m_tiles, split_k, grid, stages_a, stages_b, smem_bytes;
     int32_t kernels;     /* kernel launches one call makes */
     int32_t cta_pair;    /* 1 if the mainloop runs as CTA pairs (cluster of 2, cta_group::2) */
+    int32_t tc;          /* shg_tc_t the plan runs */
     int64_t workspace_bytes;
 } shg_plan_t;
 
@@ -100,8 +109,16 @@ typedef struct {
 shg_status_t shgemm(int64_t m, int64_t n, int64_t k, const float *A, int64_t lda, const uint16_t *Omega,
                     int64_t ldo, float *Y, int64_t ldc, shg_stream_t stream);
 
-/* shgemm with tunables, caller workspace (>= shg_workspace_size bytes, or NULL), and an optional
- * device int flag set to 1 if any output is non-finite (never cleared by the library). */
+/* shgemm by SHGEMM-TF32: Eqs 14-17 with toLow = TF32 (RN ties-to-even), so
+ * any finite FP32 A below (2 - 2^-11) * 2^127 is accepted (A_Cauchy of P:699-706 stays finite).
+ * Same arguments and layouts as shgemm; Omega stays FP16 in memory and is widened exactly to TF32
+ * in stream-ordered scratch (k x n x 4 bytes) for the tensor cores. */
+shg_status_t shgemm_tf32(int64_t m, int64_t n, int64_t k, const float *A, int64_t lda, const uint16_t *Omega,
+                         int64_t ldo, float *Y, int64_t ldc, shg_stream_t stream);
+
+/* shgemm with tunables (tune->tc selects SHGEMM-FP16 or -TF32), caller workspace
+ * (>= shg_workspace_size bytes, or NULL), and an optional device int flag set to 1 if any output
+ * is non-finite (never cleared by the library). */
 shg_status_t shgemm_ex(int64_t m, int64_t n, int64_t k, const float *A, int64_t lda, const uint16_t *Omega,
                        int64_t ldo, float *Y, int64_t ldc, const shg_tune_t *tune, void *workspace,
                        size_t workspace_bytes, int *nonfinite_flag, shg_stream_t stream);
@@ -113,7 +130,8 @@ shg_status_t shgemm_at(int64_t m, int64_t n, int64_t k, const float *At, int64_t
                        int64_t ldo, float *Y, int64_t ldc, const shg_tune_t *tune, void *workspace,
                        size_t workspace_bytes, int *nonfinite_flag, shg_stream_t stream);
 
-/* Bytes of split-K workspace shgemm_ex needs for (m, n, k) with `tune` (NULL = heuristics). */
+/* Bytes of workspace shgemm_ex needs for (m, n, k) with `tune` (NULL = heuristics): split-K
+ * partial planes, plus the TF32 copy of Omega when tune->tc == SHG_TC_TF32. */
 size_t shg_workspace_size(int64_t m, int64_t n, int64_t k, const shg_tune_t *tune);
 
 /* Fill *plan for (m, n, k) with `tune` (NULL = heuristics), without launching anything. */
@@ -149,6 +167,13 @@ shg_status_t project(const float *A, int ndim, const int64_t *dims, int mode, in
 
 size_t shg_project_workspace_size(int ndim, const int64_t *dims, int mode, int64_t n);
 
+/* project with the tensor-core kind `tc` (shg_tc_t); project() == project_ex(..., SHG_TC_FP16, ...). */
+shg_status_t project_ex(const float *A, int ndim, const int64_t *dims, int mode, int64_t n, uint64_t seed,
+                        int dist, int tc, float *W, int64_t ldw, void *workspace, size_t workspace_bytes,
+                        shg_stream_t stream);
+
+size_t shg_project_workspace_size_ex(int ndim, const int64_t *dims, int mode, int64_t n, int tc);
+
 /* ---------------------------------------------------------------------------------------------
  * shgemm_host — Y = A . Omega with A and Y in HOST memory (pinned for overlap; pageable works but
  * serialises), Omega on the device. A is streamed to the device in row chunks of `chunk_rows`
@@ -169,6 +194,10 @@ size_t shg_host_workspace_size(int64_t n, int64_t k, int64_t chunk_rows);
 /* Elementwise split of Eqs 14-15 with the SAME device function the mainloop uses:
  * hi[t], lo[t] = FP16 bits of toLow(a[t]) and toLow((a[t] - hi) * 2^11). Device pointers. */
 shg_status_t shg_debug_split(const float *a, int64_t count, uint16_t *hi, uint16_t *lo, shg_stream_t stream);
+
+/* Elementwise SHGEMM-TF32 split with the mainloop's device function: hi[t], lo[t] = FP32 bit
+ * patterns of RN_tf32(a[t]) and RN_tf32((a[t] - hi) * 2^11) (low 13 bits zero). Device pointers. */
+shg_status_t shg_debug_split_tf32(const float *a, int64_t count, uint32_t *hi, uint32_t *lo, shg_stream_t stream);
 
 /* Synthetic FP32 input of OMEGA_SPEC §6 (kind 0 Gaussian, 1 uniform [0,1)):
  * A[i*lda + l] = synth(seed, stream_id, global row row0 + i, column l), 0 <= i < m, 0 <= l < k. */

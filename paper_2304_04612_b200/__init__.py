@@ -36,7 +36,7 @@ class SHGError(RuntimeError):
 class Tune(ctypes.Structure):
     _fields_ = [("bn", ctypes.c_int32), ("split_k", ctypes.c_int32), ("max_ctas", ctypes.c_int32),
                 ("force_simt", ctypes.c_int32), ("debug_flags", ctypes.c_int32), ("pair", ctypes.c_int32),
-                ("a_box", ctypes.c_int32), ("reserved", ctypes.c_int32),
+                ("a_box", ctypes.c_int32), ("tc", ctypes.c_int32),
                 ("prof", ctypes.c_void_p)]
 
 
@@ -44,7 +44,8 @@ class Plan(ctypes.Structure):
     _fields_ = [("path", ctypes.c_int32), ("bn", ctypes.c_int32), ("n_tiles", ctypes.c_int32),
                 ("m_tiles", ctypes.c_int32), ("split_k", ctypes.c_int32), ("grid", ctypes.c_int32),
                 ("stages_a", ctypes.c_int32), ("stages_b", ctypes.c_int32), ("smem_bytes", ctypes.c_int32),
-                ("kernels", ctypes.c_int32), ("cta_pair", ctypes.c_int32), ("workspace_bytes", ctypes.c_int64)]
+                ("kernels", ctypes.c_int32), ("cta_pair", ctypes.c_int32), ("tc", ctypes.c_int32),
+                ("workspace_bytes", ctypes.c_int64)]
 
 
 def lib():
@@ -73,6 +74,11 @@ def lib():
             L.shg_host_workspace_size.restype = sz
             L.shg_debug_split.argtypes = [vp, i64, vp, vp, vp]
             L.shg_synth_f32.argtypes = [i32, u64, u32, i64, i64, i64, vp, i64, vp]
+            L.shgemm_tf32.argtypes = [i64, i64, i64, vp, i64, vp, i64, vp, i64, vp]
+            L.project_ex.argtypes = [vp, i32, vp, i32, i64, u64, i32, i32, vp, i64, vp, sz, vp]
+            L.shg_project_workspace_size_ex.argtypes = [i32, vp, i32, i64, i32]
+            L.shg_project_workspace_size_ex.restype = sz
+            L.shg_debug_split_tf32.argtypes = [vp, i64, vp, vp, vp]
             L.shg_probe_tma_read.argtypes = [vp, i64, i64, i64, i32, i32, i32, i32, i32, vp, vp]
             L.shg_launch_count.restype = u64
             L.shg_last_error.restype = ctypes.c_char_p
@@ -84,7 +90,8 @@ def lib():
             L.shg_probe_mma2_rate.argtypes = [i32, i32, i32, vp, i32, vp]
             L.shg_probe_mma2_rate.restype = i32
             for name in ("shgemm", "shgemm_ex", "shgemm_at", "shgemm_host", "shg_plan", "gen_omega_f16", "gen_omega_f16_ex", "project",
-                         "shg_debug_split", "shg_synth_f32", "shg_probe_umma"):
+                         "shg_debug_split", "shg_synth_f32", "shg_probe_umma", "shgemm_tf32", "project_ex",
+                         "shg_debug_split_tf32"):
                 getattr(L, name).restype = i32
             _lib = L
     return _lib
@@ -136,20 +143,35 @@ def gen_omega(k: int, n: int, seed: int = 0, dist="gaussian", stream_id: int = 0
 
 
 # ----------------------------------------------------------------------------------------- SHGEMM
-def _tune(tune):
-    if tune is None:
+TCS = {"fp16": 0, "tf32": 1}
+
+
+def _tc(tc) -> int:
+    """SHGEMM kind: 'fp16' (SHGEMM-FP16) or 'tf32' (SHGEMM-TF32)."""
+    if isinstance(tc, str):
+        if tc not in TCS:
+            raise ValueError(f"tc must be one of {sorted(TCS)}")
+        return TCS[tc]
+    return int(tc)
+
+
+def _tune(tune, tc=None):
+    if tune is None and tc is None:
         return None
     t = Tune()
-    for key, val in dict(tune).items():
-        setattr(t, key, int(val))
+    for key, val in dict(tune or {}).items():
+        setattr(t, key, _tc(val) if key == "tc" else int(val))
+    if tc is not None:
+        t.tc = _tc(tc)
     return ctypes.byref(t)
 
 
 def shgemm(A: torch.Tensor, Omega: torch.Tensor, out: torch.Tensor | None = None, tune=None,
            nonfinite: torch.Tensor | None = None, workspace: torch.Tensor | None = None,
-           stream=None) -> torch.Tensor:
+           stream=None, tc=None) -> torch.Tensor:
     """Y = A . Omega. A: (m, k) float32, row-major (stride(1) == 1). Omega: (k, n) float16,
-    column-major (stride(0) == 1), e.g. from gen_omega(). Returns Y (m, n) float32 row-major."""
+    column-major (stride(0) == 1), e.g. from gen_omega(). Returns Y (m, n) float32 row-major.
+    tc: 'fp16' (SHGEMM-FP16, default) or 'tf32' (SHGEMM-TF32, full FP32 exponent range)."""
     if A.dtype != torch.float32 or Omega.dtype != torch.float16:
         raise TypeError("A must be float32 and Omega float16")
     m, k = A.shape
@@ -168,13 +190,13 @@ def shgemm(A: torch.Tensor, Omega: torch.Tensor, out: torch.Tensor | None = None
     ldo = Omega.stride(1) if n > 1 else max(k, 1)
     ldc = out.stride(0) if m > 1 else max(n, 1)
     ws_bytes = 0 if workspace is None else workspace.numel() * workspace.element_size()
-    _check(lib().shgemm_ex(m, n, k, _p(A), lda, _p(Omega), ldo, _p(out), ldc, _tune(tune), _p(workspace),
+    _check(lib().shgemm_ex(m, n, k, _p(A), lda, _p(Omega), ldo, _p(out), ldc, _tune(tune, tc), _p(workspace),
                            ws_bytes, _p(nonfinite), _stream(stream)), "shgemm_ex")
     return out
 
 
 def shgemm_at(At: torch.Tensor, Omega: torch.Tensor, out: torch.Tensor | None = None, tune=None,
-              nonfinite: torch.Tensor | None = None, workspace: torch.Tensor | None = None, stream=None):
+              nonfinite: torch.Tensor | None = None, workspace: torch.Tensor | None = None, stream=None, tc=None):
     """Y = A . Omega for an M-major A given as its transpose At (k, m) float32 row-major."""
     k, m = At.shape
     k2, n = Omega.shape
@@ -189,7 +211,7 @@ def shgemm_at(At: torch.Tensor, Omega: torch.Tensor, out: torch.Tensor | None = 
     ws_bytes = 0 if workspace is None else workspace.numel() * workspace.element_size()
     _check(lib().shgemm_at(m, n, k, _p(At), At.stride(0) if k > 1 else max(m, 1), _p(Omega),
                            Omega.stride(1) if n > 1 else max(k, 1), _p(out), out.stride(0) if m > 1 else max(n, 1),
-                           _tune(tune), _p(workspace), ws_bytes, _p(nonfinite), _stream(stream)), "shgemm_at")
+                           _tune(tune, tc), _p(workspace), ws_bytes, _p(nonfinite), _stream(stream)), "shgemm_at")
     return out
 
 
@@ -214,25 +236,26 @@ def host_workspace_size(n: int, k: int, chunk_rows: int = 0) -> int:
     return int(lib().shg_host_workspace_size(n, k, chunk_rows))
 
 
-def plan(m: int, n: int, k: int, tune=None) -> dict:
+def plan(m: int, n: int, k: int, tune=None, tc=None) -> dict:
     p = Plan()
-    _check(lib().shg_plan(m, n, k, _tune(tune), ctypes.byref(p)), "shg_plan")
+    _check(lib().shg_plan(m, n, k, _tune(tune, tc), ctypes.byref(p)), "shg_plan")
     return {f: getattr(p, f) for f, _ in Plan._fields_}
 
 
-def workspace_size(m: int, n: int, k: int, tune=None) -> int:
-    return int(lib().shg_workspace_size(m, n, k, _tune(tune)))
+def workspace_size(m: int, n: int, k: int, tune=None, tc=None) -> int:
+    return int(lib().shg_workspace_size(m, n, k, _tune(tune, tc)))
 
 
 # ----------------------------------------------------------------------------------------- project
-def project_workspace_size(dims, mode: int, n: int) -> int:
+def project_workspace_size(dims, mode: int, n: int, tc="fp16") -> int:
     d = (ctypes.c_int64 * len(dims))(*dims)
-    return int(lib().shg_project_workspace_size(len(dims), d, mode, n))
+    return int(lib().shg_project_workspace_size_ex(len(dims), d, mode, n, _tc(tc)))
 
 
 def project(T: torch.Tensor, mode: int, n: int, seed: int = 0, dist="gaussian", out=None, workspace=None,
-            stream=None) -> torch.Tensor:
-    """W = A'_(mode) . Omega_(mode) (Alg 2 line 2) for a C-contiguous FP32 tensor."""
+            stream=None, tc="fp16") -> torch.Tensor:
+    """W = A'_(mode) . Omega_(mode) (Alg 2 line 2) for a C-contiguous FP32 tensor,
+    by SHGEMM-FP16 (tc='fp16') or SHGEMM-TF32 (tc='tf32')."""
     if T.dtype != torch.float32 or not T.is_contiguous():
         raise ValueError("T must be a contiguous float32 tensor")
     dims = list(T.shape)
@@ -241,8 +264,8 @@ def project(T: torch.Tensor, mode: int, n: int, seed: int = 0, dist="gaussian", 
         out = torch.empty((M, n), dtype=torch.float32, device=T.device)
     d = (ctypes.c_int64 * len(dims))(*dims)
     ws_bytes = 0 if workspace is None else workspace.numel() * workspace.element_size()
-    _check(lib().project(_p(T), len(dims), d, mode, n, seed, _dist(dist), _p(out), out.stride(0), _p(workspace),
-                         ws_bytes, _stream(stream)), "project")
+    _check(lib().project_ex(_p(T), len(dims), d, mode, n, seed, _dist(dist), _tc(tc), _p(out), out.stride(0),
+                            _p(workspace), ws_bytes, _stream(stream)), "project_ex")
     return out
 
 
@@ -253,6 +276,16 @@ def split(a: torch.Tensor, stream=None):
     hi = torch.empty(a.numel(), dtype=torch.int16, device=a.device)
     lo = torch.empty(a.numel(), dtype=torch.int16, device=a.device)
     _check(lib().shg_debug_split(_p(a), a.numel(), _p(hi), _p(lo), _stream(stream)), "shg_debug_split")
+    return hi, lo
+
+
+def split_tf32(a: torch.Tensor, stream=None):
+    """SHGEMM-TF32 split elementwise with the mainloop's device function. Returns (hi, lo) int32
+    tensors of FP32 bit patterns."""
+    a = a.contiguous().view(-1)
+    hi = torch.empty(a.numel(), dtype=torch.int32, device=a.device)
+    lo = torch.empty(a.numel(), dtype=torch.int32, device=a.device)
+    _check(lib().shg_debug_split_tf32(_p(a), a.numel(), _p(hi), _p(lo), _stream(stream)), "shg_debug_split_tf32")
     return hi, lo
 
 

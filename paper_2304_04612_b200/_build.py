@@ -8,14 +8,14 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libshgemm.so")
-SOURCES = ["api.cu", "probes.cu"]
-HEADERS = ["ptx.cuh", "omega.cuh", "split.cuh", "shgemm_sm100.cuh", "simt_fallback.cuh"]
+SOURCES = ["api.cu", "probes.cu", "tc_f16.cu", "tc_tf32.cu"]
+HEADERS = ["ptx.cuh", "omega.cuh", "split.cuh", "shgemm_sm100.cuh", "simt_fallback.cuh", "probe_tma.cuh",
+           "internal.cuh"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
 FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-O3", "-lineinfo", "-std=c++17",
-    "-Xcompiler", "-fPIC", "-shared",
     "--expt-relaxed-constexpr",
 ]
 
@@ -35,16 +35,33 @@ def up_to_date() -> bool:
 
 
 def build(force: bool = False, verbose: bool = False) -> str:
+    """Compile each translation unit to an object in parallel, then link the shared library."""
     if not force and up_to_date():
         return LIB
     extra = ["-Xptxas", "-v"] if verbose else []
-    cmd = [NVCC, *FLAGS, *extra, "-o", LIB + ".tmp", *[os.path.join(CSRC, s) for s in SOURCES]]
+    objdir = os.path.join(HERE, "build")
+    os.makedirs(objdir, exist_ok=True)
+    procs = []
+    for src in SOURCES:
+        obj = os.path.join(objdir, src.replace(".cu", ".o"))
+        cmd = [NVCC, *FLAGS, *extra, "-Xcompiler", "-fPIC", "-c", "-o", obj, os.path.join(CSRC, src)]
+        procs.append((src, obj, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.PIPE, text=True)))
+    objs, failed = [], []
+    for src, obj, pr in procs:
+        out, err = pr.communicate()
+        if pr.returncode != 0:
+            failed.append(src)
+            sys.stderr.write(out + err)
+        elif verbose:
+            sys.stderr.write(err)
+        objs.append(obj)
+    if failed:
+        raise RuntimeError("nvcc failed compiling " + ", ".join(failed))
+    cmd = [NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", LIB + ".tmp", *objs]
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
         sys.stderr.write(res.stdout + res.stderr)
-        raise RuntimeError("nvcc failed building libshgemm.so")
-    if verbose:
-        sys.stderr.write(res.stderr)
+        raise RuntimeError("nvcc failed linking libshgemm.so")
     os.replace(LIB + ".tmp", LIB)
     return LIB
 

@@ -12,13 +12,14 @@
 #include <mutex>
 
 #include "../../include/shgemm.h"
+#include "internal.cuh"
 #include "omega.cuh"
 #include "probe_tma.cuh"
 #include "shgemm_sm100.cuh"
 #include "simt_fallback.cuh"
 #include "split.cuh"
 
-namespace {
+namespace shg_api {
 
 std::atomic<uint64_t> g_launches{0};
 thread_local char g_err[256] = "";
@@ -28,11 +29,11 @@ shg_status_t cuda_fail(cudaError_t e, const char* what) {
     return SHG_ERR_CUDA;
 }
 
-#define SHG_CUDA(call)                                              \
-    do {                                                            \
-        cudaError_t e_ = (call);                                    \
-        if (e_ != cudaSuccess) return cuda_fail(e_, #call);         \
-    } while (0)
+}  // namespace shg_api
+
+namespace {
+
+using namespace shg_api;
 
 struct DevInfo {
     int sms = 0;
@@ -106,6 +107,19 @@ bool encode_a_rowpair(CUtensorMap* map, const float* A, int64_t S, int64_t M, in
               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// TF32 copy of Omega (column-major k x n FP32 bit patterns, ldo32 % 4 == 0): dims {k, n}, box {32 k, rows}
+bool encode_b32(CUtensorMap* map, const float* Om32, int64_t k, int64_t n, int64_t ldo32, int rows) {
+    EncodeFn fn = encode_fn();
+    if (!fn) return false;
+    cuuint64_t dims[2] = {static_cast<cuuint64_t>(k), static_cast<cuuint64_t>(n)};
+    cuuint64_t strides[1] = {static_cast<cuuint64_t>(ldo32) * 4};
+    cuuint32_t box[2] = {32, static_cast<cuuint32_t>(rows)};
+    cuuint32_t estr[2] = {1, 1};
+    return fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(Om32), dims, strides, box, estr,
+              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 // Omega (column-major k x n == n rows of ldo halves): dims {k, n}, box {64 k, rows}
 bool encode_b(CUtensorMap* map, const uint16_t* Om, int64_t k, int64_t n, int64_t ldo, int rows) {
     EncodeFn fn = encode_fn();
@@ -119,51 +133,39 @@ bool encode_b(CUtensorMap* map, const uint16_t* Om, int64_t k, int64_t n, int64_
               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+
 // ------------------------------------------------------------------ planning
-constexpr int kBNs[] = {32, 64, 96, 128, 144, 160, 192, 224, 256};
-
-#define SHG_BN_SWITCH(bn, EXPR)                                  \
-    switch (bn) {                                                \
-        case 32: { constexpr int BN_ = 32; EXPR; }               \
-        case 64: { constexpr int BN_ = 64; EXPR; }               \
-        case 96: { constexpr int BN_ = 96; EXPR; }               \
-        case 128: { constexpr int BN_ = 128; EXPR; }             \
-        case 144: { constexpr int BN_ = 144; EXPR; }             \
-        case 160: { constexpr int BN_ = 160; EXPR; }             \
-        case 192: { constexpr int BN_ = 192; EXPR; }             \
-        case 224: { constexpr int BN_ = 224; EXPR; }             \
-        default: { constexpr int BN_ = 256; EXPR; }              \
-    }
-
-// CTA pairs (cta_group::2) are instantiated for BN >= 128, where Omega traffic matters
-constexpr bool pair_ok(int bn) { return bn >= 128; }
-
-template <int B> using CfgPair = shg::Cfg<B, true>;
-template <int B> using CfgSingle = shg::Cfg<B, false>;
-#define SHG_CFG_FIELD(bn, pair, FIELD)                                                                    \
+template <int B> using CfgPair = shg::Cfg<B, true, false>;
+template <int B> using CfgSingle = shg::Cfg<B, false, false>;
+template <int B> using CfgPairT = shg::Cfg<B, true, true>;
+template <int B> using CfgSingleT = shg::Cfg<B, false, true>;
+#define SHG_CFG_FIELD(bn, pair, tf32, FIELD)                                                              \
+    if (tf32 && pair) { SHG_BN_SWITCH(bn, return CfgPairT<BN_>::FIELD) }                                  \
+    if (tf32) { SHG_BN_SWITCH(bn, return CfgSingleT<BN_>::FIELD) }                                        \
     if (pair) { SHG_BN_SWITCH(bn, return CfgPair<BN_>::FIELD) }                                           \
     SHG_BN_SWITCH(bn, return CfgSingle<BN_>::FIELD)
 
-int smem_for(int bn, bool pair) { SHG_CFG_FIELD(bn, pair, kSmemBytes) }
-int sa_for(int bn, bool pair) { SHG_CFG_FIELD(bn, pair, SA) }
-int so_for(int bn, bool pair) { SHG_CFG_FIELD(bn, pair, SO) }
-int r0_for(int bn, bool pair) { SHG_CFG_FIELD(bn, pair, R0) }
-int r1_for(int bn, bool pair) { SHG_CFG_FIELD(bn, pair, R1) }
+int smem_for(int bn, bool pair, bool tf32) { SHG_CFG_FIELD(bn, pair, tf32, kSmemBytes) }
+int sa_for(int bn, bool pair, bool tf32) { SHG_CFG_FIELD(bn, pair, tf32, SA) }
+int so_for(int bn, bool pair, bool tf32) { SHG_CFG_FIELD(bn, pair, tf32, SO) }
+int r0_for(int bn, bool pair, bool tf32) { SHG_CFG_FIELD(bn, pair, tf32, R0) }
+int r1_for(int bn, bool pair, bool tf32) { SHG_CFG_FIELD(bn, pair, tf32, R1) }
 
 struct Plan {
     int path = 0;  // 0 tc, 1 simt, 2 trivial
     int bn = 0, n_tiles = 0, m_tiles = 0, splits = 1, grid = 0, num_kb = 0;
     bool pair = false;
-    int64_t ws_bytes = 0, ld_ws = 0;
+    bool tf32 = false;        // SHGEMM-TF32 (tune->tc == SHG_TC_TF32)
+    // workspace = [split-K planes, 256-B aligned][TF32 copy of Omega (tc path only)]
+    int64_t ws_bytes = 0, ld_ws = 0, sk_bytes = 0, om_bytes = 0, ldo32 = 0;
 };
 
-bool valid_bn(int bn) {
-    for (int b : kBNs) if (b == bn) return true;
-    return false;
-}
+int64_t up256(int64_t b) { return (b + 255) / 256 * 256; }
+
 
 Plan make_plan(int64_t m, int64_t n, int64_t k, bool fast_ok, const shg_tune_t* tune, int sms) {
     Plan pl;
+    pl.tf32 = tune && tune->tc == SHG_TC_TF32;
     if (m == 0 || n == 0 || k == 0) { pl.path = 2; return pl; }
     if (!fast_ok || (tune && tune->force_simt)) { pl.path = 1; return pl; }
     pl.path = 0;
@@ -200,76 +202,18 @@ Plan make_plan(int64_t m, int64_t n, int64_t k, bool fast_ok, const shg_tune_t* 
     pl.grid = static_cast<int>(std::min<int64_t>(tiles * (pl.pair ? 2 : 1), cap));
     if (splits > 1) {
         pl.ld_ws = (n + 3) / 4 * 4;
-        pl.ws_bytes = static_cast<int64_t>(splits) * m * pl.ld_ws * 4;
+        pl.sk_bytes = static_cast<int64_t>(splits) * m * pl.ld_ws * 4;
     }
+    if (pl.tf32) {   // Omega widened once to TF32 (exact) for the tensor cores' smem operand
+        pl.ldo32 = (k + 3) / 4 * 4;
+        pl.om_bytes = pl.ldo32 * n * 4;
+    }
+    pl.ws_bytes = (pl.om_bytes ? up256(pl.sk_bytes) : pl.sk_bytes) + pl.om_bytes;
     return pl;
 }
 
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 
-template <int BN, bool MMAJOR, bool PAIR>
-shg_status_t launch_tc(const CUtensorMap& mapA, const CUtensorMap& mapB0, const CUtensorMap& mapB1,
-                       const shg::KParams& kp, int grid, cudaStream_t stream) {
-    using CF = shg::Cfg<BN, PAIR>;
-    auto kern = shg::shgemm_sm100_kernel<BN, MMAJOR, PAIR>;
-    static std::once_flag flags[64];
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaError_t attr_err = cudaSuccess;
-    std::call_once(flags[std::min(std::max(dev, 0), 63)], [&]() {
-        attr_err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, CF::kSmemBytes);
-    });
-    if (attr_err != cudaSuccess) return cuda_fail(attr_err, "cudaFuncSetAttribute");
-    if constexpr (!PAIR) {
-        // plain launch: a cluster-dimension attribute (even 1x1x1) takes a slower launch path
-        kern<<<grid, shg::kThreads, CF::kSmemBytes, stream>>>(mapA, mapB0, mapB1, kp);
-        g_launches.fetch_add(1, std::memory_order_relaxed);
-        SHG_CUDA(cudaGetLastError());
-        return SHG_OK;
-    }
-    cudaLaunchConfig_t cfg{};
-    cfg.gridDim = dim3(grid);
-    cfg.blockDim = dim3(shg::kThreads);
-    cfg.dynamicSmemBytes = CF::kSmemBytes;
-    cfg.stream = stream;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = PAIR ? 2 : 1;
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    SHG_CUDA(cudaLaunchKernelEx(&cfg, kern, mapA, mapB0, mapB1, kp));
-    g_launches.fetch_add(1, std::memory_order_relaxed);
-    return SHG_OK;
-}
-
-template <bool MMAJOR, bool PAIR>
-shg_status_t dispatch_bn(int bn, const CUtensorMap& a, const CUtensorMap& b0, const CUtensorMap& b1,
-                         const shg::KParams& kp, int grid, cudaStream_t s) {
-    if constexpr (PAIR) {
-        switch (bn) {
-            case 128: return launch_tc<128, MMAJOR, true>(a, b0, b1, kp, grid, s);
-            case 144: return launch_tc<144, MMAJOR, true>(a, b0, b1, kp, grid, s);
-            case 160: return launch_tc<160, MMAJOR, true>(a, b0, b1, kp, grid, s);
-            case 192: return launch_tc<192, MMAJOR, true>(a, b0, b1, kp, grid, s);
-            case 224: return launch_tc<224, MMAJOR, true>(a, b0, b1, kp, grid, s);
-            case 256: return launch_tc<256, MMAJOR, true>(a, b0, b1, kp, grid, s);
-            default: return SHG_ERR_INVALID_VALUE;
-        }
-    } else {
-        SHG_BN_SWITCH(bn, return (launch_tc<BN_, MMAJOR, false>(a, b0, b1, kp, grid, s)))
-    }
-}
-
-shg_status_t dispatch_tc(int bn, bool mmajor, bool pair, const CUtensorMap& a, const CUtensorMap& b0,
-                         const CUtensorMap& b1, const shg::KParams& kp, int grid, cudaStream_t s) {
-    if (!valid_bn(bn) || (pair && !pair_ok(bn))) return SHG_ERR_INVALID_VALUE;
-    if (mmajor) return pair ? dispatch_bn<true, true>(bn, a, b0, b1, kp, grid, s)
-                            : dispatch_bn<true, false>(bn, a, b0, b1, kp, grid, s);
-    return pair ? dispatch_bn<false, true>(bn, a, b0, b1, kp, grid, s)
-                : dispatch_bn<false, false>(bn, a, b0, b1, kp, grid, s);
-}
 
 // M-major A (element (i, l) at A[l * lda + i]): 2-D map {M, K}, box {32 rows, 64 k}
 bool encode_a_mmajor(CUtensorMap* map, const float* A, int64_t M, int64_t K, int64_t lda) {
@@ -317,7 +261,7 @@ shg_status_t run_shgemm(int64_t m, int64_t n, int64_t k, const AView& av, const 
         if (!plain) return SHG_ERR_INVALID_VALUE;  // callers materialise non-plain views first
         const int64_t sa_row = av.mmajor ? 1 : av.row_stride, sa_col = av.mmajor ? av.row_stride : 1;
         shg::shgemm_simt_kernel<<<grid_for(m * n, 256), 256, 0, stream>>>(m, n, k, av.A, sa_row, sa_col, Om, ldo, Y,
-                                                                         ldc, nonfinite);
+                                                                         ldc, nonfinite, pl.tf32);
         g_launches.fetch_add(1, std::memory_order_relaxed);
         SHG_CUDA(cudaGetLastError());
         return SHG_OK;
@@ -337,11 +281,42 @@ shg_status_t run_shgemm(int64_t m, int64_t n, int64_t k, const AView& av, const 
         std::snprintf(g_err, sizeof(g_err), "cuTensorMapEncodeTiled(A) failed");
         return SHG_ERR_CUDA;
     }
-    // pair: one box per N-part half (R0 / R1 rows); single CTA: one box of all BN rows (mapB0)
-    const int rows0 = pl.pair ? r0_for(pl.bn, true) : pl.bn;
-    if (!encode_b(&mapB0, Om, k, n, ldo, rows0) || !encode_b(&mapB1, Om, k, n, ldo, r1_for(pl.bn, pl.pair))) {
+    // workspace: caller's (checked) or stream-ordered scratch, freed on every exit below
+    uint8_t* wsb = nullptr;
+    void* own_ws = nullptr;
+    if (pl.ws_bytes > 0) {
+        if (ws && ws_bytes >= static_cast<size_t>(pl.ws_bytes)) {
+            wsb = static_cast<uint8_t*>(ws);
+        } else if (ws) {
+            return SHG_ERR_WORKSPACE;
+        } else {
+            SHG_CUDA(cudaMallocAsync(&own_ws, pl.ws_bytes, stream));
+            wsb = static_cast<uint8_t*>(own_ws);
+        }
+    }
+    auto finish = [&](shg_status_t st) -> shg_status_t {
+        if (own_ws) {
+            const cudaError_t e = cudaFreeAsync(own_ws, stream);
+            if (st == SHG_OK && e != cudaSuccess) return cuda_fail(e, "cudaFreeAsync");
+        }
+        return st;
+    };
+    // Omega operand: FP16 as given (SHGEMM-FP16), or its exact TF32 widening (SHGEMM-TF32)
+    const int rows0 = pl.pair ? r0_for(pl.bn, true, pl.tf32) : pl.bn;
+    const int rows1 = r1_for(pl.bn, pl.pair, pl.tf32);
+    bool encb_ok;
+    if (pl.tf32) {
+        float* om32 = reinterpret_cast<float*>(wsb + up256(pl.sk_bytes));
+        shg::widen_omega_kernel<<<grid_for(k * n, 256), 256, 0, stream>>>(Om, k, n, ldo, om32, pl.ldo32);
+        g_launches.fetch_add(1, std::memory_order_relaxed);
+        if (cudaGetLastError() != cudaSuccess) return finish(cuda_fail(cudaErrorLaunchFailure, "widen_omega_kernel"));
+        encb_ok = encode_b32(&mapB0, om32, k, n, pl.ldo32, rows0) && encode_b32(&mapB1, om32, k, n, pl.ldo32, rows1);
+    } else {
+        encb_ok = encode_b(&mapB0, Om, k, n, ldo, rows0) && encode_b(&mapB1, Om, k, n, ldo, rows1);
+    }
+    if (!encb_ok) {
         std::snprintf(g_err, sizeof(g_err), "cuTensorMapEncodeTiled(Omega) failed");
-        return SHG_ERR_CUDA;
+        return finish(SHG_ERR_CUDA);
     }
     shg::KParams kp{};
     kp.m = m; kp.n = n; kp.k = k;
@@ -351,17 +326,8 @@ shg_status_t run_shgemm(int64_t m, int64_t n, int64_t k, const AView& av, const 
     kp.a_rowpair = rowpair ? 1 : 0;
     kp.dbg = tune ? static_cast<uint32_t>(tune->debug_flags) : 0u;
     kp.prof = tune ? reinterpret_cast<long long*>(tune->prof) : nullptr;
-    void* own_ws = nullptr;
     if (pl.splits > 1) {
-        float* wsf = nullptr;
-        if (ws && ws_bytes >= static_cast<size_t>(pl.ws_bytes)) {
-            wsf = static_cast<float*>(ws);
-        } else if (ws) {
-            return SHG_ERR_WORKSPACE;
-        } else {
-            SHG_CUDA(cudaMallocAsync(&own_ws, pl.ws_bytes, stream));
-            wsf = static_cast<float*>(own_ws);
-        }
+        float* wsf = reinterpret_cast<float*>(wsb);
         kp.out = wsf;
         kp.ldo_out = pl.ld_ws;
         kp.split_stride = m * pl.ld_ws;
@@ -374,16 +340,17 @@ shg_status_t run_shgemm(int64_t m, int64_t n, int64_t k, const AView& av, const 
         kp.vec_store = (aligned16(Y) && ldc % 4 == 0) ? 1 : 0;
         kp.nonfinite = nonfinite;
     }
-    shg_status_t st = dispatch_tc(pl.bn, av.mmajor, pl.pair, mapA, mapB0, mapB1, kp, pl.grid, stream);
-    if (st != SHG_OK) return st;
+    shg_status_t st = pl.tf32 ? dispatch_tc_tf32(pl.bn, av.mmajor, pl.pair, mapA, mapB0, mapB1, kp, pl.grid, stream)
+                              : dispatch_tc_f16(pl.bn, av.mmajor, pl.pair, mapA, mapB0, mapB1, kp, pl.grid, stream);
+    if (st != SHG_OK) return finish(st);
     if (pl.splits > 1) {
         shg::splitk_reduce_kernel<<<grid_for(m * n, 256), 256, 0, stream>>>(kp.out, pl.splits, m, n, pl.ld_ws,
                                                                           kp.split_stride, Y, ldc, nonfinite);
         g_launches.fetch_add(1, std::memory_order_relaxed);
-        SHG_CUDA(cudaGetLastError());
-        if (own_ws) SHG_CUDA(cudaFreeAsync(own_ws, stream));
+        const cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) return finish(cuda_fail(e, "splitk_reduce_kernel"));
     }
-    return SHG_OK;
+    return finish(SHG_OK);
 }
 
 uint32_t sparse_threshold(int dist, int64_t k_total) {
@@ -482,6 +449,7 @@ shg_status_t shgemm_ex(int64_t m, int64_t n, int64_t k, const float* A, int64_t 
     if (!Y || ldc < n) return SHG_ERR_INVALID_VALUE;
     if (k > 0 && (!A || !Omega || lda < k || ldo < k)) return SHG_ERR_INVALID_VALUE;
     if (tune && tune->bn > 0 && !valid_bn(tune->bn)) return SHG_ERR_INVALID_VALUE;
+    if (tune && tune->tc != SHG_TC_FP16 && tune->tc != SHG_TC_TF32) return SHG_ERR_INVALID_VALUE;
     AView av{A, k, 1, lda, lda * std::max<int64_t>(m, 1)};
     return run_shgemm(m, n, k, av, Omega, ldo, Y, ldc, tune, workspace, workspace_bytes, nonfinite_flag,
                       reinterpret_cast<cudaStream_t>(stream));
@@ -492,6 +460,13 @@ shg_status_t shgemm(int64_t m, int64_t n, int64_t k, const float* A, int64_t lda
     return shgemm_ex(m, n, k, A, lda, Omega, ldo, Y, ldc, nullptr, nullptr, 0, nullptr, stream);
 }
 
+shg_status_t shgemm_tf32(int64_t m, int64_t n, int64_t k, const float* A, int64_t lda, const uint16_t* Omega,
+                         int64_t ldo, float* Y, int64_t ldc, shg_stream_t stream) {
+    shg_tune_t tt{};
+    tt.tc = SHG_TC_TF32;
+    return shgemm_ex(m, n, k, A, lda, Omega, ldo, Y, ldc, &tt, nullptr, 0, nullptr, stream);
+}
+
 shg_status_t shgemm_at(int64_t m, int64_t n, int64_t k, const float* At, int64_t ldat, const uint16_t* Omega,
                        int64_t ldo, float* Y, int64_t ldc, const shg_tune_t* tune, void* workspace,
                        size_t workspace_bytes, int* nonfinite_flag, shg_stream_t stream) {
@@ -500,6 +475,7 @@ shg_status_t shgemm_at(int64_t m, int64_t n, int64_t k, const float* At, int64_t
     if (!Y || ldc < n) return SHG_ERR_INVALID_VALUE;
     if (k > 0 && (!At || !Omega || ldat < m || ldo < k)) return SHG_ERR_INVALID_VALUE;
     if (tune && tune->bn > 0 && !valid_bn(tune->bn)) return SHG_ERR_INVALID_VALUE;
+    if (tune && tune->tc != SHG_TC_FP16 && tune->tc != SHG_TC_TF32) return SHG_ERR_INVALID_VALUE;
     AView av{At, k, 1, ldat, 0, true};
     return run_shgemm(m, n, k, av, Omega, ldo, Y, ldc, tune, workspace, workspace_bytes, nonfinite_flag,
                       reinterpret_cast<cudaStream_t>(stream));
@@ -520,11 +496,12 @@ shg_status_t shg_plan(int64_t m, int64_t n, int64_t k, const shg_tune_t* tune, s
     out->bn = pl.bn; out->n_tiles = pl.n_tiles; out->m_tiles = pl.m_tiles; out->split_k = pl.splits;
     out->grid = pl.grid;
     if (pl.path == 0) {
-        out->stages_a = sa_for(pl.bn, pl.pair);
-        out->stages_b = so_for(pl.bn, pl.pair);
-        out->smem_bytes = smem_for(pl.bn, pl.pair);
+        out->stages_a = sa_for(pl.bn, pl.pair, pl.tf32);
+        out->stages_b = so_for(pl.bn, pl.pair, pl.tf32);
+        out->smem_bytes = smem_for(pl.bn, pl.pair, pl.tf32);
         out->cta_pair = pl.pair ? 1 : 0;
-        out->kernels = pl.splits > 1 ? 2 : 1;
+        out->tc = pl.tf32 ? SHG_TC_TF32 : SHG_TC_FP16;
+        out->kernels = 1 + (pl.splits > 1 ? 1 : 0) + (pl.tf32 ? 1 : 0);
     } else {
         out->kernels = pl.path == 1 ? 1 : (k == 0 && m > 0 && n > 0 ? 0 : 0);
     }
@@ -532,8 +509,9 @@ shg_status_t shg_plan(int64_t m, int64_t n, int64_t k, const shg_tune_t* tune, s
     return SHG_OK;
 }
 
-size_t shg_project_workspace_size(int ndim, const int64_t* dims, int mode, int64_t n) {
+size_t shg_project_workspace_size_ex(int ndim, const int64_t* dims, int mode, int64_t n, int tc) {
     if (ndim < 1 || ndim > 8 || !dims || mode < 0 || mode >= ndim || n <= 0) return 0;
+    if (tc != SHG_TC_FP16 && tc != SHG_TC_TF32) return 0;
     int64_t K = 1, P = 1, S = 1;
     for (int i = 0; i < ndim; ++i) {
         if (i != mode) K *= dims[i];
@@ -545,15 +523,21 @@ size_t shg_project_workspace_size(int ndim, const int64_t* dims, int mode, int64
     size_t bytes = static_cast<size_t>((n * ldo * 2 + 255) / 256 * 256);
     const bool needs_copy = !(mode == 0 || S == 1 || (S % shg::kBK == 0 && S % 4 == 0));
     if (needs_copy) bytes += static_cast<size_t>((M * ((K + 3) / 4 * 4) * 4 + 255) / 256 * 256);
-    bytes += shg_workspace_size(M, n, K, nullptr);
+    shg_tune_t tt{};
+    tt.tc = tc;
+    bytes += shg_workspace_size(M, n, K, &tt);
     return bytes;
 }
 
-shg_status_t project(const float* A, int ndim, const int64_t* dims, int mode, int64_t n, uint64_t seed, int dist,
-                     float* W, int64_t ldw, void* workspace, size_t workspace_bytes, shg_stream_t stream) {
+size_t shg_project_workspace_size(int ndim, const int64_t* dims, int mode, int64_t n) {
+    return shg_project_workspace_size_ex(ndim, dims, mode, n, SHG_TC_FP16);
+}
+
+shg_status_t project_ex(const float* A, int ndim, const int64_t* dims, int mode, int64_t n, uint64_t seed, int dist,
+                        int tc, float* W, int64_t ldw, void* workspace, size_t workspace_bytes, shg_stream_t stream) {
     if (!A || !dims || !W || ndim < 1 || ndim > 8 || mode < 0 || mode >= ndim || n < 0 || ldw < n)
         return SHG_ERR_INVALID_VALUE;
-    if (dist < 0 || dist > 3) return SHG_ERR_INVALID_VALUE;
+    if (dist < 0 || dist > 3 || (tc != SHG_TC_FP16 && tc != SHG_TC_TF32)) return SHG_ERR_INVALID_VALUE;
     for (int i = 0; i < ndim; ++i) if (dims[i] < 1) return SHG_ERR_INVALID_VALUE;
     if (n == 0) return SHG_OK;
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
@@ -564,7 +548,7 @@ shg_status_t project(const float* A, int ndim, const int64_t* dims, int mode, in
         if (i > mode) S *= dims[i];
     }
     const int64_t M = dims[mode];
-    const size_t need = shg_project_workspace_size(ndim, dims, mode, n);
+    const size_t need = shg_project_workspace_size_ex(ndim, dims, mode, n, tc);
     void* own = nullptr;
     uint8_t* ws = static_cast<uint8_t*>(workspace);
     if (!ws) {
@@ -576,8 +560,15 @@ shg_status_t project(const float* A, int ndim, const int64_t* dims, int mode, in
     const int64_t ldo = (K + 7) / 8 * 8;
     uint16_t* Om = reinterpret_cast<uint16_t*>(ws);
     size_t off = static_cast<size_t>((n * ldo * 2 + 255) / 256 * 256);
+    auto finish = [&](shg_status_t st) -> shg_status_t {
+        if (own) {
+            const cudaError_t e = cudaFreeAsync(own, s);
+            if (st == SHG_OK && e != cudaSuccess) return cuda_fail(e, "cudaFreeAsync");
+        }
+        return st;
+    };
     shg_status_t st = gen_omega_f16_ex(K, n, seed, dist, static_cast<uint32_t>(mode), 0, K, Om, ldo, stream);
-    if (st != SHG_OK) return st;
+    if (st != SHG_OK) return finish(st);
     AView av{A, K, 1, K, K * M};
     if (mode == 0) {
         av = AView{A, K, 1, K, K * M};
@@ -594,19 +585,23 @@ shg_status_t project(const float* A, int ndim, const int64_t* dims, int mode, in
         const int64_t ldt = (K + 3) / 4 * 4;
         off += static_cast<size_t>((M * ldt * 4 + 255) / 256 * 256);
         for (int64_t p = 0; p < P; ++p) {
-            SHG_CUDA(cudaMemcpy2DAsync(T + p * S, ldt * 4, A + p * M * S, S * 4, S * 4, M,
-                                       cudaMemcpyDeviceToDevice, s));
+            const cudaError_t e = cudaMemcpy2DAsync(T + p * S, ldt * 4, A + p * M * S, S * 4, S * 4, M,
+                                                    cudaMemcpyDeviceToDevice, s);
+            if (e != cudaSuccess) return finish(cuda_fail(e, "cudaMemcpy2DAsync"));
         }
         av = AView{T, K, 1, ldt, ldt * M};
     }
     void* sk = ws + off;
     const size_t sk_bytes = need - off;
-    st = run_shgemm(M, n, K, av, Om, ldo, W, ldw, nullptr, sk_bytes ? sk : nullptr, sk_bytes, nullptr, s);
-    if (own) {
-        cudaError_t e = cudaFreeAsync(own, s);
-        if (st == SHG_OK && e != cudaSuccess) return cuda_fail(e, "cudaFreeAsync");
-    }
-    return st;
+    shg_tune_t tt{};
+    tt.tc = tc;
+    st = run_shgemm(M, n, K, av, Om, ldo, W, ldw, &tt, sk_bytes ? sk : nullptr, sk_bytes, nullptr, s);
+    return finish(st);
+}
+
+shg_status_t project(const float* A, int ndim, const int64_t* dims, int mode, int64_t n, uint64_t seed, int dist,
+                     float* W, int64_t ldw, void* workspace, size_t workspace_bytes, shg_stream_t stream) {
+    return project_ex(A, ndim, dims, mode, n, seed, dist, SHG_TC_FP16, W, ldw, workspace, workspace_bytes, stream);
 }
 
 size_t shg_host_workspace_size(int64_t n, int64_t k, int64_t chunk_rows) {
@@ -712,6 +707,16 @@ shg_status_t shg_debug_split(const float* a, int64_t count, uint16_t* hi, uint16
     if (count == 0) return SHG_OK;
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
     shg::debug_split_kernel<<<grid_for((count + 1) / 2, 256), 256, 0, s>>>(a, count, hi, lo);
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    SHG_CUDA(cudaGetLastError());
+    return SHG_OK;
+}
+
+shg_status_t shg_debug_split_tf32(const float* a, int64_t count, uint32_t* hi, uint32_t* lo, shg_stream_t stream) {
+    if (count < 0 || (count > 0 && (!a || !hi || !lo))) return SHG_ERR_INVALID_VALUE;
+    if (count == 0) return SHG_OK;
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    shg::debug_split_tf32_kernel<<<grid_for((count + 1) / 2, 256), 256, 0, s>>>(a, count, hi, lo);
     g_launches.fetch_add(1, std::memory_order_relaxed);
     SHG_CUDA(cudaGetLastError());
     return SHG_OK;

@@ -216,4 +216,9 @@ __host__ __device__ constexpr uint32_t idesc_f16_f32(uint32_t M, uint32_t N) {
            | ((M >> 4) << 24);         // m_dim
 }
 
+// kind::tf32 instruction descriptor: a/b format TF32 (2), D F32, K-major A and B
+__host__ __device__ constexpr uint32_t idesc_tf32_f32(uint32_t M, uint32_t N) {
+    return (1u << 4) | (2u << 7) | (2u << 10) | ((N >> 3) << 17) | ((M >> 4) << 24);
+}
+
 }  // namespace shg

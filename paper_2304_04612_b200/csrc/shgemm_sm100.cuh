@@ -52,7 +52,6 @@ constexpr int kThreads = 640;
 // splitter 256 x 56 + epilogue 256 x 168 + control 128 x 32 = 61440.
 constexpr int kSmemLimit = 232448;                // max dynamic smem per block on sm_100
 constexpr int kTmemCols = 512;
-constexpr int kAStageCols = 64;                   // hi 32 + lo 32 columns (2 FP16 per 32-bit column)
 constexpr uint32_t kPeerBitMask = 0xFEFFFFFFu;    // shared::cluster address of the even CTA's copy
 
 struct KParams {
@@ -138,25 +137,33 @@ __device__ __forceinline__ void cluster_sync_all() {
     asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
 
-template <int BN, bool PAIR>
+// TF32 = false: SHGEMM-FP16 (kind::f16, hi/lo packed 2 per 32-bit TMEM column, Omega FP16 in smem).
+// TF32 = true : SHGEMM-TF32 (kind::tf32, one hi or lo element per TMEM column,
+//               Omega as TF32 (the exactly widened FP16 values) in smem, two 128-B k-halves a stage).
+template <int BN, bool PAIR, bool TF32 = false>
 struct Cfg {
-    // K_c = 128: one promotion chunk = 2 stages of 64 k. TMEM: 4 A stages (2 chunks of hi/lo,
-    // 64 columns each) + accumulator slots; N is covered by 2 part-MMAs of widths W + WLAST = BN so
-    // that the drain of one part overlaps the MMAs of the other.
-    static constexpr int KC = 2;                           // stages per promotion chunk
+    // FP16: K_c = 128, one promotion chunk = 2 stages of 64 k; TMEM: 4 A stages (2 chunks of hi/lo,
+    // 64 columns each) + accumulator slots. TF32: a stage's hi/lo take 128 columns, so K_c = 64 =
+    // one stage and 2 chunk slots. N is covered by 2 part-MMAs of widths W + WLAST = BN so that the
+    // drain of one part overlaps the MMAs of the other.
+    static constexpr int KC = TF32 ? 1 : 2;                // stages per promotion chunk
+    static constexpr int AST = TF32 ? 128 : 64;            // TMEM columns per A stage (hi, then lo)
+    static constexpr int EB = TF32 ? 4 : 2;                // Omega bytes per element in smem
+    static constexpr int KSTEP = TF32 ? 8 : 16;            // UMMA K per instruction
+    static constexpr int NMMA = kBK / KSTEP;               // MMAs per stage per operand (hi or lo)
     static constexpr int NCH = 2;                          // chunk slots (TMEM A + Omega smem)
     static constexpr int NQ = 2;
     static constexpr int W = ((BN / 2) + 15) / 16 * 16;    // width of part 0
     static constexpr int WLAST = BN - W;                   // width of part 1
     static constexpr int NPH = 1;                          // parts per epilogue group
     static constexpr int SB = NCH * KC;                    // TMEM A stage slots
-    static constexpr int ABASE = kTmemCols - SB * kAStageCols;
+    static constexpr int ABASE = kTmemCols - SB * AST;
     static constexpr int NSLOT_fit = ABASE / W;
     static constexpr int NSLOT = NSLOT_fit > 4 ? 4 : NSLOT_fit;
     static constexpr int SO = NCH * KC;                    // Omega smem stages
     static constexpr int R0 = PAIR ? W / 2 : W;            // Omega rows of part 0 held by this CTA
     static constexpr int R1 = PAIR ? WLAST / 2 : WLAST;    // Omega rows of part 1 held by this CTA
-    static constexpr int kOmStageBytes = (R0 + R1) * kBK * 2;
+    static constexpr int kOmStageBytes = (R0 + R1) * kBK * EB;   // TF32: [k-half][R0 + R1 rows][128 B]
     static constexpr int kTileM = PAIR ? 2 * kBM : kBM;   // rows per (pair) tile
     static constexpr int kBarBytes = 512;
     static constexpr int SA_fit = (kSmemLimit - 1024 - kBarBytes - SO * kOmStageBytes) / kA32StageBytes;
@@ -194,45 +201,35 @@ __device__ __forceinline__ void advance(uint32_t& stage, uint32_t& phase, uint32
     if (++stage == n) { stage = 0; phase ^= 1u; }
 }
 
-// D[tmem] (+)= A[tmem] * B[smem]  (A operand from tensor memory, "TS" form), 1 CTA or CTA pair
-template <bool PAIR>
-__device__ __forceinline__ void mma_f16_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t bdesc, uint32_t idesc,
-                                           uint32_t accumulate) {
-    if constexpr (PAIR) {
-        asm volatile(
-            "{\n\t.reg .pred p;\n\t"
-            "setp.ne.b32 p, %4, 0;\n\t"
-            "tcgen05.mma.cta_group::2.kind::f16 [%0], [%1], %2, %3, p;\n\t}\n"
-            ::"r"(tmem_d), "r"(tmem_a), "l"(bdesc), "r"(idesc), "r"(accumulate)
-            : "memory");
-    } else {
-        asm volatile(
-            "{\n\t.reg .pred p;\n\t"
-            "setp.ne.b32 p, %4, 0;\n\t"
-            "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}\n"
-            ::"r"(tmem_d), "r"(tmem_a), "l"(bdesc), "r"(idesc), "r"(accumulate)
-            : "memory");
-    }
+// D[tmem] (+)= A[tmem] * B[smem]  (A operand from tensor memory, "TS" form), 1 CTA or CTA pair,
+// kind::f16 (SHGEMM-FP16) or kind::tf32 (SHGEMM-TF32)
+#define SHG_MMA_TS(GROUP, KIND)                                                                  \
+    asm volatile("{\n\t.reg .pred p;\n\t"                                                     \
+                 "setp.ne.b32 p, %4, 0;\n\t"                                                     \
+                 "tcgen05.mma.cta_group::" GROUP ".kind::" KIND " [%0], [%1], %2, %3, p;\n\t}\n"  \
+                 ::"r"(tmem_d), "r"(tmem_a), "l"(bdesc), "r"(idesc), "r"(accumulate) : "memory")
+#define SHG_MMA_TS_SCALE11(GROUP, KIND)                                                             \
+    asm volatile("{\n\t.reg .pred p;\n\t"                                                        \
+                 "setp.ne.b32 p, 1, 0;\n\t"                                                         \
+                 "tcgen05.mma.cta_group::" GROUP ".kind::" KIND " [%0], [%1], %2, %3, p, 11;\n\t}\n" \
+                 ::"r"(tmem_d), "r"(tmem_a), "l"(bdesc), "r"(idesc) : "memory")
+
+template <bool PAIR, bool TF32>
+__device__ __forceinline__ void mma_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t bdesc, uint32_t idesc,
+                                       uint32_t accumulate) {
+    if constexpr (PAIR && TF32) SHG_MMA_TS("2", "tf32");
+    else if constexpr (PAIR) SHG_MMA_TS("2", "f16");
+    else if constexpr (TF32) SHG_MMA_TS("1", "tf32");
+    else SHG_MMA_TS("1", "f16");
 }
 
 // D[tmem] = A[tmem] * B[smem] + D * 2^-11  (scale-input-d = 11, sm_100a)
-template <bool PAIR>
-__device__ __forceinline__ void mma_f16_ts_scale11(uint32_t tmem_d, uint32_t tmem_a, uint64_t bdesc, uint32_t idesc) {
-    if constexpr (PAIR) {
-        asm volatile(
-            "{\n\t.reg .pred p;\n\t"
-            "setp.ne.b32 p, 1, 0;\n\t"
-            "tcgen05.mma.cta_group::2.kind::f16 [%0], [%1], %2, %3, p, 11;\n\t}\n"
-            ::"r"(tmem_d), "r"(tmem_a), "l"(bdesc), "r"(idesc)
-            : "memory");
-    } else {
-        asm volatile(
-            "{\n\t.reg .pred p;\n\t"
-            "setp.ne.b32 p, 1, 0;\n\t"
-            "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p, 11;\n\t}\n"
-            ::"r"(tmem_d), "r"(tmem_a), "l"(bdesc), "r"(idesc)
-            : "memory");
-    }
+template <bool PAIR, bool TF32>
+__device__ __forceinline__ void mma_ts_scale11(uint32_t tmem_d, uint32_t tmem_a, uint64_t bdesc, uint32_t idesc) {
+    if constexpr (PAIR && TF32) SHG_MMA_TS_SCALE11("2", "tf32");
+    else if constexpr (PAIR) SHG_MMA_TS_SCALE11("2", "f16");
+    else if constexpr (TF32) SHG_MMA_TS_SCALE11("1", "tf32");
+    else SHG_MMA_TS_SCALE11("1", "f16");
 }
 
 // completion of this thread's prior tcgen05 ops -> one arrive on `bar` (in both CTAs of a pair)
@@ -306,16 +303,19 @@ __device__ __forceinline__ void add2_rn(float& a, float& b, float c, float d) {
 //                 gathers its row's k values with conflict-free 32-bit loads (one 128-B smem row per
 //                 warp instruction) — no transpose copy.
 // PAIR          : CTA pair (launch with cluster dims (2,1,1)); see the header comment.
-template <int BN, bool MMAJOR, bool PAIR>
+// TF32          : SHGEMM-TF32 (toLow = TF32; Cfg's header); mapB0/B1 then describe the FP32 (TF32)
+//                 copy of Omega.
+template <int BN, bool MMAJOR, bool PAIR, bool TF32 = false>
 __global__ void __launch_bounds__(kThreads, 1)
 shgemm_sm100_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB0,
                     const __grid_constant__ CUtensorMap mapB1, const KParams p) {
-    using CF = Cfg<BN, PAIR>;
+    using CF = Cfg<BN, PAIR, TF32>;
     constexpr int SA = CF::SA, NQ = CF::NQ, W = CF::W, WLAST = CF::WLAST;
     constexpr int NPH = CF::NPH, NSLOT = CF::NSLOT, ABASE = CF::ABASE;
     constexpr int kOm = CF::kOmStageBytes;
     constexpr int NCH = CF::NCH, KC = CF::KC;
     constexpr int SO = CF::SO;
+    constexpr int AST = CF::AST, NMMA = CF::NMMA;
 
     extern __shared__ uint8_t smem_raw[];
     const uint32_t raw_addr = smem_u32(smem_raw);
@@ -396,6 +396,52 @@ shgemm_sm100_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_const
                         // (1) read and split this thread's 32 k of its row (overlaps the MMAs that
                         //     still use the chunk slot about to be overwritten)
                         mbar_wait_prof(&a_full[sa], pa, w_a);
+                        if constexpr (TF32) {
+                            // 32 k of this row -> 64 TMEM words (32 hi + 32 lo): two rounds of 16 k,
+                            // each stored before the next is read (56-register budget), so the
+                            // chunk slot must be free before the first read
+                            if (t == 0) {
+                                mbar_wait_prof(&ch_empty[cs], pc ^ 1u, w_b);
+                                tc_fence_after();
+                            }
+                            const uint32_t col = tmem_base + lane_addr + ABASE + (cs * KC + t) * AST + kh * 32;
+#pragma unroll
+                            for (int rd = 0; rd < 2; ++rd) {
+                                uint32_t hi[16], lo[16];
+                                if (!skip_math) {
+                                    if constexpr (MMAJOR) {
+                                        const uint8_t* box = a32 + sa * kA32StageBytes + (r >> 5) * (kA32StageBytes / 4);
+                                        const int cidx = (r & 31) >> 2;
+                                        const int word = (r & 3) * 4;
+#pragma unroll
+                                        for (int i = 0; i < 8; ++i) {
+                                            const int k0 = 32 * kh + 16 * rd + 2 * i;
+                                            const float a0 = *reinterpret_cast<const float*>(box + k0 * 128 + ((cidx ^ (k0 & 7)) << 4) + word);
+                                            const float a1 = *reinterpret_cast<const float*>(
+                                                box + (k0 + 1) * 128 + ((cidx ^ ((k0 + 1) & 7)) << 4) + word);
+                                            split_tf32_x2(a0, a1, hi[2 * i], hi[2 * i + 1], lo[2 * i], lo[2 * i + 1]);
+                                        }
+                                    } else {
+                                        const uint8_t* src = a32 + sa * kA32StageBytes + a_line * 128;
+#pragma unroll
+                                        for (int c = 0; c < 2; ++c) {
+                                            const int pc0 = 4 * rd + 2 * c;
+                                            const float4 x0 = *reinterpret_cast<const float4*>(src + ((pc0 ^ rx) * 16));
+                                            const float4 x1 = *reinterpret_cast<const float4*>(src + (((pc0 + 1) ^ rx) * 16));
+                                            split_tf32_x2(x0.x, x0.y, hi[8 * c + 0], hi[8 * c + 1], lo[8 * c + 0], lo[8 * c + 1]);
+                                            split_tf32_x2(x0.z, x0.w, hi[8 * c + 2], hi[8 * c + 3], lo[8 * c + 2], lo[8 * c + 3]);
+                                            split_tf32_x2(x1.x, x1.y, hi[8 * c + 4], hi[8 * c + 5], lo[8 * c + 4], lo[8 * c + 5]);
+                                            split_tf32_x2(x1.z, x1.w, hi[8 * c + 6], hi[8 * c + 7], lo[8 * c + 6], lo[8 * c + 7]);
+                                        }
+                                    }
+                                    tmem_st16(col + 16 * rd, hi);
+                                    tmem_st16(col + 64 + 16 * rd, lo);
+                                }
+                            }
+                            __syncwarp();
+                            if (lane == 0) mbar_arrive(&a_empty[sa]);
+                            advance(sa, pa, SA);
+                        } else {
                         uint32_t hi[16], lo[16];
                         if (!skip_math && MMAJOR) {
                             // box r/32 holds rows 32*(r/32).. as 64 k-rows of 128 B (SW128); this
@@ -432,10 +478,11 @@ shgemm_sm100_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_const
                             tc_fence_after();
                         }
                         if (!skip_math) {
-                            const uint32_t col = tmem_base + lane_addr + ABASE + (cs * KC + t) * kAStageCols + kh * 16;
+                            const uint32_t col = tmem_base + lane_addr + ABASE + (cs * KC + t) * AST + kh * 16;
                             tmem_st16(col, hi);
                             tmem_st16(col + 32, lo);
                         }
+                        }   // FP16
                     }
                 }
                 tmem_st_wait();
@@ -610,15 +657,20 @@ shgemm_sm100_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_const
                         }
                         if (!skip) {
                             for (int t = 0; t < nst; ++t) {
-                                uint8_t* dst = om + (cs * KC + t) * kOm;
                                 const int kcoord = kb_global(kb + t, s, p) * kBK;
-                                if constexpr (PAIR) {
-                                    tma_load_omega<PAIR>(dst, &mapB0, &ch_ready[cs], kcoord,
-                                                         n0 + static_cast<int>(crank) * CF::R0, pol);
-                                    tma_load_omega<PAIR>(dst + CF::R0 * 128, &mapB1, &ch_ready[cs], kcoord,
-                                                         n0 + W + static_cast<int>(crank) * CF::R1, pol);
-                                } else {   // the two parts are contiguous rows: one box of BN rows (mapB0)
-                                    tma_load_omega<PAIR>(dst, &mapB0, &ch_ready[cs], kcoord, n0, pol);
+                                // FP16: one 128-B box row = 64 k; TF32: two k-halves of 32 k
+#pragma unroll
+                                for (int hh = 0; hh < (TF32 ? 2 : 1); ++hh) {
+                                    uint8_t* dst = om + (cs * KC + t) * kOm + hh * (CF::R0 + CF::R1) * 128;
+                                    const int kc = kcoord + 32 * hh;
+                                    if constexpr (PAIR) {
+                                        tma_load_omega<PAIR>(dst, &mapB0, &ch_ready[cs], kc,
+                                                             n0 + static_cast<int>(crank) * CF::R0, pol);
+                                        tma_load_omega<PAIR>(dst + CF::R0 * 128, &mapB1, &ch_ready[cs], kc,
+                                                             n0 + W + static_cast<int>(crank) * CF::R1, pol);
+                                    } else {   // the two parts are contiguous rows: one box of BN rows (mapB0)
+                                        tma_load_omega<PAIR>(dst, &mapB0, &ch_ready[cs], kc, n0, pol);
+                                    }
                                 }
                             }
                         }
@@ -639,7 +691,7 @@ shgemm_sm100_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_const
                 for (int kb = kb0; kb < kb1; kb += KC) {
                     const int nst = (kb1 - kb) < KC ? (kb1 - kb) : KC;   // stages in this chunk
                     mbar_wait_prof(&ch_ready[cs], pc, w_hl);
-                    const uint32_t a_base = tmem_base + ABASE + cs * KC * kAStageCols;
+                    const uint32_t a_base = tmem_base + ABASE + cs * KC * AST;
                     const uint64_t b_base = sw128_kmajor_desc(smem_u32(om + cs * KC * kOm));
 #pragma unroll
                     for (int part = 0; part < NQ; ++part, ++g) {
@@ -649,27 +701,34 @@ shgemm_sm100_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_const
                         if (elect_one()) {
                             if (!skip_mma) {
                                 const uint32_t d = tmem_base + slot * W;
-                                const uint32_t idesc = idesc_f16_f32(CF::kTileM, part == NQ - 1 ? WLAST : W);
+                                const uint32_t idesc = TF32 ? idesc_tf32_f32(CF::kTileM, part == NQ - 1 ? WLAST : W)
+                                                            : idesc_f16_f32(CF::kTileM, part == NQ - 1 ? WLAST : W);
                                 const uint64_t b = b_base + static_cast<uint64_t>(((part ? CF::R0 : 0) * 128) >> 4);
+                                // K step j of a stage: 32 B into a 128-B swizzle row; TF32 steps 4..7
+                                // are in the second k-half box, (R0 + R1) rows further on
+                                auto boff = [](int j) -> uint64_t {
+                                    return TF32 ? static_cast<uint64_t>((((j >> 2) * (CF::R0 + CF::R1) * 128) >> 4) + 2 * (j & 3))
+                                                : static_cast<uint64_t>(2 * j);
+                                };
                                 // D := sum over the chunk's stages of lo . Omega  (Eq 16's dA_low term)
 #pragma unroll
                                 for (int t = 0; t < KC; ++t)
                                     if (t < nst)
 #pragma unroll
-                                        for (int j = 0; j < 4; ++j)
-                                            mma_f16_ts<PAIR>(d, a_base + t * kAStageCols + 32 + 8 * j,
-                                                             b + static_cast<uint64_t>((t * kOm) >> 4) + 2 * j, idesc,
-                                                             (t > 0 || j > 0) ? 1u : 0u);
+                                        for (int j = 0; j < NMMA; ++j)
+                                            mma_ts<PAIR, TF32>(d, a_base + t * AST + AST / 2 + 8 * j,
+                                                               b + static_cast<uint64_t>((t * kOm) >> 4) + boff(j), idesc,
+                                                               (t > 0 || j > 0) ? 1u : 0u);
                                 // D := hi . Omega + D * 2^-11 (first step), then the rest of hi
 #pragma unroll
                                 for (int t = 0; t < KC; ++t)
                                     if (t < nst)
 #pragma unroll
-                                        for (int j = 0; j < 4; ++j) {
-                                            const uint32_t a = a_base + t * kAStageCols + 8 * j;
-                                            const uint64_t bb = b + static_cast<uint64_t>((t * kOm) >> 4) + 2 * j;
-                                            if (t == 0 && j == 0) mma_f16_ts_scale11<PAIR>(d, a, bb, idesc);
-                                            else mma_f16_ts<PAIR>(d, a, bb, idesc, 1u);
+                                        for (int j = 0; j < NMMA; ++j) {
+                                            const uint32_t a = a_base + t * AST + 8 * j;
+                                            const uint64_t bb = b + static_cast<uint64_t>((t * kOm) >> 4) + boff(j);
+                                            if (t == 0 && j == 0) mma_ts_scale11<PAIR, TF32>(d, a, bb, idesc);
+                                            else mma_ts<PAIR, TF32>(d, a, bb, idesc, 1u);
                                         }
                             }
                             commit_to<PAIR>(&acc_full[slot]);
@@ -705,7 +764,7 @@ shgemm_sm100_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_const
 }
 
 // Fixed-order (s = 0..S-1) RN sum of split-K partial planes (a8 of SURVEY §8a; deterministic).
-__global__ void splitk_reduce_kernel(const float* __restrict__ ws, int splits, int64_t m, int64_t n,
+static __global__ void splitk_reduce_kernel(const float* __restrict__ ws, int splits, int64_t m, int64_t n,
                                      int64_t ld_ws, int64_t split_stride, float* __restrict__ Y, int64_t ldc,
                                      int* nonfinite) {
     const int64_t total = m * n;

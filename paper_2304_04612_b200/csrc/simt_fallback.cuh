@@ -13,7 +13,7 @@ namespace shg {
 // M-major: sa_row = 1, sa_col = lda).
 __global__ void shgemm_simt_kernel(int64_t m, int64_t n, int64_t k, const float* __restrict__ A, int64_t sa_row,
                                    int64_t sa_col, const uint16_t* __restrict__ Om, int64_t ldo, float* __restrict__ Y,
-                                   int64_t ldc, int* nonfinite) {
+                                   int64_t ldc, int* nonfinite, bool tf32) {
     const int64_t total = m * n;
     for (int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; t < total;
          t += static_cast<int64_t>(gridDim.x) * blockDim.x) {
@@ -25,10 +25,18 @@ __global__ void shgemm_simt_kernel(int64_t m, int64_t n, int64_t k, const float*
             const int64_t k1 = k0 + 64 < k ? k0 + 64 : k;
             float s_hi = 0.0f, s_lo = 0.0f;
             for (int64_t l = k0; l < k1; ++l) {
-                uint32_t h, lo;
-                split2(a[l * sa_col], 0.0f, h, lo);
-                const float hf = __half2float(__ushort_as_half(static_cast<uint16_t>(h & 0xFFFFu)));
-                const float lf = __half2float(__ushort_as_half(static_cast<uint16_t>(lo & 0xFFFFu)));
+                float hf, lf;
+                if (tf32) {   // SHGEMM-TF32 split
+                    uint32_t h0, h1, l0, l1;
+                    split_tf32_x2(a[l * sa_col], 0.0f, h0, h1, l0, l1);
+                    hf = __uint_as_float(h0);
+                    lf = __uint_as_float(l0);
+                } else {
+                    uint32_t h, lo;
+                    split2(a[l * sa_col], 0.0f, h, lo);
+                    hf = __half2float(__ushort_as_half(static_cast<uint16_t>(h & 0xFFFFu)));
+                    lf = __half2float(__ushort_as_half(static_cast<uint16_t>(lo & 0xFFFFu)));
+                }
                 const float wf = __half2float(__ushort_as_half(w[l]));
                 s_hi = __fmaf_rn(hf, wf, s_hi);
                 s_lo = __fmaf_rn(lf, wf, s_lo);
@@ -37,6 +45,19 @@ __global__ void shgemm_simt_kernel(int64_t m, int64_t n, int64_t k, const float*
         }
         Y[i * ldc + j] = acc;
         if (nonfinite && !isfinite(acc)) atomicOr(nonfinite, 1);
+    }
+}
+
+// SHGEMM-TF32's B operand: Omega's FP16 values widened exactly to FP32/TF32 bit patterns (P:498:
+// "converted to TF32 ... before input to Tensor Cores"; tcgen05 reads B from shared memory, so the
+// widening is done once in global memory instead of per tile in registers). Column-major k x n.
+__global__ void widen_omega_kernel(const uint16_t* __restrict__ Om, int64_t k, int64_t n, int64_t ldo,
+                                   float* __restrict__ Om32, int64_t ldo32) {
+    const int64_t total = k * n;
+    for (int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; t < total;
+         t += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int64_t j = t / k, r = t - (t / k) * k;
+        Om32[j * ldo32 + r] = __half2float(__ushort_as_half(Om[j * ldo + r]));
     }
 }
 

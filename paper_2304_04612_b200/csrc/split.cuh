@@ -42,6 +42,33 @@ __device__ __forceinline__ void split2_x2(float a0, float a1, uint32_t& hi, uint
     lo = *reinterpret_cast<const uint32_t*>(&l);
 }
 
+// SHGEMM-TF32 split (Eqs 14-15 with toLow = TF32): hi = cvt.rn.tf32(a),
+// lo = cvt.rn.tf32((a - hi) * 2^11); TF32 values as FP32 bit patterns (the tensor core reads the
+// top 19 bits). a - hi is exact and x 2^11 an exponent shift (packed f32x2 ops, RN per lane).
+__device__ __forceinline__ uint32_t cvt_rn_tf32(float a) {
+    uint32_t r;
+    asm("cvt.rn.tf32.f32 %0, %1;" : "=r"(r) : "f"(a));
+    return r;
+}
+
+__device__ __forceinline__ void split_tf32_x2(float a0, float a1, uint32_t& h0, uint32_t& h1, uint32_t& l0,
+                                              uint32_t& l1) {
+    h0 = cvt_rn_tf32(a0);
+    h1 = cvt_rn_tf32(a1);
+    float r0, r1;
+    asm("{\n\t.reg .b64 x, y, z;\n\t"
+        "mov.b64 x, {%2, %3};\n\t"
+        "mov.b64 y, {%4, %5};\n\t"
+        "sub.rn.f32x2 x, x, y;\n\t"
+        "mov.b64 z, {%6, %6};\n\t"
+        "mul.rn.f32x2 x, x, z;\n\t"
+        "mov.b64 {%0, %1}, x;\n\t}\n"
+        : "=f"(r0), "=f"(r1)
+        : "f"(a0), "f"(a1), "f"(__uint_as_float(h0)), "f"(__uint_as_float(h1)), "f"(2048.0f));
+    l0 = cvt_rn_tf32(r0);
+    l1 = cvt_rn_tf32(r1);
+}
+
 // eight consecutive-k FP32 values -> 16 B of hi and 16 B of lo
 __device__ __forceinline__ void split8(const float4& x0, const float4& x1, uint4& hi, uint4& lo) {
     split2(x0.x, x0.y, hi.x, lo.x);
@@ -51,7 +78,7 @@ __device__ __forceinline__ void split8(const float4& x0, const float4& x1, uint4
 }
 
 // Elementwise split, for the test ABI shg_debug_split (split2_x2: the mainloop's device function).
-__global__ void debug_split_kernel(const float* __restrict__ a, int64_t count, uint16_t* __restrict__ hi,
+static __global__ void debug_split_kernel(const float* __restrict__ a, int64_t count, uint16_t* __restrict__ hi,
                                    uint16_t* __restrict__ lo) {
     for (int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; 2 * t < count;
          t += static_cast<int64_t>(gridDim.x) * blockDim.x) {
@@ -65,6 +92,25 @@ __global__ void debug_split_kernel(const float* __restrict__ a, int64_t count, u
         if (i + 1 < count) {
             hi[i + 1] = static_cast<uint16_t>(h >> 16);
             lo[i + 1] = static_cast<uint16_t>(l >> 16);
+        }
+    }
+}
+
+// Elementwise TF32 split, for the test ABI shg_debug_split_tf32 (the mainloop's device function).
+static __global__ void debug_split_tf32_kernel(const float* __restrict__ a, int64_t count, uint32_t* __restrict__ hi,
+                                        uint32_t* __restrict__ lo) {
+    for (int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; 2 * t < count;
+         t += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int64_t i = 2 * t;
+        const float a0 = a[i];
+        const float a1 = (i + 1 < count) ? a[i + 1] : 0.0f;
+        uint32_t h0, h1, l0, l1;
+        split_tf32_x2(a0, a1, h0, h1, l0, l1);
+        hi[i] = h0;
+        lo[i] = l0;
+        if (i + 1 < count) {
+            hi[i + 1] = h1;
+            lo[i + 1] = l1;
         }
     }
 }
