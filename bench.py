@@ -214,6 +214,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="shgemm", choices=["shgemm", "reference"])
     ap.add_argument("--config", default="cfg4", choices=sorted(CONFIGS) + sorted(PIPELINES))
+    ap.add_argument("--tc", default="fp16", choices=["fp16", "tf32"],
+                    help="SHGEMM-FP16 (default, the paper's headline kernel) or SHGEMM-TF32 (P:494-498)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     args = ap.parse_args()
@@ -268,8 +270,18 @@ def main():
     def gen():
         shg._check(L.gen_omega_f16(k, n, OMEGA_SEED, 0, shg._p(om_buf), ldo, sp), "gen_omega_f16")
 
-    def gemm():
-        shg._check(L.shgemm(m, n, k, shg._p(A), k, shg._p(om_buf), ldo, shg._p(Y), n, sp), "shgemm")
+    if args.tc == "fp16":
+        def gemm():
+            shg._check(L.shgemm(m, n, k, shg._p(A), k, shg._p(om_buf), ldo, shg._p(Y), n, sp), "shgemm")
+    else:
+        tune = shg.Tune()
+        tune.tc = shg.TCS[args.tc]
+        ws_bytes = shg.workspace_size(m, n, k, tc=args.tc)
+        ws = torch.empty(max(1, ws_bytes), dtype=torch.uint8, device="cuda")
+
+        def gemm():
+            shg._check(L.shgemm_ex(m, n, k, shg._p(A), k, shg._p(om_buf), ldo, shg._p(Y), n, ctypes.byref(tune),
+                                   shg._p(ws), ws_bytes, None, sp), "shgemm_ex")
 
     def step():
         gen()
@@ -318,8 +330,12 @@ def main():
     # power cap to settle (observed: reason sw_power_cap, SM clock ~1.1 GHz), so the tensor peak is
     # the driver's SUSTAINED cuBLAS figure; the burst figure is reported beside it.
     region_s = total_ms * 1e-3
+    # TF32 tensor cores run at half the FP16/BF16 rate (guide's nominal ratio)
+    tc_ratio = 0.5 if args.tc == "tf32" else 1.0
+    tc16, tc16_sus = tc16 * tc_ratio, tc16_sus * tc_ratio
     tc_peak = tc16_sus if region_s > 0.1 else tc16
-    tc_peak_kind = "sustained" if region_s > 0.1 else "burst"
+    tc_peak_kind = ("sustained" if region_s > 0.1 else "burst") + (
+        " (bf16 figure x 0.5 for TF32)" if args.tc == "tf32" else "")
     alg_bytes = 4.0 * m * k + 2.0 * k * n + 4.0 * m * n        # per launch, this rank
     achieved_gbs = alg_bytes / (gemm_ms * 1e-3) / 1e9
     ai = 2.0 * m * k * n / alg_bytes
@@ -332,7 +348,8 @@ def main():
         # the tensor pipe executes 4mnk flops (hi and lo MMAs); peak = measured dense fp16 (= bf16 rate)
         tc_ach = 4.0 * m * k * n / (gemm_ms * 1e-3) / 1e12
         roof = {"bound": "tensor", "achieved": tc_ach, "peak": tc_peak, "unit": "TFLOP/s", "frac": tc_ach / tc_peak}
-    roof["traffic"] = ncu_traffic(args.config if world == 1 else f"{args.config}_g{world}")
+    tag = args.config + ("" if args.tc == "fp16" else "_tf32")
+    roof["traffic"] = ncu_traffic(tag if world == 1 else f"{tag}_g{world}")
     roof["peak_source"] = f"{peak_src} (MEASURED_PEAKS.json); tensor peak {tc_peak_kind}"
     roof["kernel"] = "shgemm_sm100_kernel"
     roof["kernel_ms"] = gemm_ms
@@ -353,13 +370,16 @@ def main():
             cpu = cpu_baseline(m_total, k, n)
         out = {"metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps,
                "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
-               "vs_baseline": None, "dtype": "f16*f16->f32 (FP32 A split to FP16 hi/lo in-kernel)",
+               "vs_baseline": None,
+               "dtype": ("f16*f16->f32 (FP32 A split to FP16 hi/lo in-kernel)" if args.tc == "fp16" else
+                         "tf32*tf32->f32 (FP32 A split to TF32 hi/lo in-kernel; FP16 Omega widened exactly)"),
                "data": "synthetic",
                "config": {"workload": args.config, "description": desc, "m": m_total, "k": k, "n": n,
                           "rows_per_gpu": per, "parallelism": f"row-shard x{world} (no collective on the data path)",
                           "dist_backend": backend,
                           "l2": "inputs larger than L2 (A is %.1f GiB per GPU), no flush" % (4.0 * m * k / 2 ** 30),
-                          "plan": shg.plan(m, n, k)},
+                          "kernel": "SHGEMM-FP16" if args.tc == "fp16" else "SHGEMM-TF32",
+                          "plan": shg.plan(m, n, k, tc=args.tc)},
                "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
                "clocks": clk, "omega_gen_ms": gen_ms, "shgemm_ms": gemm_ms,
                "gbs_algorithmic": achieved_gbs}

@@ -303,7 +303,8 @@ shg_status_t run_shgemm(int64_t m, int64_t n, int64_t k, const AView& av, const 
     };
     // Omega operand: FP16 as given (SHGEMM-FP16), or its exact TF32 widening (SHGEMM-TF32)
     const int rows0 = pl.pair ? r0_for(pl.bn, true, pl.tf32) : pl.bn;
-    const int rows1 = r1_for(pl.bn, pl.pair, pl.tf32);
+    const int r1 = r1_for(pl.bn, pl.pair, pl.tf32);
+    const int rows1 = r1 > 0 ? r1 : rows0;         // one N part (R1 == 0): mapB1 unused
     bool encb_ok;
     if (pl.tf32) {
         float* om32 = reinterpret_cast<float*>(wsb + up256(pl.sk_bytes));

@@ -151,18 +151,23 @@ struct Cfg {
     static constexpr int EB = TF32 ? 4 : 2;                // Omega bytes per element in smem
     static constexpr int KSTEP = TF32 ? 8 : 16;            // UMMA K per instruction
     static constexpr int NMMA = kBK / KSTEP;               // MMAs per stage per operand (hi or lo)
-    static constexpr int NCH = 2;                          // chunk slots (TMEM A + Omega smem)
-    static constexpr int NQ = 2;
-    static constexpr int W = ((BN / 2) + 15) / 16 * 16;    // width of part 0
-    static constexpr int WLAST = BN - W;                   // width of part 1
+    // chunk slots (TMEM A + Omega smem); TF32 with BN <= 64 has the TMEM for a third (the ring is
+    // only one stage deep per slot there, and the splitter must not wait on the MMAs every stage)
+    static constexpr int NCH = (TF32 && BN <= 64) ? 3 : 2;
+    // N parts: 2 (drain of one overlaps the MMAs of the other), or 1 for TF32 with BN <= 64, whose
+    // MMA thread is issue-bound (8 K steps a stage: half the instructions with one part of N = BN)
+    static constexpr int NQ = (TF32 && BN <= 64) ? 1 : 2;
+    static constexpr int W = NQ == 1 ? BN : ((BN / 2) + 15) / 16 * 16;    // width of part 0
+    static constexpr int WLAST = NQ == 1 ? BN : BN - W;                     // width of the last part
     static constexpr int NPH = 1;                          // parts per epilogue group
     static constexpr int SB = NCH * KC;                    // TMEM A stage slots
     static constexpr int ABASE = kTmemCols - SB * AST;
     static constexpr int NSLOT_fit = ABASE / W;
-    static constexpr int NSLOT = NSLOT_fit > 4 ? 4 : NSLOT_fit;
+    static constexpr int NSLOT_MAX = TF32 ? 8 : 4;             // TF32 chunks are half as long: more slack
+    static constexpr int NSLOT = NSLOT_fit > NSLOT_MAX ? NSLOT_MAX : NSLOT_fit;
     static constexpr int SO = NCH * KC;                    // Omega smem stages
     static constexpr int R0 = PAIR ? W / 2 : W;            // Omega rows of part 0 held by this CTA
-    static constexpr int R1 = PAIR ? WLAST / 2 : WLAST;    // Omega rows of part 1 held by this CTA
+    static constexpr int R1 = NQ == 1 ? 0 : (PAIR ? WLAST / 2 : WLAST);   // ... of part 1
     static constexpr int kOmStageBytes = (R0 + R1) * kBK * EB;   // TF32: [k-half][R0 + R1 rows][128 B]
     static constexpr int kTileM = PAIR ? 2 * kBM : kBM;   // rows per (pair) tile
     static constexpr int kBarBytes = 512;
@@ -170,7 +175,7 @@ struct Cfg {
     static constexpr int SA = SA_fit > 6 ? 6 : SA_fit;
     static constexpr int kSmemBytes = 1024 + SA * kA32StageBytes + SO * kOmStageBytes + kBarBytes;
     static_assert(BN % 16 == 0 && BN >= 32 && BN <= 256, "BN");
-    static_assert(WLAST >= 16 && WLAST % 16 == 0 && W <= 128, "UMMA N parts");
+    static_assert(WLAST >= 16 && WLAST % 16 == 0 && (W <= 128 || NQ == 1), "UMMA N parts");
     static_assert(!PAIR || (R0 % 8 == 0 && R1 % 8 == 0), "pair halves must be whole 8-row core groups");
     static_assert(NSLOT >= NQ, "TMEM accumulator slots");
     static_assert(SA >= 2 && kSmemBytes <= kSmemLimit, "smem");
@@ -398,12 +403,8 @@ shgemm_sm100_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_const
                         mbar_wait_prof(&a_full[sa], pa, w_a);
                         if constexpr (TF32) {
                             // 32 k of this row -> 64 TMEM words (32 hi + 32 lo): two rounds of 16 k,
-                            // each stored before the next is read (56-register budget), so the
-                            // chunk slot must be free before the first read
-                            if (t == 0) {
-                                mbar_wait_prof(&ch_empty[cs], pc ^ 1u, w_b);
-                                tc_fence_after();
-                            }
+                            // each stored before the next is read (56-register budget); the wait for
+                            // the chunk slot sits after the first round's split, which it overlaps
                             const uint32_t col = tmem_base + lane_addr + ABASE + (cs * KC + t) * AST + kh * 32;
 #pragma unroll
                             for (int rd = 0; rd < 2; ++rd) {
@@ -434,6 +435,12 @@ shgemm_sm100_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_const
                                             split_tf32_x2(x1.z, x1.w, hi[8 * c + 6], hi[8 * c + 7], lo[8 * c + 6], lo[8 * c + 7]);
                                         }
                                     }
+                                }
+                                if (rd == 0 && t == 0) {
+                                    mbar_wait_prof(&ch_empty[cs], pc ^ 1u, w_b);
+                                    tc_fence_after();
+                                }
+                                if (!skip_math) {
                                     tmem_st16(col + 16 * rd, hi);
                                     tmem_st16(col + 64 + 16 * rd, lo);
                                 }
@@ -522,6 +529,7 @@ shgemm_sm100_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_const
 #pragma unroll
                 for (int j = 0; j < NPH; ++j) {
                     const int part = h + 2 * j;
+                    if (part >= NQ) continue;                      // NQ == 1: group 1 idles
                     const int width = (part == NQ - 1) ? WLAST : W;
                     const uint32_t g = stage * NQ + part;
                     const uint32_t slot = g % NSLOT;
@@ -563,6 +571,7 @@ shgemm_sm100_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_const
 #pragma unroll
                 for (int j = 0; j < NPH; ++j) {
                     const int part = h + 2 * j;
+                    if (part >= NQ) continue;
                     const int width = (part == NQ - 1) ? WLAST : W;
                     const int64_t col0 = static_cast<int64_t>(n_blk) * BN + part * W;
                     if (col0 >= p.n) continue;
