@@ -64,7 +64,8 @@ def lib():
             L.orc_split_tf32.argtypes = [vp, i64, vp, vp]
             L.orc_f32_to_tf32_rn.argtypes = [ctypes.c_float]
             L.orc_f32_to_tf32_rn.restype = u32
-            for name in ("orc_gemm_y64", "orc_gemm_y32", "orc_gemm_ysplit64", "orc_gemm_ysplit64_tf32"):
+            for name in ("orc_gemm_y64", "orc_gemm_y32", "orc_gemm_ysplit64", "orc_gemm_ysplit64_tf32",
+                         "orc_gemm_y64_f32b", "orc_gemm_y32_f32b", "orc_gemm_ytcec64"):
                 getattr(L, name).argtypes = [i64, vp, i64, i64, vp, i64, vp, i64, vp, i64]
             L.orc_gauss_f32.argtypes = [u64, u32, u64, u64]
             L.orc_gauss_f32.restype = ctypes.c_float
@@ -234,6 +235,39 @@ def gemm_ysplit64(A, omega_bits, rows=None) -> np.ndarray:
 def gemm_ysplit64_tf32(A, omega_bits, rows=None) -> np.ndarray:
     """Eq 16 in FP64 with the TF32 split of SHGEMM-TF32."""
     return _gemm(lib().orc_gemm_ysplit64_tf32, np.float64, A, omega_bits, rows)
+
+
+def _gemm_f32b(fn, out_dtype, A, B, rows=None):
+    A = np.ascontiguousarray(A, dtype=np.float32)
+    B = np.asarray(B, dtype=np.float32)
+    m, k = A.shape
+    k2, n = B.shape
+    assert k2 == k
+    bc = np.ascontiguousarray(B.T)          # n x k == column-major k x n
+    if rows is None:
+        nrows, rp = m, None
+    else:
+        rows = np.ascontiguousarray(rows, dtype=np.int64)
+        nrows, rp = rows.size, _ptr(rows)
+    Y = np.zeros((nrows, n), dtype=out_dtype)
+    if nrows and n:
+        fn(nrows, rp, n, k, _ptr(A), k, _ptr(bc), k, _ptr(Y), n)
+    return Y
+
+
+def gemm_y64_f32b(A, B, rows=None) -> np.ndarray:
+    """sum_l (double)A[i][l] * (double)B[l][j] for FP32 A and B (exact products), l ascending."""
+    return _gemm_f32b(lib().orc_gemm_y64_f32b, np.float64, A, B, rows)
+
+
+def gemm_y32_f32b(A, B, rows=None) -> np.ndarray:
+    """Naive FP32 SGEMM: acc = fmaf(a, b, acc), l ascending (the SGEMM baseline of P:613)."""
+    return _gemm_f32b(lib().orc_gemm_y32_f32b, np.float32, A, B, rows)
+
+
+def gemm_ytcec64(A, B, rows=None) -> np.ndarray:
+    """TCEC-SGEMM, Eq 9 in FP64: A_low B_low + (dA_low B_low + A_low dB_low) 2^-11."""
+    return _gemm_f32b(lib().orc_gemm_ytcec64, np.float64, A, B, rows)
 
 
 def relative_error(C, C_ref) -> float:

@@ -16,6 +16,9 @@
  *   orc_gemm_y32        naive single-precision GEMM (the "SGEMM" comparator of P:613):
  *                       acc = fmaf(A[i][l], Ω[l][j], acc), sequential in l
  *   orc_gemm_ysplit64   Eq 16 evaluated exactly in FP64: sum_l (hi + lo*2^-11) * Ω[l][j]
+ *   orc_gemm_y64_f32b / orc_gemm_y32_f32b   the same two GEMMs with an FP32 B (k x n, column-major)
+ *   orc_gemm_ytcec64    TCEC-SGEMM, Eq 9 in FP64:
+ *                       sum_l [ahi*bhi + (alo*bhi + ahi*blo) * 2^-11], hi/lo from orc_split
  *   orc_f32_to_tf32_rn  RN ties-to-even to TF32 (e8m10), as FP32 bits with 13 zero low bits
  *   orc_split_tf32      Eqs 14-15 with toLow = TF32: the SHGEMM-TF32 variant of P:494-498
  *   orc_gemm_ysplit64_tf32  Eq 16 in FP64 with the TF32 hi/lo
@@ -456,4 +459,100 @@ void orc_gauss_column_f32(uint64_t seed, uint32_t stream_id, uint32_t j, int64_t
         else       gauss_pair_f32(x[2], x[3], &za, &zb);
         out[t] = (w & 1u) ? zb : za;
     }
+}
+
+/* ------------------------------------------------------------------ FP32 x FP32 GEMMs (TCEC-SGEMM) */
+/* B: k x n FP32, column-major (element (l, j) at B[j * ldb + l]). Products of two FP32 values are
+ * exact in binary64 (24 + 24 significant bits <= 53). */
+static double *b_rows_f64(int64_t k, int64_t n, const float *B, int64_t ldb) {
+    double *w = (double *)malloc(sizeof(double) * (size_t)(k * n > 0 ? k * n : 1));
+    for (int64_t l = 0; l < k; ++l)
+        for (int64_t j = 0; j < n; ++j) w[l * n + j] = (double)B[j * ldb + l];
+    return w;
+}
+
+void orc_gemm_y64_f32b(int64_t nrows, const int64_t *rows, int64_t n, int64_t k,
+                       const float *A, int64_t lda, const float *B, int64_t ldb, double *Y, int64_t ldy) {
+    double *w = b_rows_f64(k, n, B, ldb);
+    #pragma omp parallel
+    {
+        double *acc = (double *)malloc(sizeof(double) * (size_t)(n > 0 ? n : 1));
+        #pragma omp for schedule(dynamic, 4)
+        for (int64_t r = 0; r < nrows; ++r) {
+            const float *a = A + (rows ? rows[r] : r) * lda;
+            for (int64_t j = 0; j < n; ++j) acc[j] = 0.0;
+            for (int64_t l = 0; l < k; ++l) {
+                double al = (double)a[l];
+                const double *wl = w + l * n;
+                for (int64_t j = 0; j < n; ++j) acc[j] = acc[j] + al * wl[j];
+            }
+            for (int64_t j = 0; j < n; ++j) Y[r * ldy + j] = acc[j];
+        }
+        free(acc);
+    }
+    free(w);
+}
+
+/* naive FP32: acc = fmaf(A[i][l], B[l][j], acc), l ascending */
+void orc_gemm_y32_f32b(int64_t nrows, const int64_t *rows, int64_t n, int64_t k,
+                       const float *A, int64_t lda, const float *B, int64_t ldb, float *Y, int64_t ldy) {
+    float *w = (float *)malloc(sizeof(float) * (size_t)(k * n > 0 ? k * n : 1));
+    for (int64_t l = 0; l < k; ++l)
+        for (int64_t j = 0; j < n; ++j) w[l * n + j] = B[j * ldb + l];
+    #pragma omp parallel
+    {
+        float *acc = (float *)malloc(sizeof(float) * (size_t)(n > 0 ? n : 1));
+        #pragma omp for schedule(dynamic, 4)
+        for (int64_t r = 0; r < nrows; ++r) {
+            const float *a = A + (rows ? rows[r] : r) * lda;
+            for (int64_t j = 0; j < n; ++j) acc[j] = 0.0f;
+            for (int64_t l = 0; l < k; ++l) {
+                float al = a[l];
+                const float *wl = w + l * n;
+                for (int64_t j = 0; j < n; ++j) acc[j] = fmaf(al, wl[j], acc[j]);
+            }
+            for (int64_t j = 0; j < n; ++j) Y[r * ldy + j] = acc[j];
+        }
+        free(acc);
+    }
+    free(w);
+}
+
+/* TCEC-SGEMM (Eqs 5-9): both operands split by Eqs 14-15's FP16 split (orc_split),
+ * C ~ A_low B_low + (dA_low B_low + A_low dB_low) 2^-11, each term evaluated exactly in FP64 and
+ * summed over l ascending. The dA_low dB_low term is absent (Eq 9). */
+void orc_gemm_ytcec64(int64_t nrows, const int64_t *rows, int64_t n, int64_t k,
+                      const float *A, int64_t lda, const float *B, int64_t ldb, double *Y, int64_t ldy) {
+    double *bh = (double *)malloc(sizeof(double) * (size_t)(k * n > 0 ? k * n : 1));
+    double *bl = (double *)malloc(sizeof(double) * (size_t)(k * n > 0 ? k * n : 1));
+    for (int64_t l = 0; l < k; ++l)
+        for (int64_t j = 0; j < n; ++j) {
+            uint16_t h, lo;
+            orc_split(&B[j * ldb + l], 1, &h, &lo);
+            bh[l * n + j] = (double)orc_f16_to_f32(h);
+            bl[l * n + j] = (double)orc_f16_to_f32(lo);
+        }
+    #pragma omp parallel
+    {
+        double *acc = (double *)malloc(sizeof(double) * (size_t)(n > 0 ? n : 1));
+        #pragma omp for schedule(dynamic, 4)
+        for (int64_t r = 0; r < nrows; ++r) {
+            const float *a = A + (rows ? rows[r] : r) * lda;
+            for (int64_t j = 0; j < n; ++j) acc[j] = 0.0;
+            for (int64_t l = 0; l < k; ++l) {
+                uint16_t h, lo;
+                orc_split(&a[l], 1, &h, &lo);
+                double ah = (double)orc_f16_to_f32(h), al = (double)orc_f16_to_f32(lo);
+                for (int64_t j = 0; j < n; ++j) {
+                    double hh = ah * bh[l * n + j];
+                    double corr = al * bh[l * n + j] + ah * bl[l * n + j];
+                    acc[j] = acc[j] + (hh + corr * (1.0 / 2048.0));
+                }
+            }
+            for (int64_t j = 0; j < n; ++j) Y[r * ldy + j] = acc[j];
+        }
+        free(acc);
+    }
+    free(bh);
+    free(bl);
 }
