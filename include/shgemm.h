@@ -63,9 +63,16 @@ typedef enum {
 /* Tensor-core kind of the SHGEMM ("two kinds of SGEMM"). */
 typedef enum {
     SHG_TC_FP16 = 0,  /* SHGEMM-FP16: toLow = FP16 (Eqs 14-17); |A| < 65520 (FP16 range) */
-    SHG_TC_TF32 = 1   /* SHGEMM-TF32: toLow = TF32 (e8m10): the full FP32 exponent range, Omega
+    SHG_TC_TF32 = 1,  /* SHGEMM-TF32: toLow = TF32 (e8m10): the full FP32 exponent range, Omega
                          widened exactly to TF32; half the FP16 tensor-core rate */
+    SHG_TC_TCEC = 2   /* reported in shg_plan_t.tc by tcec_plan only: TCEC-SGEMM (Eqs 5-9) */
 } shg_tc_t;
+
+/* Operand layouts for tcec_sgemm. For A (m x k): K_MAJOR = row-major, element (i, l) at
+ * A[i * lda + l], lda >= k; MN_MAJOR = element (i, l) at A[l * lda + i], lda >= m (A given as its
+ * k x m row-major transpose). For B (k x n): K_MAJOR = column-major, element (l, j) at
+ * B[j * ldb + l], ldb >= k; MN_MAJOR = row-major, element (l, j) at B[l * ldb + j], ldb >= n. */
+typedef enum { SHG_LAYOUT_K_MAJOR = 0, SHG_LAYOUT_MN_MAJOR = 1 } shg_layout_t;
 
 /* Tunables for shgemm_ex. Zero-initialise for the heuristics. */
 typedef struct {
@@ -136,6 +143,40 @@ size_t shg_workspace_size(int64_t m, int64_t n, int64_t k, const shg_tune_t *tun
 
 /* Fill *plan for (m, n, k) with `tune` (NULL = heuristics), without launching anything. */
 shg_status_t shg_plan(int64_t m, int64_t n, int64_t k, const shg_tune_t *tune, shg_plan_t *plan);
+
+/* ---------------------------------------------------------------------------------------------
+ * tcec_sgemm — C[m x n] = A[m x k] . B[k x n] for FP32 A AND FP32 B by TCEC-SGEMM, the authors'
+ * error-corrected single-precision GEMM on FP16 tensor cores (Eqs 5-9; SURVEY §8f
+ * NEXT-2): A_low = toLow(A), dA_low = toLow((A - A_low) * 2^11), likewise for B (RN to FP16,
+ * P:190), and C ~ A_low.B_low + (dA_low.B_low + A_low.dB_low) * 2^-11 (Eq 9; dA_low.dB_low is
+ * dropped), accumulated per 128-k chunk on the tensor cores and added with RN on the CUDA cores
+ * (P:181). It serves the RandNLA pipelines' other FP32 products: B = Q^T A (Alg 1 line 3, P:129;
+ * computed as B^T = A^T Q with an MN_MAJOR A) and the RP-HOSVD core contractions (Alg 2 line 5).
+ *   m, n, k  >= 0. m == 0 or n == 0: no-op. k == 0: C = 0.
+ *   A, B     device FP32 in the shg_layout_t given by a_layout / b_layout (see shg_layout_t).
+ *   C        device, row-major, ldc >= n; overwritten (beta = 0).
+ *   Range: as SHGEMM-FP16, |a|, |b| >= 65520 overflow to non-finite C; entries below 2^-14
+ *   lose relative precision in their FP16 parts (absolute error <= ~2^-36 |other operand|).
+ *   Error: |C - AB| <~ ((k/8) + 3) u |A||B| elementwise (u = 2^-24), the SGEMM level.
+ * B is split once per call (split_b_kernel) into stream-ordered scratch, or into `workspace`
+ * (>= tcec_sgemm_workspace_size bytes) with tcec_sgemm_ex. Fast path: A 16-B aligned and
+ * lda % 4 == 0 (B has no alignment requirement); otherwise a CUDA-core fallback (same contract).
+ * Errors: SHG_ERR_INVALID_VALUE for negative sizes, bad layouts, short leading dimensions, NULL
+ * pointers with k > 0, or tune->bn > 128 with single CTAs (TCEC stages two B tiles).
+ * ------------------------------------------------------------------------------------------- */
+shg_status_t tcec_sgemm(int64_t m, int64_t n, int64_t k, const float *A, int64_t lda, int a_layout,
+                        const float *B, int64_t ldb, int b_layout, float *C, int64_t ldc, shg_stream_t stream);
+
+/* tcec_sgemm with tunables (bn, split_k, max_ctas, pair, a_box, force_simt; tc ignored) and a
+ * caller workspace (NULL = stream-ordered scratch). */
+shg_status_t tcec_sgemm_ex(int64_t m, int64_t n, int64_t k, const float *A, int64_t lda, int a_layout,
+                           const float *B, int64_t ldb, int b_layout, float *C, int64_t ldc,
+                           const shg_tune_t *tune, void *workspace, size_t workspace_bytes, shg_stream_t stream);
+
+size_t tcec_sgemm_workspace_size(int64_t m, int64_t n, int64_t k, const shg_tune_t *tune);
+
+/* Plan of a tcec_sgemm call (plan->tc = SHG_TC_TCEC). */
+shg_status_t tcec_plan(int64_t m, int64_t n, int64_t k, const shg_tune_t *tune, shg_plan_t *plan);
 
 /* ---------------------------------------------------------------------------------------------
  * gen_omega_f16 — Omega[i][j] = OMEGA_SPEC(seed, stream_id = 0, dist, i, j) for 0 <= i < k,

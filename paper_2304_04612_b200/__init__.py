@@ -17,7 +17,7 @@ import threading
 
 import torch
 
-__all__ = ["shgemm", "gen_omega", "project", "split", "synth", "plan", "launch_count", "lib",
+__all__ = ["shgemm", "tcec_sgemm", "gen_omega", "project", "split", "synth", "plan", "launch_count", "lib",
            "probe_umma", "project_workspace_size", "SHGError", "DISTS"]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
@@ -80,6 +80,12 @@ def lib():
             L.shg_project_workspace_size_ex.restype = sz
             L.shg_debug_split_tf32.argtypes = [vp, i64, vp, vp, vp]
             L.shg_probe_tma_read.argtypes = [vp, i64, i64, i64, i32, i32, i32, i32, i32, vp, vp]
+            L.tcec_sgemm.argtypes = [i64, i64, i64, vp, i64, i32, vp, i64, i32, vp, i64, vp]
+            L.tcec_sgemm_ex.argtypes = [i64, i64, i64, vp, i64, i32, vp, i64, i32, vp, i64, ctypes.POINTER(Tune), vp,
+                                        sz, vp]
+            L.tcec_sgemm_workspace_size.argtypes = [i64, i64, i64, ctypes.POINTER(Tune)]
+            L.tcec_sgemm_workspace_size.restype = sz
+            L.tcec_plan.argtypes = [i64, i64, i64, ctypes.POINTER(Tune), ctypes.POINTER(Plan)]
             L.shg_launch_count.restype = u64
             L.shg_last_error.restype = ctypes.c_char_p
             L.shg_device_supported.restype = i32
@@ -91,7 +97,7 @@ def lib():
             L.shg_probe_mma2_rate.restype = i32
             for name in ("shgemm", "shgemm_ex", "shgemm_at", "shgemm_host", "shg_plan", "gen_omega_f16", "gen_omega_f16_ex", "project",
                          "shg_debug_split", "shg_synth_f32", "shg_probe_umma", "shgemm_tf32", "project_ex",
-                         "shg_debug_split_tf32"):
+                         "shg_debug_split_tf32", "tcec_sgemm", "tcec_sgemm_ex", "tcec_plan"):
                 getattr(L, name).restype = i32
             _lib = L
     return _lib
@@ -244,6 +250,56 @@ def plan(m: int, n: int, k: int, tune=None, tc=None) -> dict:
 
 def workspace_size(m: int, n: int, k: int, tune=None, tc=None) -> int:
     return int(lib().shg_workspace_size(m, n, k, _tune(tune, tc)))
+
+
+# ---------------------------------------------------------------------------------- TCEC-SGEMM
+def _layout_2d(t: torch.Tensor, k_dim: int, what: str):
+    """(layout, ld) of a 2-D float32 tensor for the C ABI: K_MAJOR (0) if the k dimension is
+    contiguous, MN_MAJOR (1) if the other one is."""
+    rows, cols = t.shape
+    other = 1 - k_dim
+    if t.shape[k_dim] <= 1 or t.stride(k_dim) == 1:
+        if t.shape[other] <= 1:
+            return 0, max(t.shape[k_dim], 1)
+        if t.stride(k_dim) == 1:
+            return 0, t.stride(other)
+    if t.stride(other) == 1:
+        return 1, (t.stride(k_dim) if t.shape[k_dim] > 1 else max(t.shape[other], 1))
+    raise ValueError(f"{what} must have one contiguous dimension (strides {t.stride()})")
+
+
+def tcec_sgemm(A: torch.Tensor, B: torch.Tensor, out: torch.Tensor | None = None, tune=None,
+               workspace: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+    """C = A . B for float32 A (m, k) and B (k, n) by TCEC-SGEMM (Eqs 5-9) on
+    the FP16 tensor cores. Either dimension of A and of B may be the contiguous one (e.g. pass
+    `X.t()` for X^T without a copy). Returns C (m, n) float32 row-major."""
+    if A.dtype != torch.float32 or B.dtype != torch.float32:
+        raise TypeError("A and B must be float32")
+    m, k = A.shape
+    k2, n = B.shape
+    if k2 != k:
+        raise ValueError(f"shape mismatch {tuple(A.shape)} x {tuple(B.shape)}")
+    a_layout, lda = _layout_2d(A, 1, "A")
+    b_layout, ldb = _layout_2d(B, 0, "B")
+    if out is None:
+        out = torch.empty((m, n), dtype=torch.float32, device=A.device)
+    elif out.dtype != torch.float32 or tuple(out.shape) != (m, n) or (m and n and out.stride(1) != 1):
+        raise ValueError("out must be (m, n) float32 row-major")
+    ldc = out.stride(0) if m > 1 else max(n, 1)
+    ws_bytes = 0 if workspace is None else workspace.numel() * workspace.element_size()
+    _check(lib().tcec_sgemm_ex(m, n, k, _p(A), lda, a_layout, _p(B), ldb, b_layout, _p(out), ldc, _tune(tune),
+                               _p(workspace), ws_bytes, _stream(stream)), "tcec_sgemm_ex")
+    return out
+
+
+def tcec_plan(m: int, n: int, k: int, tune=None) -> dict:
+    p = Plan()
+    _check(lib().tcec_plan(m, n, k, _tune(tune), ctypes.byref(p)), "tcec_plan")
+    return {f: getattr(p, f) for f, _ in Plan._fields_}
+
+
+def tcec_workspace_size(m: int, n: int, k: int, tune=None) -> int:
+    return int(lib().tcec_sgemm_workspace_size(m, n, k, _tune(tune)))
 
 
 # ----------------------------------------------------------------------------------------- project

@@ -18,6 +18,7 @@
 #include "shgemm_sm100.cuh"
 #include "simt_fallback.cuh"
 #include "split.cuh"
+#include "tcec.cuh"
 
 namespace shg_api {
 
@@ -139,6 +140,8 @@ template <int B> using CfgPair = shg::Cfg<B, true, false>;
 template <int B> using CfgSingle = shg::Cfg<B, false, false>;
 template <int B> using CfgPairT = shg::Cfg<B, true, true>;
 template <int B> using CfgSingleT = shg::Cfg<B, false, true>;
+template <int B> using CfgPairC = shg::Cfg<B, true, false, true>;
+template <int B> using CfgSingleC = shg::Cfg<B < 128 ? B : 128, false, false, true>;
 #define SHG_CFG_FIELD(bn, pair, tf32, FIELD)                                                              \
     if (tf32 && pair) { SHG_BN_SWITCH(bn, return CfgPairT<BN_>::FIELD) }                                  \
     if (tf32) { SHG_BN_SWITCH(bn, return CfgSingleT<BN_>::FIELD) }                                        \
@@ -150,37 +153,64 @@ int sa_for(int bn, bool pair, bool tf32) { SHG_CFG_FIELD(bn, pair, tf32, SA) }
 int so_for(int bn, bool pair, bool tf32) { SHG_CFG_FIELD(bn, pair, tf32, SO) }
 int r0_for(int bn, bool pair, bool tf32) { SHG_CFG_FIELD(bn, pair, tf32, R0) }
 int r1_for(int bn, bool pair, bool tf32) { SHG_CFG_FIELD(bn, pair, tf32, R1) }
+// TCEC-SGEMM configurations (pairs: BN >= 128; single CTAs: BN <= 128)
+#define SHG_CFG_FIELD_TCEC(bn, pair, FIELD)                                                              \
+    if (pair) { SHG_BN_SWITCH(bn, return CfgPairC<(BN_ < 128 ? 128 : BN_)>::FIELD) }                      \
+    SHG_BN_SWITCH(bn, return CfgSingleC<BN_>::FIELD)
+int smem_for_tcec(int bn, bool pair) { SHG_CFG_FIELD_TCEC(bn, pair, kSmemBytes) }
+int sa_for_tcec(int bn, bool pair) { SHG_CFG_FIELD_TCEC(bn, pair, SA) }
+int so_for_tcec(int bn, bool pair) { SHG_CFG_FIELD_TCEC(bn, pair, SO) }
+int r0_for_tcec(int bn, bool pair) { SHG_CFG_FIELD_TCEC(bn, pair, R0) }
+int r1_for_tcec(int bn, bool pair) { SHG_CFG_FIELD_TCEC(bn, pair, R1) }
 
 struct Plan {
     int path = 0;  // 0 tc, 1 simt, 2 trivial
     int bn = 0, n_tiles = 0, m_tiles = 0, splits = 1, grid = 0, num_kb = 0;
     bool pair = false;
     bool tf32 = false;        // SHGEMM-TF32 (tune->tc == SHG_TC_TF32)
-    // workspace = [split-K planes, 256-B aligned][TF32 copy of Omega (tc path only)]
+    bool tcec = false;        // TCEC-SGEMM (FP32 B split into B_low / dB_low)
+    // workspace = [split-K planes, 256-B aligned][TF32 copy of Omega | TCEC split of B]
     int64_t ws_bytes = 0, ld_ws = 0, sk_bytes = 0, om_bytes = 0, ldo32 = 0;
+    int64_t ldh = 0, noff = 0;  // TCEC: split B column-major, ld ldh; dB_low starts at column noff
 };
 
 int64_t up256(int64_t b) { return (b + 255) / 256 * 256; }
 
 
-Plan make_plan(int64_t m, int64_t n, int64_t k, bool fast_ok, const shg_tune_t* tune, int sms) {
+Plan make_plan(int64_t m, int64_t n, int64_t k, bool fast_ok, const shg_tune_t* tune, int sms, bool tcec = false) {
     Plan pl;
-    pl.tf32 = tune && tune->tc == SHG_TC_TF32;
+    pl.tf32 = !tcec && tune && tune->tc == SHG_TC_TF32;
+    pl.tcec = tcec;
     if (m == 0 || n == 0 || k == 0) { pl.path = 2; return pl; }
-    if (!fast_ok || (tune && tune->force_simt)) { pl.path = 1; return pl; }
-    pl.path = 0;
-    if (tune && tune->bn > 0 && valid_bn(tune->bn)) {
-        pl.bn = tune->bn;
-        pl.n_tiles = static_cast<int>((n + pl.bn - 1) / pl.bn);
-    } else {
-        pl.n_tiles = static_cast<int>((n + 255) / 256);
-        const int64_t need = (n + pl.n_tiles - 1) / pl.n_tiles;
-        pl.bn = 256;
-        for (int b : kBNs) if (b >= need) { pl.bn = b; break; }
+    if (tcec) {   // the B split runs on every path
+        pl.ldh = (k + 7) / 8 * 8;
     }
+    if (!fast_ok || (tune && tune->force_simt)) {
+        pl.path = 1;
+        if (tcec) {
+            pl.noff = n;
+            pl.om_bytes = 2 * pl.noff * pl.ldh * 2;
+            pl.ws_bytes = pl.om_bytes;
+        }
+        return pl;
+    }
+    pl.path = 0;
     // CTA pair: halves Omega's L2->SMEM traffic per SM (the power-cap lever at BN >= 128); needs > 128 rows
     const int pair_mode = tune ? tune->pair : 0;   // 0 auto, 1 force on, 2 force off
-    pl.pair = pair_ok(pl.bn) && ((pair_mode == 0 && m > shg::kBM) || pair_mode == 1);
+    const bool want_pair = (pair_mode == 0 && m > shg::kBM) || pair_mode == 1;
+    // TCEC stages two B tiles: single CTAs stop at BN = 128
+    const int max_bn = (tcec && !want_pair) ? kTcecMaxBnSingle : 256;
+    if (tune && tune->bn > 0 && valid_bn(tune->bn)) {
+        pl.bn = tune->bn;
+        if (pl.bn > max_bn) { pl.path = -1; return pl; }
+        pl.n_tiles = static_cast<int>((n + pl.bn - 1) / pl.bn);
+    } else {
+        pl.n_tiles = static_cast<int>((n + max_bn - 1) / max_bn);
+        const int64_t need = (n + pl.n_tiles - 1) / pl.n_tiles;
+        pl.bn = max_bn;
+        for (int b : kBNs) if (b >= need) { pl.bn = b; break; }
+    }
+    pl.pair = pair_ok(pl.bn) && want_pair;
     const int tile_m = pl.pair ? 2 * shg::kBM : shg::kBM;
     const int slots = pl.pair ? std::max(1, sms / 2) : sms;     // concurrent tiles
     pl.m_tiles = static_cast<int>((m + tile_m - 1) / tile_m);
@@ -207,6 +237,10 @@ Plan make_plan(int64_t m, int64_t n, int64_t k, bool fast_ok, const shg_tune_t* 
     if (pl.tf32) {   // Omega widened once to TF32 (exact) for the tensor cores' smem operand
         pl.ldo32 = (k + 3) / 4 * 4;
         pl.om_bytes = pl.ldo32 * n * 4;
+    }
+    if (pl.tcec) {   // [B_low | pad | dB_low | pad], each n_tiles * BN columns (pads zeroed)
+        pl.noff = static_cast<int64_t>(pl.n_tiles) * pl.bn;
+        pl.om_bytes = 2 * pl.noff * pl.ldh * 2;
     }
     pl.ws_bytes = (pl.om_bytes ? up256(pl.sk_bytes) : pl.sk_bytes) + pl.om_bytes;
     return pl;
@@ -242,9 +276,11 @@ struct AView {
     bool mmajor = false;
 };
 
+// B32 != nullptr selects TCEC-SGEMM: B element (l, j) at B32[l * sbk + j * sbn] (FP32), Om unused.
 shg_status_t run_shgemm(int64_t m, int64_t n, int64_t k, const AView& av, const uint16_t* Om, int64_t ldo,
                         float* Y, int64_t ldc, const shg_tune_t* tune, void* ws, size_t ws_bytes, int* nonfinite,
-                        cudaStream_t stream) {
+                        cudaStream_t stream, const float* B32 = nullptr, int64_t sbk = 0, int64_t sbn = 0) {
+    const bool tcec = B32 != nullptr;
     if (m == 0 || n == 0) return SHG_OK;
     if (k == 0) {
         SHG_CUDA(cudaMemset2DAsync(Y, ldc * sizeof(float), 0, n * sizeof(float), m, stream));
@@ -254,9 +290,30 @@ shg_status_t run_shgemm(int64_t m, int64_t n, int64_t k, const AView& av, const 
     if (!d.ok) return SHG_ERR_UNSUPPORTED_DEVICE;
     const bool plain = (av.P == 1 && av.S == k);
     const bool fast_ok = aligned16(av.A) && aligned16(Om) && (av.row_stride % 4 == 0) && (av.slab % 4 == 0) &&
-                         (ldo % 8 == 0) && (plain || av.S % shg::kBK == 0) && encode_fn() != nullptr &&
+                         (tcec || ldo % 8 == 0) && (plain || av.S % shg::kBK == 0) && encode_fn() != nullptr &&
                          k < (int64_t(1) << 31) && av.S < (int64_t(1) << 31) && m < (int64_t(1) << 31);
-    Plan pl = make_plan(m, n, k, fast_ok, tune, d.sms);
+    Plan pl = make_plan(m, n, k, fast_ok, tune, d.sms, tcec);
+    if (pl.path < 0) return SHG_ERR_INVALID_VALUE;
+    if (pl.path == 1 && tcec) {
+        if (!plain) return SHG_ERR_INVALID_VALUE;
+        void* own = nullptr;
+        uint16_t* H = static_cast<uint16_t*>(ws);
+        if (ws && ws_bytes < static_cast<size_t>(pl.ws_bytes)) return SHG_ERR_WORKSPACE;
+        if (!ws) {
+            SHG_CUDA(cudaMallocAsync(&own, pl.ws_bytes, stream));
+            H = static_cast<uint16_t*>(own);
+        }
+        shg::split_b_kernel<<<grid_for(((k + 31) / 32) * ((pl.noff + 31) / 32) * 256, 256), dim3(32, 8), 0, stream>>>(
+            B32, k, n, sbk, sbn, H, pl.ldh, pl.noff);
+        const int64_t sa_row = av.mmajor ? 1 : av.row_stride, sa_col = av.mmajor ? av.row_stride : 1;
+        shg::tcec_simt_kernel<<<grid_for(m * n, 256), 256, 0, stream>>>(m, n, k, av.A, sa_row, sa_col, H, pl.ldh,
+                                                                       pl.noff, Y, ldc);
+        g_launches.fetch_add(2, std::memory_order_relaxed);
+        const cudaError_t e = cudaGetLastError();
+        if (own) cudaFreeAsync(own, stream);
+        if (e != cudaSuccess) return cuda_fail(e, "tcec_simt_kernel");
+        return SHG_OK;
+    }
     if (pl.path == 1) {
         if (!plain) return SHG_ERR_INVALID_VALUE;  // callers materialise non-plain views first
         const int64_t sa_row = av.mmajor ? 1 : av.row_stride, sa_col = av.mmajor ? av.row_stride : 1;
@@ -301,12 +358,20 @@ shg_status_t run_shgemm(int64_t m, int64_t n, int64_t k, const AView& av, const 
         }
         return st;
     };
-    // Omega operand: FP16 as given (SHGEMM-FP16), or its exact TF32 widening (SHGEMM-TF32)
-    const int rows0 = pl.pair ? r0_for(pl.bn, true, pl.tf32) : pl.bn;
-    const int r1 = r1_for(pl.bn, pl.pair, pl.tf32);
+    // Omega operand: FP16 as given (SHGEMM-FP16), or its exact TF32 widening (SHGEMM-TF32),
+    // or TCEC-SGEMM's [B_low | dB_low] split of an FP32 B (Eqs 5-9)
+    const int rows0 = pl.pair ? (tcec ? r0_for_tcec(pl.bn, true) : r0_for(pl.bn, true, pl.tf32)) : pl.bn;
+    const int r1 = tcec ? r1_for_tcec(pl.bn, pl.pair) : r1_for(pl.bn, pl.pair, pl.tf32);
     const int rows1 = r1 > 0 ? r1 : rows0;         // one N part (R1 == 0): mapB1 unused
     bool encb_ok;
-    if (pl.tf32) {
+    if (tcec) {
+        uint16_t* H = reinterpret_cast<uint16_t*>(wsb + up256(pl.sk_bytes));
+        shg::split_b_kernel<<<grid_for(((k + 31) / 32) * ((pl.noff + 31) / 32) * 256, 256), dim3(32, 8), 0, stream>>>(
+            B32, k, n, sbk, sbn, H, pl.ldh, pl.noff);
+        g_launches.fetch_add(1, std::memory_order_relaxed);
+        if (cudaGetLastError() != cudaSuccess) return finish(cuda_fail(cudaErrorLaunchFailure, "split_b_kernel"));
+        encb_ok = encode_b(&mapB0, H, k, 2 * pl.noff, pl.ldh, rows0) && encode_b(&mapB1, H, k, 2 * pl.noff, pl.ldh, rows1);
+    } else if (pl.tf32) {
         float* om32 = reinterpret_cast<float*>(wsb + up256(pl.sk_bytes));
         shg::widen_omega_kernel<<<grid_for(k * n, 256), 256, 0, stream>>>(Om, k, n, ldo, om32, pl.ldo32);
         g_launches.fetch_add(1, std::memory_order_relaxed);
@@ -325,6 +390,7 @@ shg_status_t run_shgemm(int64_t m, int64_t n, int64_t k, const AView& av, const 
     kp.num_kb = pl.num_kb;
     kp.m_tiles = pl.m_tiles; kp.n_tiles = pl.n_tiles; kp.splits = pl.splits;
     kp.a_rowpair = rowpair ? 1 : 0;
+    kp.b_lo_col = static_cast<int32_t>(pl.noff);
     kp.dbg = tune ? static_cast<uint32_t>(tune->debug_flags) : 0u;
     kp.prof = tune ? reinterpret_cast<long long*>(tune->prof) : nullptr;
     if (pl.splits > 1) {
@@ -341,8 +407,9 @@ shg_status_t run_shgemm(int64_t m, int64_t n, int64_t k, const AView& av, const 
         kp.vec_store = (aligned16(Y) && ldc % 4 == 0) ? 1 : 0;
         kp.nonfinite = nonfinite;
     }
-    shg_status_t st = pl.tf32 ? dispatch_tc_tf32(pl.bn, av.mmajor, pl.pair, mapA, mapB0, mapB1, kp, pl.grid, stream)
-                              : dispatch_tc_f16(pl.bn, av.mmajor, pl.pair, mapA, mapB0, mapB1, kp, pl.grid, stream);
+    shg_status_t st = tcec      ? dispatch_tc_tcec(pl.bn, av.mmajor, pl.pair, mapA, mapB0, mapB1, kp, pl.grid, stream)
+                      : pl.tf32 ? dispatch_tc_tf32(pl.bn, av.mmajor, pl.pair, mapA, mapB0, mapB1, kp, pl.grid, stream)
+                                : dispatch_tc_f16(pl.bn, av.mmajor, pl.pair, mapA, mapB0, mapB1, kp, pl.grid, stream);
     if (st != SHG_OK) return finish(st);
     if (pl.splits > 1) {
         shg::splitk_reduce_kernel<<<grid_for(m * n, 256), 256, 0, stream>>>(kp.out, pl.splits, m, n, pl.ld_ws,
@@ -480,6 +547,60 @@ shg_status_t shgemm_at(int64_t m, int64_t n, int64_t k, const float* At, int64_t
     AView av{At, k, 1, ldat, 0, true};
     return run_shgemm(m, n, k, av, Omega, ldo, Y, ldc, tune, workspace, workspace_bytes, nonfinite_flag,
                       reinterpret_cast<cudaStream_t>(stream));
+}
+
+shg_status_t tcec_sgemm_ex(int64_t m, int64_t n, int64_t k, const float* A, int64_t lda, int a_layout, const float* B,
+                           int64_t ldb, int b_layout, float* C, int64_t ldc, const shg_tune_t* tune, void* workspace,
+                           size_t workspace_bytes, shg_stream_t stream) {
+    if (m < 0 || n < 0 || k < 0) return SHG_ERR_INVALID_VALUE;
+    if ((a_layout != SHG_LAYOUT_K_MAJOR && a_layout != SHG_LAYOUT_MN_MAJOR) ||
+        (b_layout != SHG_LAYOUT_K_MAJOR && b_layout != SHG_LAYOUT_MN_MAJOR))
+        return SHG_ERR_INVALID_VALUE;
+    if (m == 0 || n == 0) return SHG_OK;
+    if (!C || ldc < n) return SHG_ERR_INVALID_VALUE;
+    if (k > 0) {
+        if (!A || !B) return SHG_ERR_INVALID_VALUE;
+        if (lda < (a_layout == SHG_LAYOUT_K_MAJOR ? k : m)) return SHG_ERR_INVALID_VALUE;
+        if (ldb < (b_layout == SHG_LAYOUT_K_MAJOR ? k : n)) return SHG_ERR_INVALID_VALUE;
+    }
+    if (tune && tune->bn > 0 && !valid_bn(tune->bn)) return SHG_ERR_INVALID_VALUE;
+    const AView av = a_layout == SHG_LAYOUT_K_MAJOR ? AView{A, k, 1, lda, lda * std::max<int64_t>(m, 1)}
+                                                    : AView{A, k, 1, lda, 0, true};
+    const int64_t sbk = b_layout == SHG_LAYOUT_K_MAJOR ? 1 : ldb;
+    const int64_t sbn = b_layout == SHG_LAYOUT_K_MAJOR ? ldb : 1;
+    return run_shgemm(m, n, k, av, nullptr, 8, C, ldc, tune, workspace, workspace_bytes, nullptr,
+                      reinterpret_cast<cudaStream_t>(stream), B ? B : reinterpret_cast<const float*>(C), sbk, sbn);
+}
+
+shg_status_t tcec_sgemm(int64_t m, int64_t n, int64_t k, const float* A, int64_t lda, int a_layout, const float* B,
+                        int64_t ldb, int b_layout, float* C, int64_t ldc, shg_stream_t stream) {
+    return tcec_sgemm_ex(m, n, k, A, lda, a_layout, B, ldb, b_layout, C, ldc, nullptr, nullptr, 0, stream);
+}
+
+size_t tcec_sgemm_workspace_size(int64_t m, int64_t n, int64_t k, const shg_tune_t* tune) {
+    if (m <= 0 || n <= 0 || k <= 0) return 0;
+    const Plan pl = make_plan(m, n, k, true, tune, std::max(1, dev_info().sms), true);
+    return pl.path < 0 ? 0 : static_cast<size_t>(pl.ws_bytes);
+}
+
+shg_status_t tcec_plan(int64_t m, int64_t n, int64_t k, const shg_tune_t* tune, shg_plan_t* out) {
+    if (!out || m < 0 || n < 0 || k < 0) return SHG_ERR_INVALID_VALUE;
+    const Plan pl = make_plan(m, n, k, true, tune, std::max(1, dev_info().sms), true);
+    if (pl.path < 0) return SHG_ERR_INVALID_VALUE;
+    std::memset(out, 0, sizeof(*out));
+    out->path = pl.path;
+    out->bn = pl.bn; out->n_tiles = pl.n_tiles; out->m_tiles = pl.m_tiles; out->split_k = pl.splits;
+    out->grid = pl.grid;
+    out->tc = SHG_TC_TCEC;
+    if (pl.path == 0) {
+        out->stages_a = sa_for_tcec(pl.bn, pl.pair);
+        out->stages_b = so_for_tcec(pl.bn, pl.pair);
+        out->smem_bytes = smem_for_tcec(pl.bn, pl.pair);
+        out->cta_pair = pl.pair ? 1 : 0;
+        out->kernels = 2 + (pl.splits > 1 ? 1 : 0);
+    }
+    out->workspace_bytes = pl.ws_bytes;
+    return SHG_OK;
 }
 
 size_t shg_workspace_size(int64_t m, int64_t n, int64_t k, const shg_tune_t* tune) {

@@ -48,11 +48,11 @@ inline bool valid_bn(int bn) {
     return false;
 }
 
-template <int BN, bool MMAJOR, bool PAIR, bool TF32>
+template <int BN, bool MMAJOR, bool PAIR, bool TF32, bool TCEC = false>
 shg_status_t launch_tc(const CUtensorMap& mapA, const CUtensorMap& mapB0, const CUtensorMap& mapB1,
                        const shg::KParams& kp, int grid, cudaStream_t stream) {
-    using CF = shg::Cfg<BN, PAIR, TF32>;
-    auto kern = shg::shgemm_sm100_kernel<BN, MMAJOR, PAIR, TF32>;
+    using CF = shg::Cfg<BN, PAIR, TF32, TCEC>;
+    auto kern = shg::shgemm_sm100_kernel<BN, MMAJOR, PAIR, TF32, TCEC>;
     static std::once_flag flags[64];
     int dev = 0;
     cudaGetDevice(&dev);
@@ -103,10 +103,15 @@ shg_status_t dispatch_bn(int bn, const CUtensorMap& a, const CUtensorMap& b0, co
     }
 }
 
-// Defined in tc_f16.cu / tc_tf32.cu (one instantiation set per translation unit).
+// TCEC-SGEMM: two B tiles per stage, so single CTAs stop at BN = 128 (smem); pairs cover 128..256
+constexpr int kTcecMaxBnSingle = 128;
+
+// Defined in tc_f16.cu / tc_tf32.cu / tc_tcec.cu (one instantiation set per translation unit).
 shg_status_t dispatch_tc_f16(int bn, bool mmajor, bool pair, const CUtensorMap& a, const CUtensorMap& b0,
                              const CUtensorMap& b1, const shg::KParams& kp, int grid, cudaStream_t s);
 shg_status_t dispatch_tc_tf32(int bn, bool mmajor, bool pair, const CUtensorMap& a, const CUtensorMap& b0,
+                              const CUtensorMap& b1, const shg::KParams& kp, int grid, cudaStream_t s);
+shg_status_t dispatch_tc_tcec(int bn, bool mmajor, bool pair, const CUtensorMap& a, const CUtensorMap& b0,
                               const CUtensorMap& b1, const shg::KParams& kp, int grid, cudaStream_t s);
 
 }  // namespace shg_api

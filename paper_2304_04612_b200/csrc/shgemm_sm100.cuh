@@ -66,6 +66,7 @@ struct KParams {
     int64_t ldo_out;        // leading dimension of out (elements)
     int64_t split_stride;   // elements between split planes (workspace)
     int32_t vec_store;      // out rows 16-B aligned and ldo_out % 4 == 0
+    int32_t b_lo_col;       // TCEC: column (n) coordinate of dB_low in the B tensor maps (B_low at 0)
     int* nonfinite;         // optional flag (set to 1 on any non-finite output)
     uint32_t dbg;           // diagnostics: bit0 skip promotion loads, bit1 skip split math, bit2 skip MMAs,
                             //              bit3 skip the Omega TMA (results are wrong when dbg != 0)
@@ -140,7 +141,11 @@ __device__ __forceinline__ void cluster_sync_all() {
 // TF32 = false: SHGEMM-FP16 (kind::f16, hi/lo packed 2 per 32-bit TMEM column, Omega FP16 in smem).
 // TF32 = true : SHGEMM-TF32 (kind::tf32, one hi or lo element per TMEM column,
 //               Omega as TF32 (the exactly widened FP16 values) in smem, two 128-B k-halves a stage).
-template <int BN, bool PAIR, bool TF32 = false>
+// TCEC = true: TCEC-SGEMM (Eqs 5-9; NEXT-2): A split in-kernel exactly as for
+//               SHGEMM-FP16; B (FP32) pre-split into FP16 B_low / dB_low, whose tiles sit side by
+//               side in each Omega smem stage (NB = 2); per chunk the MMA issuer accumulates
+//               dA_low.B_low + A_low.dB_low, then folds it under A_low.B_low with scale-input-d = 11.
+template <int BN, bool PAIR, bool TF32 = false, bool TCEC = false>
 struct Cfg {
     // FP16: K_c = 128, one promotion chunk = 2 stages of 64 k; TMEM: 4 A stages (2 chunks of hi/lo,
     // 64 columns each) + accumulator slots. TF32: a stage's hi/lo take 128 columns, so K_c = 64 =
@@ -168,7 +173,9 @@ struct Cfg {
     static constexpr int SO = NCH * KC;                    // Omega smem stages
     static constexpr int R0 = PAIR ? W / 2 : W;            // Omega rows of part 0 held by this CTA
     static constexpr int R1 = NQ == 1 ? 0 : (PAIR ? WLAST / 2 : WLAST);   // ... of part 1
-    static constexpr int kOmStageBytes = (R0 + R1) * kBK * EB;   // TF32: [k-half][R0 + R1 rows][128 B]
+    static constexpr int NB = TCEC ? 2 : 1;                // B tiles per stage (TCEC: B_low, then dB_low)
+    static constexpr int kOmTileBytes = (R0 + R1) * kBK * EB;   // TF32: [k-half][R0 + R1 rows][128 B]
+    static constexpr int kOmStageBytes = NB * kOmTileBytes;
     static constexpr int kTileM = PAIR ? 2 * kBM : kBM;   // rows per (pair) tile
     static constexpr int kBarBytes = 512;
     static constexpr int SA_fit = (kSmemLimit - 1024 - kBarBytes - SO * kOmStageBytes) / kA32StageBytes;
@@ -179,6 +186,7 @@ struct Cfg {
     static_assert(!PAIR || (R0 % 8 == 0 && R1 % 8 == 0), "pair halves must be whole 8-row core groups");
     static_assert(NSLOT >= NQ, "TMEM accumulator slots");
     static_assert(SA >= 2 && kSmemBytes <= kSmemLimit, "smem");
+    static_assert(!(TF32 && TCEC), "TCEC-SGEMM is instantiated for FP16 tensor cores only");
 };
 
 __device__ __forceinline__ void tile_coords(int tile, const KParams& p, int& m_blk, int& s, int& n_blk) {
@@ -310,11 +318,11 @@ __device__ __forceinline__ void add2_rn(float& a, float& b, float c, float d) {
 // PAIR          : CTA pair (launch with cluster dims (2,1,1)); see the header comment.
 // TF32          : SHGEMM-TF32 (toLow = TF32; Cfg's header); mapB0/B1 then describe the FP32 (TF32)
 //                 copy of Omega.
-template <int BN, bool MMAJOR, bool PAIR, bool TF32 = false>
+template <int BN, bool MMAJOR, bool PAIR, bool TF32 = false, bool TCEC = false>
 __global__ void __launch_bounds__(kThreads, 1)
 shgemm_sm100_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB0,
                     const __grid_constant__ CUtensorMap mapB1, const KParams p) {
-    using CF = Cfg<BN, PAIR, TF32>;
+    using CF = Cfg<BN, PAIR, TF32, TCEC>;
     constexpr int SA = CF::SA, NQ = CF::NQ, W = CF::W, WLAST = CF::WLAST;
     constexpr int NPH = CF::NPH, NSLOT = CF::NSLOT, ABASE = CF::ABASE;
     constexpr int kOm = CF::kOmStageBytes;
@@ -672,13 +680,18 @@ shgemm_sm100_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_const
                                 for (int hh = 0; hh < (TF32 ? 2 : 1); ++hh) {
                                     uint8_t* dst = om + (cs * KC + t) * kOm + hh * (CF::R0 + CF::R1) * 128;
                                     const int kc = kcoord + 32 * hh;
-                                    if constexpr (PAIR) {
-                                        tma_load_omega<PAIR>(dst, &mapB0, &ch_ready[cs], kc,
-                                                             n0 + static_cast<int>(crank) * CF::R0, pol);
-                                        tma_load_omega<PAIR>(dst + CF::R0 * 128, &mapB1, &ch_ready[cs], kc,
-                                                             n0 + W + static_cast<int>(crank) * CF::R1, pol);
-                                    } else {   // the two parts are contiguous rows: one box of BN rows (mapB0)
-                                        tma_load_omega<PAIR>(dst, &mapB0, &ch_ready[cs], kc, n0, pol);
+#pragma unroll
+                                    for (int bt = 0; bt < CF::NB; ++bt) {   // TCEC: B_low tile, then dB_low
+                                        uint8_t* d2 = dst + bt * CF::kOmTileBytes;
+                                        const int nb0 = n0 + bt * p.b_lo_col;
+                                        if constexpr (PAIR) {
+                                            tma_load_omega<PAIR>(d2, &mapB0, &ch_ready[cs], kc,
+                                                                 nb0 + static_cast<int>(crank) * CF::R0, pol);
+                                            tma_load_omega<PAIR>(d2 + CF::R0 * 128, &mapB1, &ch_ready[cs], kc,
+                                                                 nb0 + W + static_cast<int>(crank) * CF::R1, pol);
+                                        } else {   // the two parts are contiguous rows: one box of BN rows (mapB0)
+                                            tma_load_omega<PAIR>(d2, &mapB0, &ch_ready[cs], kc, nb0, pol);
+                                        }
                                     }
                                 }
                             }
@@ -728,6 +741,17 @@ shgemm_sm100_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_const
                                             mma_ts<PAIR, TF32>(d, a_base + t * AST + AST / 2 + 8 * j,
                                                                b + static_cast<uint64_t>((t * kOm) >> 4) + boff(j), idesc,
                                                                (t > 0 || j > 0) ? 1u : 0u);
+                                // TCEC (Eq 9): D += A_low . dB_low, so D = dA_low B_low + A_low dB_low
+                                if constexpr (TCEC) {
+#pragma unroll
+                                    for (int t = 0; t < KC; ++t)
+                                        if (t < nst)
+#pragma unroll
+                                            for (int j = 0; j < NMMA; ++j)
+                                                mma_ts<PAIR, TF32>(d, a_base + t * AST + 8 * j,
+                                                                   b + static_cast<uint64_t>((t * kOm + CF::kOmTileBytes) >> 4) + boff(j),
+                                                                   idesc, 1u);
+                                }
                                 // D := hi . Omega + D * 2^-11 (first step), then the rest of hi
 #pragma unroll
                                 for (int t = 0; t < KC; ++t)

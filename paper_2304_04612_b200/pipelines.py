@@ -8,6 +8,11 @@ TF32 disabled). `projection="sgemm"` is the FP32 baseline of the paper's speedup
 "the random matrix is FP16 when using SHGEMM, otherwise FP32"): the same Gaussian stream kept in
 FP32 (OMEGA_SPEC §6 values before FP16 rounding) and a cuBLAS SGEMM. Per-line device times are
 recorded with CUDA events (the Fig 8 / Fig 9 breakdowns).
+
+`gemm="tcec"` also moves the pipelines' other FP32 products onto the tensor cores
+with the library's TCEC-SGEMM (Eqs 5-9): RSVD line 3 (B = Q^T A, computed as
+B^T = A^T Q with A read in place) and the RP-HOSVD core contractions
+(Alg 2 line 5). `gemm="sgemm"` keeps them on cuBLAS FP32 (TF32 off) as in the paper.
 """
 from __future__ import annotations
 
@@ -15,7 +20,7 @@ import contextlib
 
 import torch
 
-from . import gen_omega, project, project_workspace_size, shgemm, synth
+from . import gen_omega, project, project_workspace_size, shgemm, synth, tcec_sgemm
 
 
 @contextlib.contextmanager
@@ -65,8 +70,10 @@ def omega_fp32(k: int, n: int, seed: int = 0, stream_id: int = 0, device="cuda")
 
 
 def rsvd(A: torch.Tensor, p: int, s: int = 10, seed: int = 0, dist="gaussian", projection="shgemm",
-         timing: bool = False):
+         timing: bool = False, gemm: str = "sgemm"):
     """Alg 1: Y = A Omega; Q = QR(Y); B = Q^T A; (U', S, V) = tSVD(B, p); U = Q U'."""
+    if gemm not in ("sgemm", "tcec"):
+        raise ValueError(gemm)
     m, n = A.shape
     nhat = p + s
     t = _Timer(timing)
@@ -83,11 +90,11 @@ def rsvd(A: torch.Tensor, p: int, s: int = 10, seed: int = 0, dist="gaussian", p
         t.mark("2_qr")
         Q = _qr_pos(Y)
         t.mark("3_QtA")
-        B = Q.t() @ A
+        B = tcec_sgemm(A.t(), Q).t() if gemm == "tcec" else Q.t() @ A
         t.mark("4_svd")
         Uh, S, Vt = torch.linalg.svd(B, full_matrices=False)
         t.mark("5_QU")
-        U = Q @ Uh[:, :p]
+        U = Q @ Uh[:, :p]     # 16384 x 272 x 256: launch-bound either way, left on cuBLAS
         t.mark("end")
     return {"U": U, "S": S[:p], "V": Vt[:p].t(), "Q": Q, "times_ms": t.result()}
 
@@ -109,9 +116,25 @@ def mode_product(T, M, mode):
     return torch.movedim(out, -1, mode)
 
 
-def rp_hosvd(T: torch.Tensor, ranks, seed: int = 0, dist="gaussian", projection="shgemm", timing=False):
+def core_tcec(T: torch.Tensor, Qs) -> torch.Tensor:
+    """g = T x_1 Q_1^T ... x_N Q_N^T by TCEC-SGEMM: each step contracts the LEADING mode of the
+    current C-order tensor, G'[rest, j] = sum_i g[i, rest] Q[i, j] — an MN-major A read in place
+    (the (I x rest) view transposed) times an N-major Q — which moves the new mode to the end; after
+    N steps the modes are back in order (J_1, ..., J_N)."""
+    g = T.contiguous()
+    for Q in Qs:
+        I = g.shape[0]
+        rest = g.shape[1:]
+        g = tcec_sgemm(g.reshape(I, -1).t(), Q).reshape(*rest, Q.shape[1])
+    return g
+
+
+def rp_hosvd(T: torch.Tensor, ranks, seed: int = 0, dist="gaussian", projection="shgemm", timing=False,
+             gemm: str = "sgemm"):
     """Alg 2: for each mode W = A'_(i) Omega_(i) (project, stream_id = mode), Q_i = QR(W);
     g = A x_1 Q_1^T ... x_N Q_N^T."""
+    if gemm not in ("sgemm", "tcec"):
+        raise ValueError(gemm)
     t = _Timer(timing)
     Qs = []
     ws = None
@@ -132,9 +155,12 @@ def rp_hosvd(T: torch.Tensor, ranks, seed: int = 0, dist="gaussian", projection=
             t.mark("3_qr")
             Qs.append(_qr_pos(W))
         t.mark("5_core")
-        g = T
-        for i, Q in enumerate(Qs):
-            g = mode_product(g, Q, i)
+        if gemm == "tcec":
+            g = core_tcec(T, Qs)
+        else:
+            g = T
+            for i, Q in enumerate(Qs):
+                g = mode_product(g, Q, i)
         t.mark("end")
     return {"core": g, "Q": Qs, "times_ms": t.result()}
 

@@ -31,7 +31,8 @@ def test_header_declares_the_boundary():
     names = declared_functions()
     for need in ("shgemm", "shgemm_ex", "gen_omega_f16", "gen_omega_f16_ex", "project", "shg_debug_split",
                  "shg_workspace_size", "shg_plan", "shg_project_workspace_size", "shg_synth_f32",
-                 "shg_launch_count", "shg_last_error", "shg_device_supported", "shg_version", "shg_probe_umma"):
+                 "shg_launch_count", "shg_last_error", "shg_device_supported", "shg_version", "shg_probe_umma",
+                 "tcec_sgemm", "tcec_sgemm_ex", "tcec_sgemm_workspace_size", "tcec_plan"):
         assert need in names, need
 
 
@@ -65,6 +66,16 @@ def test_argument_validation_without_gpu(shg):
     dims = (ctypes.c_int64 * 3)(2, 3, 4)
     assert L.project(ctypes.c_void_p(16), 3, dims, 3, 4, 0, 0, ctypes.c_void_p(16), 4, None, 0, None) == 1
     assert L.shg_probe_umma(None, None, 24, None, 0, 4, None, None) == 1
+    # TCEC-SGEMM: negative dims, bad layouts, short leading dimensions, NULL operands
+    v = ctypes.c_void_p(16)
+    assert L.tcec_sgemm(-1, 4, 4, v, 4, 0, v, 4, 0, v, 4, None) == 1
+    assert L.tcec_sgemm(4, 4, 4, v, 4, 2, v, 4, 0, v, 4, None) == 1          # a_layout
+    assert L.tcec_sgemm(4, 4, 4, v, 4, 0, v, 4, 5, v, 4, None) == 1          # b_layout
+    assert L.tcec_sgemm(4, 4, 8, v, 4, 0, v, 8, 0, v, 4, None) == 1          # lda < k (K-major A)
+    assert L.tcec_sgemm(8, 4, 4, v, 4, 1, v, 4, 0, v, 4, None) == 1          # lda < m (MN-major A)
+    assert L.tcec_sgemm(4, 8, 4, v, 4, 0, v, 4, 1, v, 8, None) == 1          # ldb < n (N-major B)
+    assert L.tcec_sgemm(4, 4, 4, None, 4, 0, v, 4, 0, v, 4, None) == 1       # NULL A
+    assert L.tcec_sgemm(4, 0, 4, None, 4, 0, None, 4, 0, None, 4, None) == 0  # n == 0: no-op
 
 
 def test_python_binding_has_no_fallback(shg, monkeypatch, tmp_path):

@@ -82,3 +82,48 @@ def test_rsvd_config2_full_size(shg, pl):
     floor = synth.eckart_young_floor("exp", N, p, s_p) / float(np.linalg.norm(A_h.astype(np.float64)))
     assert e_gpu >= floor * (1 - 1e-4)
     assert abs(e_gpu - e_or) <= 1e-4 * e_or, (e_gpu, e_or)
+
+
+# ------------------------------------------------------------ TCEC-SGEMM for the other products (NEXT-2)
+@pytest.mark.parametrize("kind", ["linear", "exp"])
+def test_rsvd_tcec_matches_oracle_pipeline(shg, pl, kind):
+    """Alg 1 with lines 3 and 5 on TCEC-SGEMM: same residual as the FP32 oracle pipeline (R10)."""
+    from oracle import pipelines as opl
+    N, p, s, s_p = 512, 22, 10, 1e-2
+    A = synth.spectrum_matrix(synth.spectrum(kind, N, p, s_p), seed=3)
+    r = pl.rsvd(torch.from_numpy(A).cuda(), p, s, seed=4, gemm="tcec")
+    e_gpu = pl.reconstruction_error(torch.from_numpy(A).cuda(), r["U"], r["S"], r["V"])
+    e_or = opl.rsvd(A, p, s, seed=4, precision="f32")["residual"]
+    assert abs(e_gpu - e_or) <= 1e-4 * e_or, (e_gpu, e_or)
+
+
+def test_core_tcec_matches_mode_products(shg, pl):
+    """core_tcec (leading-mode contractions on TCEC-SGEMM) == the FP64 mode products within the
+    SGEMM-level bound, and the RP-HOSVD residual with it matches the oracle pipeline."""
+    from oracle import pipelines as opl
+    T = synth.alg3_tensor((64, 48, 40), (16, 16, 16), pad=4, seed=5, noise=1e-2)
+    Tc = torch.from_numpy(T).cuda()
+    Qs = [torch.linalg.qr(torch.randn(d, 16, device="cuda", dtype=torch.float64))[0].float() for d in T.shape]
+    g = pl.core_tcec(Tc, Qs)
+    g64 = Tc.double()
+    for i, Q in enumerate(Qs):
+        g64 = pl.mode_product(g64, Q.double(), i)
+    rel = float(torch.linalg.norm(g.double() - g64) / torch.linalg.norm(g64))
+    assert rel <= 1e-6, rel
+    r = pl.rp_hosvd(Tc, (16, 16, 16), seed=2, gemm="tcec")
+    e_gpu = pl.hosvd_error(Tc, r["core"], r["Q"])
+    e_or = opl.rp_hosvd(T, (16, 16, 16), seed=2, precision="f32")["residual"]
+    assert abs(e_gpu - e_or) <= 1e-4 * e_or, (e_gpu, e_or)
+
+
+def test_rsvd_config2_full_size_tcec(shg, pl):
+    """cfg2 with TCEC-SGEMM for B = Q^T A: residual within 1e-4 relative of the SGEMM pipeline's
+    (which the previous test pins to the oracle at this size)."""
+    N, p, s, s_p = 16384, 256, 16, 1e-2
+    A = synth.spectrum_matrix_torch(synth.spectrum("exp", N, p, s_p), seed=1)
+    r_t = pl.rsvd(A, p, s, seed=0, gemm="tcec")
+    e_t = pl.reconstruction_error(A, r_t["U"], r_t["S"], r_t["V"])
+    del r_t
+    r_s = pl.rsvd(A, p, s, seed=0, gemm="sgemm")
+    e_s = pl.reconstruction_error(A, r_s["U"], r_s["S"], r_s["V"])
+    assert abs(e_t - e_s) <= 1e-4 * e_s, (e_t, e_s)
