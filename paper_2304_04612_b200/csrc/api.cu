@@ -169,12 +169,16 @@ struct Plan {
     bool pair = false;
     bool tf32 = false;        // SHGEMM-TF32 (tune->tc == SHG_TC_TF32)
     bool tcec = false;        // TCEC-SGEMM (FP32 B split into B_low / dB_low)
+    int np = 1;               // CTA pairs per cluster sharing Omega stages by multicast
     // workspace = [split-K planes, 256-B aligned][TF32 copy of Omega | TCEC split of B]
     int64_t ws_bytes = 0, ld_ws = 0, sk_bytes = 0, om_bytes = 0, ldo32 = 0;
     int64_t ldh = 0, noff = 0;  // TCEC: split B column-major, ld ldh; dB_low starts at column noff
 };
 
 int64_t up256(int64_t b) { return (b + 255) / 256 * 256; }
+
+// Omega multicast default (pairs per cluster) when tune->omega_mcast == 0 and the shape allows it
+constexpr int kAutoMcast = 1;
 
 
 Plan make_plan(int64_t m, int64_t n, int64_t k, bool fast_ok, const shg_tune_t* tune, int sms, bool tcec = false) {
@@ -211,9 +215,18 @@ Plan make_plan(int64_t m, int64_t n, int64_t k, bool fast_ok, const shg_tune_t* 
         for (int b : kBNs) if (b >= need) { pl.bn = b; break; }
     }
     pl.pair = pair_ok(pl.bn) && want_pair;
+    const int mc = tune ? tune->omega_mcast : 0;   // 0 auto, 1 off, 2 / 4 pairs per cluster
+    if (mc < 0 || mc == 3 || mc > 4) { pl.path = -1; return pl; }
     const int tile_m = pl.pair ? 2 * shg::kBM : shg::kBM;
     const int slots = pl.pair ? std::max(1, sms / 2) : sms;     // concurrent tiles
     pl.m_tiles = static_cast<int>((m + tile_m - 1) / tile_m);
+    if (mc >= 2) {
+        if (!pl.pair || pl.tf32 || pl.tcec || pl.m_tiles % mc) { pl.path = -1; return pl; }
+        pl.np = mc;
+    } else if (mc == 0 && pl.pair && !pl.tf32 && !pl.tcec && kAutoMcast > 1 && pl.m_tiles % kAutoMcast == 0 &&
+               pl.m_tiles >= kAutoMcast * 8) {
+        pl.np = kAutoMcast;
+    }
     pl.num_kb = static_cast<int>((k + shg::kBK - 1) / shg::kBK);
     const int64_t mn_tiles = static_cast<int64_t>(pl.m_tiles) * pl.n_tiles;
     int splits = 1;
@@ -228,8 +241,10 @@ Plan make_plan(int64_t m, int64_t n, int64_t k, bool fast_ok, const shg_tune_t* 
     pl.splits = splits;
     const int64_t tiles = mn_tiles * splits;
     int cap = (tune && tune->max_ctas > 0) ? tune->max_ctas : sms;
-    if (pl.pair) cap = std::max(2, cap / 2 * 2);
+    const int cl = pl.pair ? 2 * pl.np : 1;        // CTAs per cluster
+    cap = std::max(cl, cap / cl * cl);
     pl.grid = static_cast<int>(std::min<int64_t>(tiles * (pl.pair ? 2 : 1), cap));
+    pl.grid = std::max(cl, pl.grid / cl * cl);
     if (splits > 1) {
         pl.ld_ws = (n + 3) / 4 * 4;
         pl.sk_bytes = static_cast<int64_t>(splits) * m * pl.ld_ws * 4;
@@ -407,7 +422,9 @@ shg_status_t run_shgemm(int64_t m, int64_t n, int64_t k, const AView& av, const 
         kp.vec_store = (aligned16(Y) && ldc % 4 == 0) ? 1 : 0;
         kp.nonfinite = nonfinite;
     }
-    shg_status_t st = tcec      ? dispatch_tc_tcec(pl.bn, av.mmajor, pl.pair, mapA, mapB0, mapB1, kp, pl.grid, stream)
+    shg_status_t st = pl.np == 2 ? dispatch_tc_f16_mc2(pl.bn, av.mmajor, mapA, mapB0, mapB1, kp, pl.grid, stream)
+                      : pl.np == 4 ? dispatch_tc_f16_mc4(pl.bn, av.mmajor, mapA, mapB0, mapB1, kp, pl.grid, stream)
+                      : tcec      ? dispatch_tc_tcec(pl.bn, av.mmajor, pl.pair, mapA, mapB0, mapB1, kp, pl.grid, stream)
                       : pl.tf32 ? dispatch_tc_tf32(pl.bn, av.mmajor, pl.pair, mapA, mapB0, mapB1, kp, pl.grid, stream)
                                 : dispatch_tc_f16(pl.bn, av.mmajor, pl.pair, mapA, mapB0, mapB1, kp, pl.grid, stream);
     if (st != SHG_OK) return finish(st);
@@ -613,6 +630,7 @@ shg_status_t shg_plan(int64_t m, int64_t n, int64_t k, const shg_tune_t* tune, s
     if (!out || m < 0 || n < 0 || k < 0) return SHG_ERR_INVALID_VALUE;
     const int sms = std::max(1, dev_info().sms);
     const Plan pl = make_plan(m, n, k, true, tune, sms);
+    if (pl.path < 0) return SHG_ERR_INVALID_VALUE;
     std::memset(out, 0, sizeof(*out));
     out->path = pl.path;
     out->bn = pl.bn; out->n_tiles = pl.n_tiles; out->m_tiles = pl.m_tiles; out->split_k = pl.splits;
@@ -623,6 +641,7 @@ shg_status_t shg_plan(int64_t m, int64_t n, int64_t k, const shg_tune_t* tune, s
         out->smem_bytes = smem_for(pl.bn, pl.pair, pl.tf32);
         out->cta_pair = pl.pair ? 1 : 0;
         out->tc = pl.tf32 ? SHG_TC_TF32 : SHG_TC_FP16;
+        out->omega_mcast = pl.np;
         out->kernels = 1 + (pl.splits > 1 ? 1 : 0) + (pl.tf32 ? 1 : 0);
     } else {
         out->kernels = pl.path == 1 ? 1 : (k == 0 && m > 0 && n > 0 ? 0 : 0);

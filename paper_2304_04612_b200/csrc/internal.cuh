@@ -48,11 +48,11 @@ inline bool valid_bn(int bn) {
     return false;
 }
 
-template <int BN, bool MMAJOR, bool PAIR, bool TF32, bool TCEC = false>
+template <int BN, bool MMAJOR, bool PAIR, bool TF32, bool TCEC = false, int NP = 1>
 shg_status_t launch_tc(const CUtensorMap& mapA, const CUtensorMap& mapB0, const CUtensorMap& mapB1,
                        const shg::KParams& kp, int grid, cudaStream_t stream) {
     using CF = shg::Cfg<BN, PAIR, TF32, TCEC>;
-    auto kern = shg::shgemm_sm100_kernel<BN, MMAJOR, PAIR, TF32, TCEC>;
+    auto kern = shg::shgemm_sm100_kernel<BN, MMAJOR, PAIR, TF32, TCEC, NP>;
     static std::once_flag flags[64];
     int dev = 0;
     cudaGetDevice(&dev);
@@ -75,11 +75,27 @@ shg_status_t launch_tc(const CUtensorMap& mapA, const CUtensorMap& mapB0, const 
     cfg.stream = stream;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = PAIR ? 2 : 1;
+    attr[0].val.clusterDim.x = PAIR ? 2 * NP : 1;
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
+    // The grid is persistent: every cluster must be co-resident, or the clusters that do not fit
+    // run as a second wave. Clusters of 2*NP CTAs must sit in one GPC, so fewer than
+    // #SMs / (2*NP) may fit (GPC sizes are not multiples of 2*NP): clamp to the occupancy query.
+    static int max_clusters[64];
+    static std::once_flag occ_flags[64];
+    const int di = std::min(std::max(dev, 0), 63);
+    std::call_once(occ_flags[di], [&]() {
+        int nc = 0;
+        if (cudaOccupancyMaxActiveClusters(&nc, kern, &cfg) != cudaSuccess) {
+            (void)cudaGetLastError();
+            nc = 0;
+        }
+        max_clusters[di] = nc;
+    });
+    constexpr int kCl = PAIR ? 2 * NP : 1;
+    if (max_clusters[di] > 0 && grid > max_clusters[di] * kCl) cfg.gridDim = dim3(max_clusters[di] * kCl);
     SHG_CUDA(cudaLaunchKernelEx(&cfg, kern, mapA, mapB0, mapB1, kp));
     g_launches.fetch_add(1, std::memory_order_relaxed);
     return SHG_OK;
@@ -113,5 +129,10 @@ shg_status_t dispatch_tc_tf32(int bn, bool mmajor, bool pair, const CUtensorMap&
                               const CUtensorMap& b1, const shg::KParams& kp, int grid, cudaStream_t s);
 shg_status_t dispatch_tc_tcec(int bn, bool mmajor, bool pair, const CUtensorMap& a, const CUtensorMap& b0,
                               const CUtensorMap& b1, const shg::KParams& kp, int grid, cudaStream_t s);
+// SHGEMM-FP16 CTA pairs with Omega multicast across np = 2 (tc_f16_mc2.cu) or 4 (tc_f16_mc4.cu) pairs
+shg_status_t dispatch_tc_f16_mc2(int bn, bool mmajor, const CUtensorMap& a, const CUtensorMap& b0,
+                                 const CUtensorMap& b1, const shg::KParams& kp, int grid, cudaStream_t s);
+shg_status_t dispatch_tc_f16_mc4(int bn, bool mmajor, const CUtensorMap& a, const CUtensorMap& b0,
+                                 const CUtensorMap& b1, const shg::KParams& kp, int grid, cudaStream_t s);
 
 }  // namespace shg_api

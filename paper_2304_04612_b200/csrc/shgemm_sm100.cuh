@@ -245,16 +245,29 @@ __device__ __forceinline__ void mma_ts_scale11(uint32_t tmem_d, uint32_t tmem_a,
     else SHG_MMA_TS_SCALE11("1", "f16");
 }
 
-// completion of this thread's prior tcgen05 ops -> one arrive on `bar` (in both CTAs of a pair)
+// completion of this thread's prior tcgen05 ops -> one arrive on `bar` in every CTA of `mask`
+// (a pair: its two CTAs; an Omega-multicast cluster: all CTAs for the chunk-slot release)
 template <bool PAIR>
-__device__ __forceinline__ void commit_to(uint64_t* bar) {
+__device__ __forceinline__ void commit_to(uint64_t* bar, uint16_t mask = 3) {
     if constexpr (PAIR) {
         asm volatile(
             "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;"
-            ::"r"(smem_u32(bar)), "h"(static_cast<uint16_t>(3)) : "memory");
+            ::"r"(smem_u32(bar)), "h"(mask) : "memory");
     } else {
         tc_commit(bar);
     }
+}
+
+// Omega tile load for CTA pairs, multicast to the CTAs in `mask` (the same half of every pair of
+// the cluster); each destination's transaction bytes land on ITS pair leader's barrier
+__device__ __forceinline__ void tma_load_omega_mc(void* smem_dst, const CUtensorMap* map, uint64_t* bar, int32_t c0,
+                                                  int32_t c1, uint16_t mask, uint64_t policy) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster"
+        ".L2::cache_hint [%0], [%1, {%4, %5}], [%2], %3, %6;"
+        ::"r"(smem_u32(smem_dst)), "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar) & kPeerBitMask),
+          "h"(mask), "r"(c0), "r"(c1), "l"(policy)
+        : "memory");
 }
 
 // Omega tile load; in a pair the transaction bytes land on the leader's (even CTA's) barrier
@@ -316,9 +329,14 @@ __device__ __forceinline__ void add2_rn(float& a, float& b, float c, float d) {
 //                 gathers its row's k values with conflict-free 32-bit loads (one 128-B smem row per
 //                 warp instruction) — no transpose copy.
 // PAIR          : CTA pair (launch with cluster dims (2,1,1)); see the header comment.
-// TF32          : SHGEMM-TF32 (toLow = TF32; Cfg's header); mapB0/B1 then describe the FP32 (TF32)
-//                 copy of Omega.
-template <int BN, bool MMAJOR, bool PAIR, bool TF32 = false, bool TCEC = false>
+// TF32          : SHGEMM-TF32 (Cfg's header); mapB0/B1 then describe the FP32 (TF32) copy of Omega.
+// TCEC          : TCEC-SGEMM (Cfg's header): two B tiles per stage, three MMA groups per chunk.
+// NP            : CTA pairs per cluster (PAIR only). NP > 1 runs NP pairs on NP consecutive m-blocks in
+//                 lockstep (host: m_tiles % NP == 0) and MULTICASTS every Omega stage to them: stage t
+//                 of chunk c is loaded by pair (c*KC + t) % NP into the same half of every pair, so
+//                 Omega's L2 reads drop NP-fold (the power-cap lever). Chunk slots are
+//                 released to all pairs (ch_empty counts NP commits).
+template <int BN, bool MMAJOR, bool PAIR, bool TF32 = false, bool TCEC = false, int NP = 1>
 __global__ void __launch_bounds__(kThreads, 1)
 shgemm_sm100_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB0,
                     const __grid_constant__ CUtensorMap mapB1, const KParams p) {
@@ -346,16 +364,31 @@ shgemm_sm100_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_const
 
     const uint32_t warp = warp_id();
     const uint32_t lane = threadIdx.x & 31u;
-    const uint32_t crank = PAIR ? cluster_ctarank() : 0u;      // 0 = leader (issues the MMAs)
-    const int cta_of_tile = PAIR ? static_cast<int>(blockIdx.x >> 1) : static_cast<int>(blockIdx.x);
-    const int tile_stride = PAIR ? static_cast<int>(gridDim.x >> 1) : static_cast<int>(gridDim.x);
+    static_assert(NP == 1 || (PAIR && (NP == 2 || NP == 4)), "Omega multicast needs CTA pairs");
+    constexpr int CL = PAIR ? 2 * NP : 1;                         // CTAs per cluster
+    const uint32_t crank_cl = PAIR ? cluster_ctarank() : 0u;
+    const uint32_t crank = crank_cl & 1u;                         // rank in the pair: 0 = leader (issues the MMAs)
+    const uint32_t pp = crank_cl >> 1;                            // pair index in the cluster
+    const uint32_t lead = crank_cl & ~1u;                         // cluster rank of this pair's leader
+    const uint16_t pair_mask = static_cast<uint16_t>(3u << lead);
+    const uint16_t cl_mask = static_cast<uint16_t>((1u << CL) - 1u);
+    uint16_t half_mask = 0;                                       // this half in every pair of the cluster
+#pragma unroll
+    for (int q = 0; q < NP; ++q) half_mask |= static_cast<uint16_t>(1u << (2 * q + static_cast<int>(crank)));
+    const int cta_of_tile = static_cast<int>(blockIdx.x) / CL;
+    const int tile_stride = static_cast<int>(gridDim.x) / CL;
     constexpr int kPair = PAIR ? 2 : 1;
+    // cluster tiles (m-group, k-split, n-block); pair pp of the cluster takes m-block mg * NP + pp
+    auto coords = [&](int tile, int& m_blk, int& s, int& n_blk) {
+        tile_coords(tile, p, m_blk, s, n_blk);
+        m_blk = m_blk * NP + static_cast<int>(pp);
+    };
 
     if (threadIdx.x == 0) {
         for (int i = 0; i < SA; ++i) { mbar_init(&a_full[i], 1); mbar_init(&a_empty[i], kNumSplitWarps); }
         for (int i = 0; i < NCH; ++i) {
             mbar_init(&ch_ready[i], kPair * (kNumSplitWarps + 1));
-            mbar_init(&ch_empty[i], 1);
+            mbar_init(&ch_empty[i], NP);
         }
         for (int i = 0; i < NSLOT; ++i) { mbar_init(&acc_full[i], 1); mbar_init(&acc_empty[i], 4 * kPair); }
         fence_mbar_init();
@@ -379,7 +412,7 @@ shgemm_sm100_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_const
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
 
-    const int num_tiles = p.m_tiles * p.splits * p.n_tiles;
+    const int num_tiles = (p.m_tiles / NP) * p.splits * p.n_tiles;
     const long long t_kernel0 = clock64();
 
     if (warp < kNumSplitWarps) {
@@ -398,7 +431,7 @@ shgemm_sm100_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_const
         const bool skip_math = (p.dbg & 2u) != 0;
         for (int tile = cta_of_tile; tile < num_tiles; tile += tile_stride) {
             int m_blk, s, n_blk, kb0, kb1;
-            tile_coords(tile, p, m_blk, s, n_blk);
+            coords(tile, m_blk, s, n_blk);
             kb_range(s, p, kb0, kb1);
             for (int kb = kb0; kb < kb1; kb += KC) {
                 const int nst = (kb1 - kb) < KC ? (kb1 - kb) : KC;
@@ -504,7 +537,7 @@ shgemm_sm100_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_const
                 tc_fence_before();
                 __syncwarp();
                 if (lane == 0) {
-                    if constexpr (PAIR) mbar_arrive_cluster(&ch_ready[cs], 0u);
+                    if constexpr (PAIR) mbar_arrive_cluster(&ch_ready[cs], lead);
                     else mbar_arrive(&ch_ready[cs]);
                 }
                 advance(cs, pc, NCH);
@@ -528,7 +561,7 @@ shgemm_sm100_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_const
         const bool skip_ld = (p.dbg & 1u) != 0;
         for (int tile = cta_of_tile; tile < num_tiles; tile += tile_stride) {
             int m_blk, s, n_blk, kb0, kb1;
-            tile_coords(tile, p, m_blk, s, n_blk);
+            coords(tile, m_blk, s, n_blk);
             kb_range(s, p, kb0, kb1);
             float acc[NPH * W];
 #pragma unroll
@@ -566,7 +599,7 @@ shgemm_sm100_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_const
                     tc_fence_before();
                     __syncwarp();
                     if (lane == 0) {
-                        if constexpr (PAIR) mbar_arrive_cluster(&acc_empty[slot], 0u);
+                        if constexpr (PAIR) mbar_arrive_cluster(&acc_empty[slot], lead);
                         else mbar_arrive(&acc_empty[slot]);
                     }
                 }
@@ -622,7 +655,7 @@ shgemm_sm100_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_const
                 long long w = 0;
                 for (int tile = cta_of_tile; tile < num_tiles; tile += tile_stride) {
                     int m_blk, s, n_blk, kb0, kb1;
-                    tile_coords(tile, p, m_blk, s, n_blk);
+                    coords(tile, m_blk, s, n_blk);
                     kb_range(s, p, kb0, kb1);
                     const int m0 = m_blk * CF::kTileM + static_cast<int>(crank) * kBM;
                     for (int kb = kb0; kb < kb1; ++kb) {
@@ -657,10 +690,11 @@ shgemm_sm100_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_const
             if (elect_one()) {
                 const uint64_t pol = policy_evict_last();
                 uint32_t cs = 0, pc = 0;
+                uint32_t chunk_ctr = 0;
                 long long w = 0;
                 for (int tile = cta_of_tile; tile < num_tiles; tile += tile_stride) {
                     int m_blk, s, n_blk, kb0, kb1;
-                    tile_coords(tile, p, m_blk, s, n_blk);
+                    coords(tile, m_blk, s, n_blk);
                     kb_range(s, p, kb0, kb1);
                     const int n0 = n_blk * BN;
                     for (int kb = kb0; kb < kb1; kb += KC) {
@@ -670,10 +704,12 @@ shgemm_sm100_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_const
                         if (crank == 0) {
                             mbar_arrive_expect_tx(&ch_ready[cs], skip ? 0u : static_cast<uint32_t>(kPair * nst * kOm));
                         } else {
-                            mbar_arrive_cluster(&ch_ready[cs], 0u);
+                            mbar_arrive_cluster(&ch_ready[cs], lead);
                         }
                         if (!skip) {
                             for (int t = 0; t < nst; ++t) {
+                                // NP > 1: one pair per stage loads it for all pairs (multicast)
+                                if (NP > 1 && static_cast<uint32_t>((chunk_ctr * KC + t) % NP) != pp) continue;
                                 const int kcoord = kb_global(kb + t, s, p) * kBK;
                                 // FP16: one 128-B box row = 64 k; TF32: two k-halves of 32 k
 #pragma unroll
@@ -684,7 +720,12 @@ shgemm_sm100_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_const
                                     for (int bt = 0; bt < CF::NB; ++bt) {   // TCEC: B_low tile, then dB_low
                                         uint8_t* d2 = dst + bt * CF::kOmTileBytes;
                                         const int nb0 = n0 + bt * p.b_lo_col;
-                                        if constexpr (PAIR) {
+                                        if constexpr (PAIR && NP > 1) {
+                                            tma_load_omega_mc(d2, &mapB0, &ch_ready[cs], kc,
+                                                              nb0 + static_cast<int>(crank) * CF::R0, half_mask, pol);
+                                            tma_load_omega_mc(d2 + CF::R0 * 128, &mapB1, &ch_ready[cs], kc,
+                                                              nb0 + W + static_cast<int>(crank) * CF::R1, half_mask, pol);
+                                        } else if constexpr (PAIR) {
                                             tma_load_omega<PAIR>(d2, &mapB0, &ch_ready[cs], kc,
                                                                  nb0 + static_cast<int>(crank) * CF::R0, pol);
                                             tma_load_omega<PAIR>(d2 + CF::R0 * 128, &mapB1, &ch_ready[cs], kc,
@@ -697,6 +738,7 @@ shgemm_sm100_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_const
                             }
                         }
                         advance(cs, pc, NCH);
+                        ++chunk_ctr;
                     }
                 }
                 if (p.prof) p.prof[blockIdx.x * kProfSlots + kProfProdBEmpty] = w;
@@ -708,7 +750,7 @@ shgemm_sm100_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_const
             const bool skip_mma = (p.dbg & 4u) != 0;
             for (int tile = cta_of_tile; tile < num_tiles; tile += tile_stride) {
                 int m_blk, s, n_blk, kb0, kb1;
-                tile_coords(tile, p, m_blk, s, n_blk);
+                coords(tile, m_blk, s, n_blk);
                 kb_range(s, p, kb0, kb1);
                 for (int kb = kb0; kb < kb1; kb += KC) {
                     const int nst = (kb1 - kb) < KC ? (kb1 - kb) : KC;   // stages in this chunk
@@ -764,11 +806,11 @@ shgemm_sm100_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_const
                                             else mma_ts<PAIR, TF32>(d, a, bb, idesc, 1u);
                                         }
                             }
-                            commit_to<PAIR>(&acc_full[slot]);
+                            commit_to<PAIR>(&acc_full[slot], pair_mask);
                         }
                         __syncwarp();
                     }
-                    if (elect_one()) commit_to<PAIR>(&ch_empty[cs]);
+                    if (elect_one()) commit_to<PAIR>(&ch_empty[cs], NP > 1 ? cl_mask : pair_mask);
                     __syncwarp();
                     advance(cs, pc, NCH);
                 }

@@ -355,3 +355,33 @@ def test_a_box_layouts(shg, orc, m, k, n, tune):
     check_bars(orc, A, om, Y)
     with pytest.raises(shg.SHGError):
         shg.shgemm(cuda(synth.gaussian(64, 100, seed=1)), shg.gen_omega(100, 16), tune={"a_box": 2})
+
+
+@pytest.mark.parametrize("m,k,n,mmajor", [(2048, 1000, 256, False), (4096, 640, 144, False), (1024, 3000, 200, True),
+                                          (2048, 512, 130, False)])
+@pytest.mark.parametrize("mc", [2, 4])
+def test_omega_multicast_bitwise_identical(shg, orc, m, k, n, mmajor, mc):
+    """Omega stages multicast to 2 / 4 CTA pairs of a cluster change only who loads Omega, not the
+    arithmetic: Y is bitwise identical to the unicast pair kernel (and meets the bars)."""
+    rng = np.random.default_rng(m + n + mc)
+    A = rng.standard_normal((m, k)).astype(np.float32)
+    Om = shg.gen_omega(k, n, seed=3)
+    if mmajor:
+        At = cuda(np.ascontiguousarray(A.T))
+        y1 = shg.shgemm_at(At, Om, tune={"omega_mcast": 1, "pair": 1})
+        ym = shg.shgemm_at(At, Om, tune={"omega_mcast": mc, "pair": 1})
+    else:
+        Ad = cuda(A)
+        y1 = shg.shgemm(Ad, Om, tune={"omega_mcast": 1, "pair": 1})
+        ym = shg.shgemm(Ad, Om, tune={"omega_mcast": mc, "pair": 1})
+    torch.cuda.synchronize()
+    assert shg.plan(m, n, k, {"omega_mcast": mc, "pair": 1})["omega_mcast"] == mc
+    assert torch.equal(y1, ym)
+    check_bars(orc, A, omega_bits(Om), to_np(ym))
+
+
+def test_omega_multicast_rejects_ragged_pair_tiles(shg):
+    with pytest.raises(shg.SHGError):
+        shg.plan(3 * 256, 256, 512, {"omega_mcast": 2})     # 3 pair tiles: not a multiple of 2
+    with pytest.raises(shg.SHGError):
+        shg.plan(4096, 64, 512, {"omega_mcast": 2})         # BN = 64: single CTAs, no pairs

@@ -15,6 +15,8 @@ def run(shape, variants, rounds=5, reps=5):
         t = dict(tune or {}); t['prof'] = prof.data_ptr()
         shg.shgemm(A, Om, out=Y, tune=t); torch.cuda.synchronize()
         cyc[name] = float(prof[:, 0].max() / prof[:, 11].max().clamp(min=1))
+        cyc[name + '_ctas'] = int((prof[:, 0] > 0).sum())
+        cyc[name + '_cycles'] = float(prof[:, 0].max())
     for _ in range(rounds):
         for name, tune in variants:
             for _ in range(2): shg.shgemm(A, Om, out=Y, tune=tune)
@@ -27,7 +29,8 @@ def run(shape, variants, rounds=5, reps=5):
     for name, _ in variants:
         ms = statistics.median(res[name])
         out.append(dict(shape=shape, variant=name, ms=ms, gbs=(4.0*m*k+2.0*k*n+4.0*m*n)/ms/1e6, tflops=2.0*m*n*k/ms/1e9,
-                        cyc_per_stage=cyc[name], spread=(max(res[name]) - min(res[name])) / ms))
+                        cyc_per_stage=cyc[name], spread=(max(res[name]) - min(res[name])) / ms,
+                        ctas=cyc[name + '_ctas'], ghz_eff=cyc[name + '_cycles'] / ms / 1e6))
         print(json.dumps(out[-1]), flush=True)
     del A, Y; torch.cuda.empty_cache()
     return out
