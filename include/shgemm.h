@@ -220,6 +220,18 @@ shg_status_t project_ex(const float *A, int ndim, const int64_t *dims, int mode,
 
 size_t shg_project_workspace_size_ex(int ndim, const int64_t *dims, int mode, int64_t n, int tc);
 
+/* project_ex for a SLAB of a larger tensor (K-sharded RP-HOSVD): A is
+ * this rank's C-order piece with dims `dims`, and its mode-`mode` unfolding's K_local columns are
+ * columns [omega_row0, omega_row0 + K_local) of the full tensor's unfolding, so W is multiplied with
+ * rows [omega_row0, omega_row0 + K_local) of the full Omega_(mode) = gen_omega_f16_ex(k_total, n,
+ * seed, dist, stream_id = mode). Summing W over the slabs (one all-reduce) gives the full W.
+ * k_total = 0 means omega_row0 + K_local (matters only for SHG_DIST_VERYSPARSE). Workspace as
+ * project_ex (shg_project_workspace_size_ex of the LOCAL dims). omega_row0 < 0 or
+ * k_total < omega_row0 + K_local: SHG_ERR_INVALID_VALUE. */
+shg_status_t project_shard(const float *A, int ndim, const int64_t *dims, int mode, int64_t n, uint64_t seed,
+                           int dist, int tc, int64_t omega_row0, int64_t k_total, float *W, int64_t ldw,
+                           void *workspace, size_t workspace_bytes, shg_stream_t stream);
+
 /* ---------------------------------------------------------------------------------------------
  * shgemm_host — Y = A . Omega with A and Y in HOST memory (pinned for overlap; pageable works but
  * serialises), Omega on the device. A is streamed to the device in row chunks of `chunk_rows`

@@ -674,10 +674,12 @@ size_t shg_project_workspace_size(int ndim, const int64_t* dims, int mode, int64
     return shg_project_workspace_size_ex(ndim, dims, mode, n, SHG_TC_FP16);
 }
 
-shg_status_t project_ex(const float* A, int ndim, const int64_t* dims, int mode, int64_t n, uint64_t seed, int dist,
-                        int tc, float* W, int64_t ldw, void* workspace, size_t workspace_bytes, shg_stream_t stream) {
+shg_status_t project_shard(const float* A, int ndim, const int64_t* dims, int mode, int64_t n, uint64_t seed,
+                           int dist, int tc, int64_t omega_row0, int64_t k_total, float* W, int64_t ldw,
+                           void* workspace, size_t workspace_bytes, shg_stream_t stream) {
     if (!A || !dims || !W || ndim < 1 || ndim > 8 || mode < 0 || mode >= ndim || n < 0 || ldw < n)
         return SHG_ERR_INVALID_VALUE;
+    if (omega_row0 < 0) return SHG_ERR_INVALID_VALUE;
     if (dist < 0 || dist > 3 || (tc != SHG_TC_FP16 && tc != SHG_TC_TF32)) return SHG_ERR_INVALID_VALUE;
     for (int i = 0; i < ndim; ++i) if (dims[i] < 1) return SHG_ERR_INVALID_VALUE;
     if (n == 0) return SHG_OK;
@@ -708,7 +710,10 @@ shg_status_t project_ex(const float* A, int ndim, const int64_t* dims, int mode,
         }
         return st;
     };
-    shg_status_t st = gen_omega_f16_ex(K, n, seed, dist, static_cast<uint32_t>(mode), 0, K, Om, ldo, stream);
+    if (k_total < 1) k_total = omega_row0 + K;
+    if (k_total < omega_row0 + K) return finish(SHG_ERR_INVALID_VALUE);
+    shg_status_t st = gen_omega_f16_ex(K, n, seed, dist, static_cast<uint32_t>(mode), omega_row0, k_total, Om, ldo,
+                                       stream);
     if (st != SHG_OK) return finish(st);
     AView av{A, K, 1, K, K * M};
     if (mode == 0) {
@@ -738,6 +743,11 @@ shg_status_t project_ex(const float* A, int ndim, const int64_t* dims, int mode,
     tt.tc = tc;
     st = run_shgemm(M, n, K, av, Om, ldo, W, ldw, &tt, sk_bytes ? sk : nullptr, sk_bytes, nullptr, s);
     return finish(st);
+}
+
+shg_status_t project_ex(const float* A, int ndim, const int64_t* dims, int mode, int64_t n, uint64_t seed, int dist,
+                        int tc, float* W, int64_t ldw, void* workspace, size_t workspace_bytes, shg_stream_t stream) {
+    return project_shard(A, ndim, dims, mode, n, seed, dist, tc, 0, 0, W, ldw, workspace, workspace_bytes, stream);
 }
 
 shg_status_t project(const float* A, int ndim, const int64_t* dims, int mode, int64_t n, uint64_t seed, int dist,
