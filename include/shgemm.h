@@ -308,6 +308,12 @@ shg_status_t shg_probe_mma_rate(int n, int iters, int ts, int lsu_warps, float *
  * cycles per pair-MMA instruction (256 x n x 16 MACs on two SMs). */
 shg_status_t shg_probe_mma2_rate(int n, int iters, int ts, float *out, int clusters, shg_stream_t stream);
 
+/* MMA energy probe: `clusters` CTA pairs each issue `iters` K steps of
+ * cta_group::2 kind::f16 MMAs (M = 256, A from TMEM, B from smem, random FP16 data), each K step
+ * split into `parts` (1 or 2) MMAs of N = n / parts; out[cluster] (device int64) = clock64 cycles
+ * of the issuing loop. Timed with events under the power cap it measures tensor work per joule. */
+shg_status_t shg_probe_mma_energy(int n, int parts, int iters, long long *out, int clusters, shg_stream_t stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -5,6 +5,7 @@
 // chosen FP32 accumulator preload, so RN-vs-RZ, alignment width and the scale-input-d semantics the
 // mainloop relies on can be measured instead of assumed.
 #include <cstdint>
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 #include "ptx.cuh"
 #include "../../include/shgemm.h"
@@ -262,4 +263,120 @@ extern "C" shg_status_t shg_probe_mma2_rate(int n, int iters, int ts, float* out
     if (e != cudaSuccess) return SHG_ERR_CUDA;
     shg::probe_mma2_rate_kernel<<<2 * clusters, 128, smem, reinterpret_cast<cudaStream_t>(stream)>>>(n, iters, ts, out);
     return cudaGetLastError() == cudaSuccess ? SHG_OK : SHG_ERR_CUDA;
+}
+
+// ------------------------------------------------------------------ MMA energy probe (diagnostics)
+// Same tensor work split into `parts` MMAs per K step (N = n / parts each) on random FP16 data
+// (A from TMEM, B from smem, both filled with hashed values in [-1, 1)), so that a long run under
+// the power cap shows whether the N-split of the mainloop (two parts of N = 128 for BN = 256) costs
+// energy: out[cluster] = clock64 cycles of the issuing loop.
+namespace shg {
+__device__ __forceinline__ uint32_t probe_hash(uint32_t x) {
+    x ^= x >> 16; x *= 0x7feb352dU; x ^= x >> 15; x *= 0x846ca68bU; x ^= x >> 16;
+    return x;
+}
+__device__ __forceinline__ uint32_t rand_h2(uint32_t x) {
+    const uint32_t h = probe_hash(x);
+    const __half2 v = __floats2half2_rn(static_cast<float>(h & 0xFFFF) * (2.0f / 65536.0f) - 1.0f,
+                                        static_cast<float>(h >> 16) * (2.0f / 65536.0f) - 1.0f);
+    return *reinterpret_cast<const uint32_t*>(&v);
+}
+
+__global__ void __launch_bounds__(128, 1) probe_mma_energy_kernel(int n, int parts, int iters, long long* out) {
+    extern __shared__ uint8_t smem_raw[];
+    const uint32_t raw_addr = smem_u32(smem_raw);
+    uint8_t* base = smem_raw + ((1024u - (raw_addr & 1023u)) & 1023u);
+    uint8_t* sB = base;                                   // 128 rows x 128 B (n/2 rows used)
+    uint64_t* bar = reinterpret_cast<uint64_t*>(base + 16384);
+    uint32_t* tslot = reinterpret_cast<uint32_t*>(bar + 1);
+    uint32_t rank;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(rank));
+    const uint32_t warp = warp_id();
+    for (int i = threadIdx.x; i < 16384 / 4; i += blockDim.x)
+        reinterpret_cast<uint32_t*>(sB)[i] = rand_h2(static_cast<uint32_t>(i) * 2654435761u + rank);
+    fence_proxy_async_smem();
+    if (threadIdx.x == 0) { mbar_init(bar, 1); fence_mbar_init(); }
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tslot)) : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+    }
+    tc_fence_before();
+    asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+    tc_fence_after();
+    const uint32_t tbase = *tslot;
+    {   // A operand: TMEM columns 256..511 of this warp's lane quarter, random FP16 pairs
+        const uint32_t lane_addr = (32u * (warp & 3u)) << 16;
+        for (int c = 0; c < 256; c += 16) {
+            uint32_t r[16];
+#pragma unroll
+            for (int i = 0; i < 16; ++i) r[i] = rand_h2((threadIdx.x * 977u + c + i) * 40503u + rank * 7u);
+            asm volatile(
+                "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], "
+                "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};"
+                ::"r"(tbase + lane_addr + 256 + c), "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]),
+                  "r"(r[6]), "r"(r[7]), "r"(r[8]), "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]),
+                  "r"(r[14]), "r"(r[15]) : "memory");
+        }
+        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+    }
+    tc_fence_before();
+    asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+    tc_fence_after();
+    if (rank == 0 && warp == 0) {
+        if (elect_one()) {
+            const int w = n / parts;
+            const uint32_t idesc = idesc_f16_f32(256, static_cast<uint32_t>(w));
+            const uint64_t bd = sw128_kmajor_desc(smem_u32(sB));
+            const long long t0 = clock64();
+            for (int i = 0; i < iters; ++i) {
+                const uint32_t j = static_cast<uint32_t>(i & 3);
+                const uint32_t a = tbase + 256 + 8 * j + ((i & 4) ? 32u : 0u) + ((i & 8) ? 64u : 0u);
+                for (int q = 0; q < parts; ++q) {
+                    const uint64_t b = bd + static_cast<uint64_t>((q * (w / 2) * 128) >> 4) + 2 * j;
+                    asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, 1, 0;\n\t"
+                                 "tcgen05.mma.cta_group::2.kind::f16 [%0], [%1], %2, %3, p;\n\t}\n"
+                                 ::"r"(tbase + q * w), "r"(a), "l"(b), "r"(idesc) : "memory");
+                }
+            }
+            asm volatile("tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;"
+                         ::"r"(smem_u32(bar)), "h"(static_cast<uint16_t>(3)) : "memory");
+            mbar_wait(bar, 0);
+            uint32_t cid;
+            asm volatile("mov.u32 %0, %%clusterid.x;" : "=r"(cid));
+            out[cid] = clock64() - t0;
+        }
+        __syncwarp();
+    } else if (rank == 1 && threadIdx.x == 0) {
+        mbar_wait(bar, 0);
+    }
+    tc_fence_before();
+    asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+    if (warp == 0) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;" ::"r"(tbase) : "memory");
+    }
+}
+}  // namespace shg
+
+extern "C" shg_status_t shg_probe_mma_energy(int n, int parts, int iters, long long* out, int clusters,
+                                             shg_stream_t stream) {
+    if (!out || parts < 1 || parts > 2 || n % (32 * parts) || n < 32 || n > 256 || iters < 1 || clusters < 1)
+        return SHG_ERR_INVALID_VALUE;
+    const int smem = 1024 + 16384 + 64;
+    cudaError_t e = cudaFuncSetAttribute(shg::probe_mma_energy_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return SHG_ERR_CUDA;
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(2 * clusters);
+    cfg.blockDim = dim3(128);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = reinterpret_cast<cudaStream_t>(stream);
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    e = cudaLaunchKernelEx(&cfg, shg::probe_mma_energy_kernel, n, parts, iters, out);
+    return e == cudaSuccess ? SHG_OK : SHG_ERR_CUDA;
 }
