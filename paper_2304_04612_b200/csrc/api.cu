@@ -143,6 +143,8 @@ template <int B> using CfgSingleT = shg::Cfg<B, false, true>;
 template <int B> using CfgPairC = shg::Cfg<B, true, false, true>;
 template <int B> using CfgSingleC = shg::Cfg<B < 128 ? B : 128, false, false, true>;
 #define SHG_CFG_FIELD(bn, pair, tf32, FIELD)                                                              \
+    if (!tf32 && bn == 272) return pair ? shg::Cfg<272, true>::FIELD : shg::Cfg<272, false>::FIELD;      \
+    if (!tf32 && bn == 288) return pair ? shg::Cfg<288, true>::FIELD : shg::Cfg<288, false>::FIELD;      \
     if (tf32 && pair) { SHG_BN_SWITCH(bn, return CfgPairT<BN_>::FIELD) }                                  \
     if (tf32) { SHG_BN_SWITCH(bn, return CfgSingleT<BN_>::FIELD) }                                        \
     if (pair) { SHG_BN_SWITCH(bn, return CfgPair<BN_>::FIELD) }                                           \
@@ -155,6 +157,8 @@ int r0_for(int bn, bool pair, bool tf32) { SHG_CFG_FIELD(bn, pair, tf32, R0) }
 int r1_for(int bn, bool pair, bool tf32) { SHG_CFG_FIELD(bn, pair, tf32, R1) }
 // TCEC-SGEMM configurations (pairs: BN >= 128; single CTAs: BN <= 128)
 #define SHG_CFG_FIELD_TCEC(bn, pair, FIELD)                                                              \
+    if (pair && bn == 272) return shg::Cfg<272, true, false, true>::FIELD;                                \
+    if (pair && bn == 288) return shg::Cfg<288, true, false, true>::FIELD;                                \
     if (pair) { SHG_BN_SWITCH(bn, return CfgPairC<(BN_ < 128 ? 128 : BN_)>::FIELD) }                      \
     SHG_BN_SWITCH(bn, return CfgSingleC<BN_>::FIELD)
 int smem_for_tcec(int bn, bool pair) { SHG_CFG_FIELD_TCEC(bn, pair, kSmemBytes) }
@@ -202,16 +206,21 @@ Plan make_plan(int64_t m, int64_t n, int64_t k, bool fast_ok, const shg_tune_t* 
     // CTA pair: halves Omega's L2->SMEM traffic per SM (the power-cap lever at BN >= 128); needs > 128 rows
     const int pair_mode = tune ? tune->pair : 0;   // 0 auto, 1 force on, 2 force off
     const bool want_pair = (pair_mode == 0 && m > shg::kBM) || pair_mode == 1;
-    // TCEC stages two B tiles: single CTAs stop at BN = 128
+    // TCEC stages two B tiles: single CTAs stop at BN = 128; wide tiles (BN 272 / 288) are FP16-only
     const int max_bn = (tcec && !want_pair) ? kTcecMaxBnSingle : 256;
     if (tune && tune->bn > 0 && valid_bn(tune->bn)) {
         pl.bn = tune->bn;
-        if (pl.bn > max_bn) { pl.path = -1; return pl; }
+        if (pl.bn > max_bn && !(wide_bn(pl.bn) && !pl.tf32 && (!tcec || want_pair))) { pl.path = -1; return pl; }
         pl.n_tiles = static_cast<int>((n + pl.bn - 1) / pl.bn);
     } else {
         pl.n_tiles = static_cast<int>((n + max_bn - 1) / max_bn);
+        // SHGEMM-FP16, 256 < n <= 288: ONE wide tile (BN 272 / 288) instead of two of <= 144, so A
+        // streams once: 0.29 vs 0.35 ms at cfg2, 11.1 vs 16.0 ms at m = 2^21 (profiles/r01_ab_wide.jsonl).
+        // Not for n > 288: two wide tiles of 272 measured slower than three of 192 at n = 544.
+        // TCEC-SGEMM likewise when it runs as CTA pairs (RSVD line 3: n = p + s = 272).
+        if (!pl.tf32 && (!tcec || want_pair) && n > 256 && n <= 288) pl.n_tiles = 1;
         const int64_t need = (n + pl.n_tiles - 1) / pl.n_tiles;
-        pl.bn = max_bn;
+        pl.bn = 288;
         for (int b : kBNs) if (b >= need) { pl.bn = b; break; }
     }
     pl.pair = pair_ok(pl.bn) && want_pair;
@@ -221,9 +230,9 @@ Plan make_plan(int64_t m, int64_t n, int64_t k, bool fast_ok, const shg_tune_t* 
     const int slots = pl.pair ? std::max(1, sms / 2) : sms;     // concurrent tiles
     pl.m_tiles = static_cast<int>((m + tile_m - 1) / tile_m);
     if (mc >= 2) {
-        if (!pl.pair || pl.tf32 || pl.tcec || pl.m_tiles % mc) { pl.path = -1; return pl; }
+        if (!pl.pair || pl.tf32 || pl.tcec || wide_bn(pl.bn) || pl.m_tiles % mc) { pl.path = -1; return pl; }
         pl.np = mc;
-    } else if (mc == 0 && pl.pair && !pl.tf32 && !pl.tcec && kAutoMcast > 1 && pl.m_tiles % kAutoMcast == 0 &&
+    } else if (mc == 0 && pl.pair && !pl.tf32 && !pl.tcec && !wide_bn(pl.bn) && kAutoMcast > 1 && pl.m_tiles % kAutoMcast == 0 &&
                pl.m_tiles >= kAutoMcast * 8) {
         pl.np = kAutoMcast;
     }
@@ -375,7 +384,8 @@ shg_status_t run_shgemm(int64_t m, int64_t n, int64_t k, const AView& av, const 
     };
     // Omega operand: FP16 as given (SHGEMM-FP16), or its exact TF32 widening (SHGEMM-TF32),
     // or TCEC-SGEMM's [B_low | dB_low] split of an FP32 B (Eqs 5-9)
-    const int rows0 = pl.pair ? (tcec ? r0_for_tcec(pl.bn, true) : r0_for(pl.bn, true, pl.tf32)) : pl.bn;
+    const int rows0 = pl.pair ? (tcec ? r0_for_tcec(pl.bn, true) : r0_for(pl.bn, true, pl.tf32))
+                              : (wide_bn(pl.bn) ? r0_for(pl.bn, false, false) : pl.bn);
     const int r1 = tcec ? r1_for_tcec(pl.bn, pl.pair) : r1_for(pl.bn, pl.pair, pl.tf32);
     const int rows1 = r1 > 0 ? r1 : rows0;         // one N part (R1 == 0): mapB1 unused
     bool encb_ok;

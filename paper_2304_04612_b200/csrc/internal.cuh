@@ -25,7 +25,9 @@ shg_status_t cuda_fail(cudaError_t e, const char* what);
         if (e_ != cudaSuccess) return shg_api::cuda_fail(e_, #call); \
     } while (0)
 
-constexpr int kBNs[] = {32, 64, 96, 128, 144, 160, 192, 224, 256};
+constexpr int kBNs[] = {32, 64, 96, 128, 144, 160, 192, 224, 256, 272, 288};
+// wide tiles (one N tile for 256 < n <= 288): SHGEMM-FP16 only
+constexpr bool wide_bn(int bn) { return bn > 256; }
 
 #define SHG_BN_SWITCH(bn, EXPR)                                  \
     switch (bn) {                                                \
@@ -112,9 +114,18 @@ shg_status_t dispatch_bn(int bn, const CUtensorMap& a, const CUtensorMap& b0, co
             case 192: return launch_tc<192, MMAJOR, true, TF32>(a, b0, b1, kp, grid, s);
             case 224: return launch_tc<224, MMAJOR, true, TF32>(a, b0, b1, kp, grid, s);
             case 256: return launch_tc<256, MMAJOR, true, TF32>(a, b0, b1, kp, grid, s);
+            case 272: if constexpr (!TF32) return launch_tc<272, MMAJOR, true, false>(a, b0, b1, kp, grid, s);
+                      return SHG_ERR_INVALID_VALUE;
+            case 288: if constexpr (!TF32) return launch_tc<288, MMAJOR, true, false>(a, b0, b1, kp, grid, s);
+                      return SHG_ERR_INVALID_VALUE;
             default: return SHG_ERR_INVALID_VALUE;
         }
     } else {
+        if constexpr (!TF32) {
+            if (bn == 272) return launch_tc<272, MMAJOR, false, false>(a, b0, b1, kp, grid, s);
+            if (bn == 288) return launch_tc<288, MMAJOR, false, false>(a, b0, b1, kp, grid, s);
+        }
+        if (wide_bn(bn)) return SHG_ERR_INVALID_VALUE;
         SHG_BN_SWITCH(bn, return (launch_tc<BN_, MMAJOR, false, TF32>(a, b0, b1, kp, grid, s)))
     }
 }

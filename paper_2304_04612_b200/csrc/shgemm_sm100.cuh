@@ -151,14 +151,18 @@ struct Cfg {
     // 64 columns each) + accumulator slots. TF32: a stage's hi/lo take 128 columns, so K_c = 64 =
     // one stage and 2 chunk slots. N is covered by 2 part-MMAs of widths W + WLAST = BN so that the
     // drain of one part overlaps the MMAs of the other.
-    static constexpr int KC = TF32 ? 1 : 2;                // stages per promotion chunk
+    // WIDE (SHGEMM-FP16, 256 < BN <= 288): one N tile covers n = 257..288 (e.g. RSVD's p + s = 272)
+    // so A streams once; two accumulator parts of up to 144 columns leave 192 TMEM columns for A,
+    // hence K_c = 64 (one stage per chunk) and 3 chunk slots.
+    static constexpr bool WIDE = BN > 256;
+    static constexpr int KC = (TF32 || WIDE) ? 1 : 2;      // stages per promotion chunk
     static constexpr int AST = TF32 ? 128 : 64;            // TMEM columns per A stage (hi, then lo)
     static constexpr int EB = TF32 ? 4 : 2;                // Omega bytes per element in smem
     static constexpr int KSTEP = TF32 ? 8 : 16;            // UMMA K per instruction
     static constexpr int NMMA = kBK / KSTEP;               // MMAs per stage per operand (hi or lo)
     // chunk slots (TMEM A + Omega smem); TF32 with BN <= 64 has the TMEM for a third (the ring is
     // only one stage deep per slot there, and the splitter must not wait on the MMAs every stage)
-    static constexpr int NCH = (TF32 && BN <= 64) ? 3 : 2;
+    static constexpr int NCH = ((TF32 && BN <= 64) || WIDE) ? 3 : 2;
     // N parts: 2 (drain of one overlaps the MMAs of the other), or 1 for TF32 with BN <= 64, whose
     // MMA thread is issue-bound (8 K steps a stage: half the instructions with one part of N = BN)
     static constexpr int NQ = (TF32 && BN <= 64) ? 1 : 2;
@@ -181,8 +185,8 @@ struct Cfg {
     static constexpr int SA_fit = (kSmemLimit - 1024 - kBarBytes - SO * kOmStageBytes) / kA32StageBytes;
     static constexpr int SA = SA_fit > 6 ? 6 : SA_fit;
     static constexpr int kSmemBytes = 1024 + SA * kA32StageBytes + SO * kOmStageBytes + kBarBytes;
-    static_assert(BN % 16 == 0 && BN >= 32 && BN <= 256, "BN");
-    static_assert(WLAST >= 16 && WLAST % 16 == 0 && (W <= 128 || NQ == 1), "UMMA N parts");
+    static_assert(BN % 16 == 0 && BN >= 32 && BN <= (TF32 ? 256 : 288) && (!TCEC || !WIDE || PAIR), "BN");
+    static_assert(WLAST >= 16 && WLAST % 16 == 0 && (W <= 128 || NQ == 1 || (WIDE && W <= 144)), "UMMA N parts");
     static_assert(!PAIR || (R0 % 8 == 0 && R1 % 8 == 0), "pair halves must be whole 8-row core groups");
     static_assert(NSLOT >= NQ, "TMEM accumulator slots");
     static_assert(SA >= 2 && kSmemBytes <= kSmemLimit, "smem");
@@ -578,16 +582,18 @@ shgemm_sm100_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_const
                     tc_fence_after();
                     const uint32_t taddr = tmem_base + lane_addr + slot * W;
                     if (!skip_ld) {
+                        // 16 columns per wait (two tcgen05.ld in flight)
+                        constexpr int LDU = 2;
 #pragma unroll
-                        for (int c = 0; c < W; c += 16) {
+                        for (int c = 0; c < W; c += 8 * LDU) {
                             if (c < width) {
-                                float v[2][8];
+                                float v[LDU][8];
 #pragma unroll
-                                for (int u = 0; u < 2; ++u)
+                                for (int u = 0; u < LDU; ++u)
                                     if (c + 8 * u < width) tmem_ld8(taddr + c + 8 * u, v[u]);
                                 tmem_ld_wait();
 #pragma unroll
-                                for (int u = 0; u < 2; ++u)
+                                for (int u = 0; u < LDU; ++u)
 #pragma unroll
                                     for (int i = 0; i < 8; i += 2)
                                         if (c + 8 * u < width)
@@ -730,6 +736,9 @@ shgemm_sm100_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_const
                                                                  nb0 + static_cast<int>(crank) * CF::R0, pol);
                                             tma_load_omega<PAIR>(d2 + CF::R0 * 128, &mapB1, &ch_ready[cs], kc,
                                                                  nb0 + W + static_cast<int>(crank) * CF::R1, pol);
+                                        } else if constexpr (CF::WIDE) {   // > 256 rows: one box per part
+                                            tma_load_omega<PAIR>(d2, &mapB0, &ch_ready[cs], kc, nb0, pol);
+                                            tma_load_omega<PAIR>(d2 + CF::R0 * 128, &mapB1, &ch_ready[cs], kc, nb0 + W, pol);
                                         } else {   // the two parts are contiguous rows: one box of BN rows (mapB0)
                                             tma_load_omega<PAIR>(d2, &mapB0, &ch_ready[cs], kc, nb0, pol);
                                         }

@@ -28,6 +28,8 @@ shg_status_t dispatch_pair(int bn, const CUtensorMap& a, const CUtensorMap& b0, 
         case 192: return launch_tc<192, MMAJOR, true, false, true>(a, b0, b1, kp, grid, s);
         case 224: return launch_tc<224, MMAJOR, true, false, true>(a, b0, b1, kp, grid, s);
         case 256: return launch_tc<256, MMAJOR, true, false, true>(a, b0, b1, kp, grid, s);
+        case 272: return launch_tc<272, MMAJOR, true, false, true>(a, b0, b1, kp, grid, s);
+        case 288: return launch_tc<288, MMAJOR, true, false, true>(a, b0, b1, kp, grid, s);
         default: return SHG_ERR_INVALID_VALUE;
     }
 }

@@ -385,3 +385,29 @@ def test_omega_multicast_rejects_ragged_pair_tiles(shg):
         shg.plan(3 * 256, 256, 512, {"omega_mcast": 2})     # 3 pair tiles: not a multiple of 2
     with pytest.raises(shg.SHGError):
         shg.plan(4096, 64, 512, {"omega_mcast": 2})         # BN = 64: single CTAs, no pairs
+
+
+@pytest.mark.parametrize("m,k,n,tune", [(1000, 1500, 272, None), (600, 777, 288, None), (130, 640, 270, None),
+                                        (700, 512, 560, {"bn": 288}), (512, 2048, 272, {"pair": 2}),
+                                        (1024, 1024, 300, {"bn": 288})])
+@pytest.mark.parametrize("mmajor", [False, True])
+def test_wide_tiles(shg, orc, m, k, n, tune, mmajor):
+    """256 < BN <= 288 (one N tile for n = 257..288, K_c = 64, 3 chunk slots): the bars, K- and
+    M-major A, single CTAs and pairs, ragged n inside the wide tile, two wide tiles."""
+    rng = np.random.default_rng(m + k + n)
+    A = rng.standard_normal((m, k)).astype(np.float32)
+    Om = shg.gen_omega(k, n, seed=2)
+    plan = shg.plan(m, n, k, tune)
+    assert plan["bn"] in (272, 288) and plan["path"] == 0, plan
+    if mmajor:
+        Y = shg.shgemm_at(cuda(np.ascontiguousarray(A.T)), Om, tune=tune)
+    else:
+        Y = shg.shgemm(cuda(A), Om, tune=tune)
+    torch.cuda.synchronize()
+    check_bars(orc, A, omega_bits(Om), to_np(Y))
+
+
+def test_wide_tiles_rejected_for_tf32(shg):
+    with pytest.raises(shg.SHGError):
+        shg.plan(1000, 272, 512, {"bn": 272}, tc="tf32")
+    assert shg.plan(1000, 272, 512, tc="tf32")["bn"] <= 256

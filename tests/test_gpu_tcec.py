@@ -127,7 +127,7 @@ def test_tunables(shg, orc, tune):
 
 def test_plans(shg):
     p = shg.tcec_plan(16384, 272, 16384)
-    assert p["path"] == 0 and p["tc"] == 2 and p["cta_pair"] == 1 and p["bn"] <= 256
+    assert p["path"] == 0 and p["tc"] == 2 and p["cta_pair"] == 1 and p["bn"] == 272 and p["n_tiles"] == 1
     p1 = shg.tcec_plan(100, 200, 512)          # one row block: single CTAs, BN capped at 128
     assert p1["cta_pair"] == 0 and p1["bn"] <= 128
     with pytest.raises(shg.SHGError):
