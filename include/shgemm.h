@@ -196,8 +196,26 @@ shg_status_t gen_omega_f16_ex(int64_t k, int64_t n, uint64_t seed, int dist, uin
                               int64_t row0, int64_t k_total, uint16_t *Omega, int64_t ldo,
                               shg_stream_t stream);
 
+/* gen_omega_f16_ex into the K-TILED layout that project() streams: rows i of Omega are grouped in
+ * tiles of 64 (t = i / 64), each tile stored as n contiguous 128-byte rows (one per column j):
+ * element (i, j) at Omega[(i / 64) * n * 64 + j * 64 + i % 64]. Omega holds ceil(k/64) * n * 64
+ * halves; rows k .. 64*ceil(k/64)-1 of the last tile are written as +0. The same values as
+ * gen_omega_f16_ex(k, n, seed, dist, stream_id, row0, k_total). Why: a column-major 64-k TMA box
+ * visits n rows 2*ldo bytes apart (2 MiB for an RP-HOSVD unfolding, k = 2^20); a tiled box is one
+ * contiguous run of n x 128 bytes. */
+shg_status_t gen_omega_f16_tiled(int64_t k, int64_t n, uint64_t seed, int dist, uint32_t stream_id, int64_t row0,
+                                 int64_t k_total, uint16_t *Omega, shg_stream_t stream);
+
+/* shgemm_ex (SHGEMM-FP16 only: tune->tc must be SHG_TC_FP16) reading a k-tiled Omega written by
+ * gen_omega_f16_tiled(k, n, ...). Needs the tcgen05 fast path (A 16-B aligned, lda % 4 == 0);
+ * otherwise SHG_ERR_INVALID_VALUE (the CUDA-core fallback reads column-major Omega only). */
+shg_status_t shgemm_tiled(int64_t m, int64_t n, int64_t k, const float *A, int64_t lda, const uint16_t *Omega_tiled,
+                          float *Y, int64_t ldc, const shg_tune_t *tune, void *workspace, size_t workspace_bytes,
+                          int *nonfinite_flag, shg_stream_t stream);
+
 /* ---------------------------------------------------------------------------------------------
- * project — W[I_mode x n] = A'_(mode) . Omega_(mode) (Alg 2 line 2).
+ * project — W[I_mode x n] = A'_(mode) . Omega_(mode) (Alg 2 line 2). With SHGEMM-FP16 and
+ * an aligned A view, Omega_(mode) is generated in the k-tiled layout (gen_omega_f16_tiled).
  *   A        device, C-order tensor with ndim dims (1 <= ndim <= 8), dims[i] >= 1.
  *   mode     0 <= mode < ndim. The unfolding's column index is the C-order linear index over the
  *            remaining modes in ascending order (== torch.movedim(A, mode, 0).reshape(I_mode, -1)).

@@ -78,6 +78,8 @@ def lib():
             L.project_ex.argtypes = [vp, i32, vp, i32, i64, u64, i32, i32, vp, i64, vp, sz, vp]
             L.shg_project_workspace_size_ex.argtypes = [i32, vp, i32, i64, i32]
             L.project_shard.argtypes = [vp, i32, vp, i32, i64, u64, i32, i32, i64, i64, vp, i64, vp, sz, vp]
+            L.gen_omega_f16_tiled.argtypes = [i64, i64, u64, i32, u32, i64, i64, vp, vp]
+            L.shgemm_tiled.argtypes = [i64, i64, i64, vp, i64, vp, vp, i64, ctypes.POINTER(Tune), vp, sz, vp, vp]
             L.shg_project_workspace_size_ex.restype = sz
             L.shg_debug_split_tf32.argtypes = [vp, i64, vp, vp, vp]
             L.shg_probe_tma_read.argtypes = [vp, i64, i64, i64, i32, i32, i32, i32, i32, vp, vp]
@@ -98,7 +100,8 @@ def lib():
             L.shg_probe_mma2_rate.restype = i32
             for name in ("shgemm", "shgemm_ex", "shgemm_at", "shgemm_host", "shg_plan", "gen_omega_f16", "gen_omega_f16_ex", "project",
                          "shg_debug_split", "shg_synth_f32", "shg_probe_umma", "shgemm_tf32", "project_ex",
-                         "shg_debug_split_tf32", "tcec_sgemm", "tcec_sgemm_ex", "tcec_plan", "project_shard"):
+                         "shg_debug_split_tf32", "tcec_sgemm", "tcec_sgemm_ex", "tcec_plan", "project_shard",
+                         "gen_omega_f16_tiled", "shgemm_tiled"):
                 getattr(L, name).restype = i32
             _lib = L
     return _lib
@@ -147,6 +150,33 @@ def gen_omega(k: int, n: int, seed: int = 0, dist="gaussian", stream_id: int = 0
                                   k if k_total is None else k_total, _p(buf), ldo, _stream(stream)),
            "gen_omega_f16_ex")
     return buf[:, :k].t()
+
+
+def gen_omega_tiled(k: int, n: int, seed: int = 0, dist="gaussian", stream_id: int = 0, row0: int = 0,
+                    k_total: int | None = None, device=None, stream=None) -> torch.Tensor:
+    """Omega in the k-tiled layout project() streams (include/shgemm.h gen_omega_f16_tiled): a flat
+    float16 tensor of ceil(k/64) * n * 64 elements, element (i, j) at (i//64)*n*64 + j*64 + i%64."""
+    device = torch.device("cuda") if device is None else torch.device(device)
+    buf = torch.empty(((k + 63) // 64) * n * 64, dtype=torch.float16, device=device)
+    _check(lib().gen_omega_f16_tiled(k, n, seed & (2 ** 64 - 1), _dist(dist), stream_id, row0,
+                                     k if k_total is None else k_total, _p(buf), _stream(stream)),
+           "gen_omega_f16_tiled")
+    return buf
+
+
+def shgemm_tiled(A: torch.Tensor, Omega_tiled: torch.Tensor, n: int, out=None, tune=None, workspace=None,
+                 stream=None) -> torch.Tensor:
+    """Y = A . Omega with Omega in the k-tiled layout (gen_omega_tiled(k, n, ...))."""
+    m, k = A.shape
+    if A.dtype != torch.float32 or (m and k and A.stride(1) != 1):
+        raise ValueError("A must be float32 row-major")
+    if out is None:
+        out = torch.empty((m, n), dtype=torch.float32, device=A.device)
+    ws_bytes = 0 if workspace is None else workspace.numel() * workspace.element_size()
+    _check(lib().shgemm_tiled(m, n, k, _p(A), A.stride(0) if m > 1 else max(k, 1), _p(Omega_tiled), _p(out),
+                              out.stride(0) if m > 1 else max(n, 1), _tune(tune), _p(workspace), ws_bytes, None,
+                              _stream(stream)), "shgemm_tiled")
+    return out
 
 
 # ----------------------------------------------------------------------------------------- SHGEMM

@@ -67,6 +67,7 @@ struct KParams {
     int64_t split_stride;   // elements between split planes (workspace)
     int32_t vec_store;      // out rows 16-B aligned and ldo_out % 4 == 0
     int32_t b_lo_col;       // TCEC: column (n) coordinate of dB_low in the B tensor maps (B_low at 0)
+    int32_t om_tiled;       // Omega in the k-tiled layout (3-D maps {64, n_pad, k/64}; SHGEMM-FP16 only)
     int* nonfinite;         // optional flag (set to 1 on any non-finite output)
     uint32_t dbg;           // diagnostics: bit0 skip promotion loads, bit1 skip split math, bit2 skip MMAs,
                             //              bit3 skip the Omega TMA (results are wrong when dbg != 0)
@@ -274,10 +275,26 @@ __device__ __forceinline__ void tma_load_omega_mc(void* smem_dst, const CUtensor
         : "memory");
 }
 
-// Omega tile load; in a pair the transaction bytes land on the leader's (even CTA's) barrier
+// Omega tile load; in a pair the transaction bytes land on the leader's (even CTA's) barrier.
+// tiled: Omega in the k-tiled layout (KParams::om_tiled), a 3-D map {64, n, k/64}: the box of a
+// 64-k stage is one contiguous run of rows x 128 B instead of one 128-B visit per column.
 template <bool PAIR>
 __device__ __forceinline__ void tma_load_omega(void* smem_dst, const CUtensorMap* map, uint64_t* bar, int32_t c0,
-                                               int32_t c1, uint64_t policy) {
+                                               int32_t c1, uint64_t policy, bool tiled = false) {
+    if (tiled) {
+        const int32_t t0 = c0 & 63, t2 = c0 >> 6;
+        if constexpr (PAIR) {
+            asm volatile(
+                "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+                " [%0], [%1, {%3, %4, %5}], [%2], %6;"
+                ::"r"(smem_u32(smem_dst)), "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar) & kPeerBitMask),
+                  "r"(t0), "r"(c1), "r"(t2), "l"(policy)
+                : "memory");
+        } else {
+            tma_load_3d(smem_dst, map, bar, t0, c1, t2, policy);
+        }
+        return;
+    }
     if constexpr (PAIR) {
         asm volatile(
             "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
@@ -695,6 +712,7 @@ shgemm_sm100_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_const
             // [n0 + W + crank*R1, +R1) (pair: each CTA holds its half of every part)
             if (elect_one()) {
                 const uint64_t pol = policy_evict_last();
+                const bool tiled = !TF32 && p.om_tiled != 0;
                 uint32_t cs = 0, pc = 0;
                 uint32_t chunk_ctr = 0;
                 long long w = 0;
@@ -733,14 +751,15 @@ shgemm_sm100_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_const
                                                               nb0 + W + static_cast<int>(crank) * CF::R1, half_mask, pol);
                                         } else if constexpr (PAIR) {
                                             tma_load_omega<PAIR>(d2, &mapB0, &ch_ready[cs], kc,
-                                                                 nb0 + static_cast<int>(crank) * CF::R0, pol);
+                                                                 nb0 + static_cast<int>(crank) * CF::R0, pol, tiled);
                                             tma_load_omega<PAIR>(d2 + CF::R0 * 128, &mapB1, &ch_ready[cs], kc,
-                                                                 nb0 + W + static_cast<int>(crank) * CF::R1, pol);
+                                                                 nb0 + W + static_cast<int>(crank) * CF::R1, pol, tiled);
                                         } else if constexpr (CF::WIDE) {   // > 256 rows: one box per part
-                                            tma_load_omega<PAIR>(d2, &mapB0, &ch_ready[cs], kc, nb0, pol);
-                                            tma_load_omega<PAIR>(d2 + CF::R0 * 128, &mapB1, &ch_ready[cs], kc, nb0 + W, pol);
+                                            tma_load_omega<PAIR>(d2, &mapB0, &ch_ready[cs], kc, nb0, pol, tiled);
+                                            tma_load_omega<PAIR>(d2 + CF::R0 * 128, &mapB1, &ch_ready[cs], kc, nb0 + W, pol,
+                                                                 tiled);
                                         } else {   // the two parts are contiguous rows: one box of BN rows (mapB0)
-                                            tma_load_omega<PAIR>(d2, &mapB0, &ch_ready[cs], kc, nb0, pol);
+                                            tma_load_omega<PAIR>(d2, &mapB0, &ch_ready[cs], kc, nb0, pol, tiled);
                                         }
                                     }
                                 }

@@ -411,3 +411,28 @@ def test_wide_tiles_rejected_for_tf32(shg):
     with pytest.raises(shg.SHGError):
         shg.plan(1000, 272, 512, {"bn": 272}, tc="tf32")
     assert shg.plan(1000, 272, 512, tc="tf32")["bn"] <= 256
+
+
+@pytest.mark.parametrize("k,n,row0,dist", [(1000, 64, 0, 0), (4096, 272, 8, 0), (77, 33, 4, 1), (130, 16, 0, 3)])
+def test_omega_tiled_layout_bit_exact(shg, orc, k, n, row0, dist):
+    """gen_omega_f16_tiled: element (i, j) at (i//64)*n*64 + j*64 + i%64, same bits as the oracle,
+    the last tile's rows beyond k zero."""
+    t = to_np(shg.gen_omega_tiled(k, n, seed=11, dist=dist, stream_id=3, row0=row0, k_total=k + row0)).view(np.uint16)
+    ref = orc.omega_f16(k, n, seed=11, dist=dist, stream_id=3, row0=row0, k_total=k + row0)   # (k, n)
+    kt = (k + 63) // 64
+    tiles = t.reshape(kt, n, 64)
+    full = np.zeros((kt * 64, n), dtype=np.uint16)
+    full[:k] = ref
+    np.testing.assert_array_equal(tiles.transpose(0, 2, 1).reshape(kt * 64, n), full)
+
+
+@pytest.mark.parametrize("m,k,n,tune", [(1024, 4096, 64, None), (700, 1000, 256, None), (300, 640, 272, None),
+                                        (128, 8192, 32, None), (512, 1024, 128, {"pair": 2})])
+def test_shgemm_tiled_equals_column_major(shg, m, k, n, tune):
+    """The k-tiled Omega changes only the TMA box shape: Y bitwise equal to the column-major path."""
+    g = torch.Generator(device="cuda").manual_seed(m + n)
+    A = torch.randn(m, k, device="cuda", generator=g)
+    y_cm = shg.shgemm(A, shg.gen_omega(k, n, seed=5), tune=tune)
+    y_t = shg.shgemm_tiled(A, shg.gen_omega_tiled(k, n, seed=5), n, tune=tune)
+    torch.cuda.synchronize()
+    assert torch.equal(y_cm, y_t)
