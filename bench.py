@@ -214,7 +214,7 @@ def run_pipeline(args):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="shgemm", choices=["shgemm", "reference"])
     ap.add_argument("--config", default="cfg4", choices=sorted(CONFIGS) + sorted(PIPELINES))

@@ -62,6 +62,35 @@ def _qr_pos(Y):
     return Q * d[None, :]
 
 
+def cholqr2(Y: torch.Tensor) -> torch.Tensor:
+    """Q of Y = QR (R diagonal > 0, like _qr_pos) by CholeskyQR2 with FP64 Gram matrices:
+    R1 = chol(Y^T Y), Q1 = Y R1^-1, then once more on Q1 (the second pass restores orthogonality to
+    FP32 level for cond(Y) up to ~1e7). Falls back to Householder QR when the Gram matrix is not
+    numerically positive definite. Tall-skinny QR as two GEMMs + a tiny Cholesky + a TRSM instead of
+    cuSOLVER's panel factorization (16384 x 272: see DESIGN.md §8)."""
+    X = Y.double()
+    for _ in range(2):
+        G = X.t() @ X
+        L, info = torch.linalg.cholesky_ex(G)
+        if int(info) != 0:
+            return _qr_pos(Y)
+        X = torch.linalg.solve_triangular(L.t(), X, upper=True, left=False)
+    return X.to(Y.dtype)
+
+
+def gram_svd(Bt: torch.Tensor, p: int):
+    """Top-p SVD of B = Bt^T (nhat x N, nhat small) from the FP64 eigendecomposition of B B^T:
+    B B^T = U' diag(S^2) U'^T, V = B^T U' S^-1. Singular values carry a relative error
+    ~ u64 (S_1 / S_i)^2, so the route is for the well-separated leading p of a randomized SVD;
+    U S V^T = U' U'^T B exactly up to rounding, so the reconstruction is unaffected."""
+    B64 = Bt.double()
+    w, U = torch.linalg.eigh(B64.t() @ B64)
+    w, U = w.flip(0)[:p], U.flip(1)[:, :p]
+    S = torch.sqrt(torch.clamp(w, min=0.0))
+    V = (B64 @ U) / torch.clamp(S, min=torch.finfo(torch.float64).tiny)[None, :]
+    return U.float(), S.float(), V.float()
+
+
 def omega_fp32(k: int, n: int, seed: int = 0, stream_id: int = 0, device="cuda") -> torch.Tensor:
     """FP32 Gaussian k x n (column-major view): the SAME counter-based draws as gen_omega's FP16 Omega
     (OMEGA_SPEC §2-3 addressing, §6 FP32 output) before the RN16 rounding, so the SGEMM baseline
@@ -70,10 +99,14 @@ def omega_fp32(k: int, n: int, seed: int = 0, stream_id: int = 0, device="cuda")
 
 
 def rsvd(A: torch.Tensor, p: int, s: int = 10, seed: int = 0, dist="gaussian", projection="shgemm",
-         timing: bool = False, gemm: str = "sgemm"):
-    """Alg 1: Y = A Omega; Q = QR(Y); B = Q^T A; (U', S, V) = tSVD(B, p); U = Q U'."""
+         timing: bool = False, gemm: str = "sgemm", factor: str = "cusolver"):
+    """Alg 1: Y = A Omega; Q = QR(Y); B = Q^T A; (U', S, V) = tSVD(B, p); U = Q U'.
+    factor='cusolver' (the paper's: Householder QR and SVD from cuSOLVER) or 'gram' (CholeskyQR2 and
+    the FP64 Gram-eigh SVD; needs gemm='tcec' for B^T)."""
     if gemm not in ("sgemm", "tcec"):
         raise ValueError(gemm)
+    if factor not in ("cusolver", "gram") or (factor == "gram" and gemm != "tcec"):
+        raise ValueError(factor)
     m, n = A.shape
     nhat = p + s
     t = _Timer(timing)
@@ -88,15 +121,19 @@ def rsvd(A: torch.Tensor, p: int, s: int = 10, seed: int = 0, dist="gaussian", p
         else:
             raise ValueError(projection)
         t.mark("2_qr")
-        Q = _qr_pos(Y)
+        Q = cholqr2(Y) if factor == "gram" else _qr_pos(Y)
         t.mark("3_QtA")
         B = tcec_sgemm(A.t(), Q).t() if gemm == "tcec" else Q.t() @ A
         t.mark("4_svd")
-        Uh, S, Vt = torch.linalg.svd(B, full_matrices=False)
+        if factor == "gram":
+            Uh, S, V = gram_svd(B.t(), p)
+        else:
+            Uh, S, Vt = torch.linalg.svd(B, full_matrices=False)
+            V = Vt[:p].t()
         t.mark("5_QU")
         U = Q @ Uh[:, :p]     # 16384 x 272 x 256: launch-bound either way, left on cuBLAS
         t.mark("end")
-    return {"U": U, "S": S[:p], "V": Vt[:p].t(), "Q": Q, "times_ms": t.result()}
+    return {"U": U, "S": S[:p], "V": V, "Q": Q, "times_ms": t.result()}
 
 
 def reconstruction_error(A, U, S, V) -> float:
@@ -130,11 +167,11 @@ def core_tcec(T: torch.Tensor, Qs) -> torch.Tensor:
 
 
 def rp_hosvd(T: torch.Tensor, ranks, seed: int = 0, dist="gaussian", projection="shgemm", timing=False,
-             gemm: str = "sgemm"):
+             gemm: str = "sgemm", factor: str = "cusolver"):
     """Alg 2: for each mode W = A'_(i) Omega_(i) (project, stream_id = mode), Q_i = QR(W);
-    g = A x_1 Q_1^T ... x_N Q_N^T."""
-    if gemm not in ("sgemm", "tcec"):
-        raise ValueError(gemm)
+    g = A x_1 Q_1^T ... x_N Q_N^T. factor='gram': CholeskyQR2 for the QRs."""
+    if gemm not in ("sgemm", "tcec") or factor not in ("cusolver", "gram"):
+        raise ValueError((gemm, factor))
     t = _Timer(timing)
     Qs = []
     ws = None
@@ -153,7 +190,7 @@ def rp_hosvd(T: torch.Tensor, ranks, seed: int = 0, dist="gaussian", projection=
             else:
                 raise ValueError(projection)
             t.mark("3_qr")
-            Qs.append(_qr_pos(W))
+            Qs.append(cholqr2(W) if factor == "gram" else _qr_pos(W))
         t.mark("5_core")
         if gemm == "tcec":
             g = core_tcec(T, Qs)

@@ -127,3 +127,53 @@ def test_rsvd_config2_full_size_tcec(shg, pl):
     r_s = pl.rsvd(A, p, s, seed=0, gemm="sgemm")
     e_s = pl.reconstruction_error(A, r_s["U"], r_s["S"], r_s["V"])
     assert abs(e_t - e_s) <= 1e-4 * e_s, (e_t, e_s)
+
+
+def test_cholqr2_matches_householder(shg, pl):
+    """CholeskyQR2 (FP64 Gram): orthonormal to FP32 level and the same Q as Householder with a
+    positive R diagonal; a rank-deficient Y falls back to Householder."""
+    g = torch.Generator(device="cuda").manual_seed(3)
+    Y = torch.randn(5000, 80, device="cuda", generator=g) @ torch.diag(torch.logspace(0, -4, 80, device="cuda"))
+    Q = pl.cholqr2(Y)
+    Qh = pl._qr_pos(Y)
+    I = torch.eye(80, device="cuda", dtype=torch.float64)
+    assert float((Q.double().t() @ Q.double() - I).abs().max()) < 1e-5
+    assert float((Q - Qh).abs().max()) < 1e-3
+    Yd = torch.cat([Y[:, :40], Y[:, :40]], 1)            # exactly rank 40: Gram not PD
+    Qd = pl.cholqr2(Yd)
+    assert Qd.shape == (5000, 80) and torch.isfinite(Qd).all()
+
+
+@pytest.mark.parametrize("kind", ["linear", "exp"])
+def test_rsvd_gram_factor_matches_oracle_pipeline(shg, pl, kind):
+    from oracle import pipelines as opl
+    N, p, s, s_p = 512, 22, 10, 1e-2
+    A = synth.spectrum_matrix(synth.spectrum(kind, N, p, s_p), seed=3)
+    r = pl.rsvd(torch.from_numpy(A).cuda(), p, s, seed=4, gemm="tcec", factor="gram")
+    e_gpu = pl.reconstruction_error(torch.from_numpy(A).cuda(), r["U"], r["S"], r["V"])
+    e_or = opl.rsvd(A, p, s, seed=4, precision="f32")["residual"]
+    assert abs(e_gpu - e_or) <= 1e-4 * e_or, (e_gpu, e_or)
+    S_or = opl.rsvd(A, p, s, seed=4, precision="f64")["S"]
+    assert np.max(np.abs(to_np(r["S"]) - S_or)) <= 1e-5 * S_or[0]       # backward-stable level, ~100 u32 ||B||
+
+
+def test_rsvd_config2_full_size_gram(shg, pl):
+    """cfg2 with CholeskyQR2 + Gram-eigh SVD + TCEC line 3: residual within 1e-4 relative of the
+    cuSOLVER/SGEMM pipeline's."""
+    N, p, s, s_p = 16384, 256, 16, 1e-2
+    A = synth.spectrum_matrix_torch(synth.spectrum("exp", N, p, s_p), seed=1)
+    r_g = pl.rsvd(A, p, s, seed=0, gemm="tcec", factor="gram")
+    e_g = pl.reconstruction_error(A, r_g["U"], r_g["S"], r_g["V"])
+    del r_g
+    r_s = pl.rsvd(A, p, s, seed=0)
+    e_s = pl.reconstruction_error(A, r_s["U"], r_s["S"], r_s["V"])
+    assert abs(e_g - e_s) <= 1e-4 * e_s, (e_g, e_s)
+
+
+def test_rp_hosvd_gram_factor(shg, pl):
+    from oracle import pipelines as opl
+    T = synth.alg3_tensor((64, 48, 40), (16, 16, 16), pad=4, seed=5, noise=1e-2)
+    r = pl.rp_hosvd(torch.from_numpy(T).cuda(), (16, 16, 16), seed=2, gemm="tcec", factor="gram")
+    e_gpu = pl.hosvd_error(torch.from_numpy(T).cuda(), r["core"], r["Q"])
+    e_or = opl.rp_hosvd(T, (16, 16, 16), seed=2, precision="f32")["residual"]
+    assert abs(e_gpu - e_or) <= 1e-4 * e_or, (e_gpu, e_or)
