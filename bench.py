@@ -175,22 +175,25 @@ def run_pipeline(args):
     if args.config == "rsvd_cfg2":
         N, p, sov = 16384, 256, 16
         X = synth.spectrum_matrix_torch(synth.spectrum("exp", N, p, 1e-2), seed=1)
-        run = lambda proj, gemm: pl.rsvd(X, p, sov, seed=0, projection=proj, timing=True, gemm=gemm)
+        run = lambda proj, gemm, fac: pl.rsvd(X, p, sov, seed=0, projection=proj, timing=True, gemm=gemm, factor=fac)
         err = lambda r: pl.reconstruction_error(X, r["U"], r["S"], r["V"])
         flops = 2.0 * N * N * (p + sov)
     else:
         X = torch.from_numpy(synth.alg3_tensor((1024, 1024, 1024), (64, 64, 64), pad=4, seed=1)).cuda()
-        run = lambda proj, gemm: pl.rp_hosvd(X, (64, 64, 64), seed=0, projection=proj, timing=True, gemm=gemm)
+        run = lambda proj, gemm, fac: pl.rp_hosvd(X, (64, 64, 64), seed=0, projection=proj, timing=True, gemm=gemm,
+                                                  factor=fac)
         err = lambda r: pl.hosvd_error(X, r["core"], r["Q"])
         flops = 3 * 2.0 * X.numel() * 64
     res = {}
-    # product: SHGEMM projection + TCEC-SGEMM for the other FP32 products (NEXT-2); the paper's own
-    # configuration (SHGEMM projection only); the FP32 SGEMM baseline pipeline
-    variants = {"shgemm+tcec": ("shgemm", "tcec"), "shgemm": ("shgemm", "sgemm"), "sgemm": ("sgemm", "sgemm")}
-    for name, (proj, gemm) in variants.items():
+    # product: SHGEMM projection + TCEC-SGEMM for the other FP32 products (NEXT-2) + CholeskyQR2 /
+    # Gram-eigh factorizations; the same with cuSOLVER QR/SVD; the paper's own configuration
+    # (SHGEMM projection only); the FP32 SGEMM baseline pipeline
+    variants = {"shgemm+tcec+gram": ("shgemm", "tcec", "gram"), "shgemm+tcec": ("shgemm", "tcec", "cusolver"),
+                "shgemm": ("shgemm", "sgemm", "cusolver"), "sgemm": ("sgemm", "sgemm", "cusolver")}
+    for name, (proj, gemm, fac) in variants.items():
         times, last = [], None
         for it in range(args.warmup + args.steps):
-            last = run(proj, gemm)
+            last = run(proj, gemm, fac)
             if it >= args.warmup:
                 times.append(last["times_ms"])
         tot = sorted(t["total"] for t in times)
@@ -200,11 +203,12 @@ def run_pipeline(args):
     proj_key = [k for k in res["shgemm"]["lines_ms"] if "projection" in k][0]
     if rank == 0:
         print(json.dumps({
-            "metric": METRIC, "value": res["shgemm+tcec"]["total_ms"], "unit": "ms", "n_gpus": 1, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": res["shgemm+tcec"]["total_ms"], "higher_is_better": False,
-            "scaling": "none", "vs_baseline": None, "dtype": "f16*f16->f32 projection; TCEC f16 (FP32-accurate) other products; f32 QR/SVD",
+            "metric": METRIC, "value": res["shgemm+tcec+gram"]["total_ms"], "unit": "ms", "n_gpus": 1,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": res["shgemm+tcec+gram"]["total_ms"],
+            "higher_is_better": False,
+            "scaling": "none", "vs_baseline": None, "dtype": "f16*f16->f32 projection; TCEC f16 (FP32-accurate) other products; f64-Gram CholeskyQR2 / eigh",
             "data": "synthetic", "config": {"workload": args.config, "description": PIPELINES[args.config]},
-            "pipeline": res, "speedup_vs_sgemm_pipeline": res["sgemm"]["total_ms"] / res["shgemm+tcec"]["total_ms"],
+            "pipeline": res, "speedup_vs_sgemm_pipeline": res["sgemm"]["total_ms"] / res["shgemm+tcec+gram"]["total_ms"],
             "speedup_projection_only_vs_sgemm_pipeline": res["sgemm"]["total_ms"] / res["shgemm"]["total_ms"],
             "projection_speedup": res["sgemm"]["lines_ms"][proj_key] / res["shgemm"]["lines_ms"][proj_key],
             "projection_tflops": flops / (res["shgemm"]["lines_ms"][proj_key] * 1e-3) / 1e12,

@@ -54,6 +54,14 @@ DevInfo& dev_info() {
         cudaDeviceGetAttribute(&d.major, cudaDevAttrComputeCapabilityMajor, dev);
         cudaDeviceGetAttribute(&d.minor, cudaDevAttrComputeCapabilityMinor, dev);
         d.ok = (d.major == 10 && d.minor == 0);
+        // stream-ordered scratch (split-K planes, B splits, Omega of project()) comes from the default
+        // pool: keep freed blocks in the pool instead of returning them to the OS at every sync
+        cudaMemPool_t pool;
+        if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+            uint64_t keep = ~0ull;
+            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+        }
+        (void)cudaGetLastError();
     });
     return infos[dev];
 }

@@ -62,20 +62,28 @@ def _qr_pos(Y):
     return Q * d[None, :]
 
 
-def cholqr2(Y: torch.Tensor) -> torch.Tensor:
-    """Q of Y = QR (R diagonal > 0, like _qr_pos) by CholeskyQR2 with FP64 Gram matrices:
-    R1 = chol(Y^T Y), Q1 = Y R1^-1, then once more on Q1 (the second pass restores orthogonality to
-    FP32 level for cond(Y) up to ~1e7). Falls back to Householder QR when the Gram matrix is not
-    numerically positive definite. Tall-skinny QR as two GEMMs + a tiny Cholesky + a TRSM instead of
-    cuSOLVER's panel factorization (16384 x 272: see DESIGN.md §8)."""
+def cholqr2_async(Y: torch.Tensor):
+    """(Q, bad) for Y = QR (R diagonal > 0, like _qr_pos) by CholeskyQR2 with FP64 Gram matrices:
+    L1 = chol(Y^T Y), Q1 = Y L1^-T, then once more on Q1 (the second pass restores orthogonality to
+    FP32 level for cond(Y) up to ~1e7). Tall-skinny QR as GEMMs + a tiny Cholesky + a tiny
+    triangular inverse instead of cuSOLVER's panel factorization (16384 x 272: 1.2 vs 4.6 ms, DESIGN.md
+    §8). Nothing synchronizes: `bad` is a device tensor, nonzero if a Gram matrix was not numerically
+    positive definite (then Q is garbage and the caller recomputes with Householder)."""
     X = Y.double()
+    n = X.shape[1]
+    eye = torch.eye(n, dtype=torch.float64, device=Y.device)
+    bad = torch.zeros((), dtype=torch.int32, device=Y.device)
     for _ in range(2):
-        G = X.t() @ X
-        L, info = torch.linalg.cholesky_ex(G)
-        if int(info) != 0:
-            return _qr_pos(Y)
-        X = torch.linalg.solve_triangular(L.t(), X, upper=True, left=False)
-    return X.to(Y.dtype)
+        L, info = torch.linalg.cholesky_ex(X.t() @ X)
+        bad = bad + info.to(torch.int32)
+        X = X @ torch.linalg.solve_triangular(L, eye, upper=False).t()
+    return X.to(Y.dtype), bad
+
+
+def cholqr2(Y: torch.Tensor) -> torch.Tensor:
+    """cholqr2_async with the Householder fallback applied (one synchronization)."""
+    Q, bad = cholqr2_async(Y)
+    return _qr_pos(Y) if int(bad) != 0 else Q
 
 
 def gram_svd(Bt: torch.Tensor, p: int):
@@ -121,7 +129,11 @@ def rsvd(A: torch.Tensor, p: int, s: int = 10, seed: int = 0, dist="gaussian", p
         else:
             raise ValueError(projection)
         t.mark("2_qr")
-        Q = cholqr2(Y) if factor == "gram" else _qr_pos(Y)
+        bad = None
+        if factor == "gram":
+            Q, bad = cholqr2_async(Y)
+        else:
+            Q = _qr_pos(Y)
         t.mark("3_QtA")
         B = tcec_sgemm(A.t(), Q).t() if gemm == "tcec" else Q.t() @ A
         t.mark("4_svd")
@@ -133,6 +145,8 @@ def rsvd(A: torch.Tensor, p: int, s: int = 10, seed: int = 0, dist="gaussian", p
         t.mark("5_QU")
         U = Q @ Uh[:, :p]     # 16384 x 272 x 256: launch-bound either way, left on cuBLAS
         t.mark("end")
+    if bad is not None and int(bad) != 0:     # Gram not positive definite: redo with Householder QR
+        return rsvd(A, p, s, seed, dist, projection, timing, gemm, "cusolver")
     return {"U": U, "S": S[:p], "V": V, "Q": Q, "times_ms": t.result()}
 
 
@@ -173,7 +187,7 @@ def rp_hosvd(T: torch.Tensor, ranks, seed: int = 0, dist="gaussian", projection=
     if gemm not in ("sgemm", "tcec") or factor not in ("cusolver", "gram"):
         raise ValueError((gemm, factor))
     t = _Timer(timing)
-    Qs = []
+    Qs, bads = [], []
     ws = None
     if projection == "shgemm":   # one persistent scratch buffer (Omega_(i) + split-K partials) for all modes
         nbytes = max(project_workspace_size(list(T.shape), i, J) for i, J in enumerate(ranks))
@@ -190,7 +204,12 @@ def rp_hosvd(T: torch.Tensor, ranks, seed: int = 0, dist="gaussian", projection=
             else:
                 raise ValueError(projection)
             t.mark("3_qr")
-            Qs.append(cholqr2(W) if factor == "gram" else _qr_pos(W))
+            if factor == "gram":
+                Q, b = cholqr2_async(W)
+                bads.append(b)
+                Qs.append(Q)
+            else:
+                Qs.append(_qr_pos(W))
         t.mark("5_core")
         if gemm == "tcec":
             g = core_tcec(T, Qs)
@@ -199,6 +218,8 @@ def rp_hosvd(T: torch.Tensor, ranks, seed: int = 0, dist="gaussian", projection=
             for i, Q in enumerate(Qs):
                 g = mode_product(g, Q, i)
         t.mark("end")
+    if bads and int(sum(bads)) != 0:
+        return rp_hosvd(T, ranks, seed, dist, projection, timing, gemm, "cusolver")
     return {"core": g, "Q": Qs, "times_ms": t.result()}
 
 

@@ -16,13 +16,15 @@ def best(fn, reps=3):
 
 N, p, s = 16384, 256, 16
 A = synth.spectrum_matrix_torch(synth.spectrum('exp', N, p, 1e-2), seed=1)
-for proj, gemm in (('shgemm', 'tcec'), ('shgemm', 'sgemm'), ('sgemm', 'sgemm')):
-    r = best(lambda: pl.rsvd(A, p, s, seed=0, projection=proj, timing=True, gemm=gemm))
+for proj, gemm, fac in (('shgemm', 'tcec', 'gram'), ('shgemm', 'tcec', 'cusolver'), ('shgemm', 'sgemm', 'cusolver'),
+                        ('sgemm', 'sgemm', 'cusolver')):
+    r = best(lambda: pl.rsvd(A, p, s, seed=0, projection=proj, timing=True, gemm=gemm, factor=fac))
     e = pl.reconstruction_error(A, r['U'], r['S'], r['V'])
-    print(json.dumps({'pipeline': 'rsvd_cfg2', 'projection': proj, 'gemm': gemm, 'times_ms': r['times_ms'], 'residual': e}), flush=True)
+    print(json.dumps({'pipeline': 'rsvd_cfg2', 'projection': proj, 'gemm': gemm, 'factor': fac, 'times_ms': r['times_ms'], 'residual': e}), flush=True)
 del A; torch.cuda.empty_cache()
 T = torch.from_numpy(synth.alg3_tensor((1024, 1024, 1024), (64, 64, 64), pad=4, seed=1)).cuda()
-for proj, gemm in (('shgemm', 'tcec'), ('shgemm', 'sgemm'), ('sgemm', 'sgemm')):
-    r = best(lambda: pl.rp_hosvd(T, (64, 64, 64), seed=0, projection=proj, timing=True, gemm=gemm))
+for proj, gemm, fac in (('shgemm', 'tcec', 'gram'), ('shgemm', 'tcec', 'cusolver'), ('shgemm', 'sgemm', 'cusolver'),
+                        ('sgemm', 'sgemm', 'cusolver')):
+    r = best(lambda: pl.rp_hosvd(T, (64, 64, 64), seed=0, projection=proj, timing=True, gemm=gemm, factor=fac))
     e = pl.hosvd_error(T, r['core'], r['Q'])
-    print(json.dumps({'pipeline': 'rphosvd_cfg3', 'projection': proj, 'gemm': gemm, 'times_ms': r['times_ms'], 'residual': e}), flush=True)
+    print(json.dumps({'pipeline': 'rphosvd_cfg3', 'projection': proj, 'gemm': gemm, 'factor': fac, 'times_ms': r['times_ms'], 'residual': e}), flush=True)
