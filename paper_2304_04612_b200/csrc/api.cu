@@ -295,16 +295,17 @@ Plan make_plan(int64_t m, int64_t n, int64_t k, bool fast_ok, const shg_tune_t* 
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 
 
-// M-major A (element (i, l) at A[l * lda + i]): 2-D map {M, K}, box {32 rows, 64 k}
+// M-major A (element (i, l) at A[l * lda + i]): 2-D map {M, K}, box {128 rows, 64 k}, no swizzle
+// (512 contiguous bytes per k-line; rows >= M zero-filled)
 bool encode_a_mmajor(CUtensorMap* map, const float* A, int64_t M, int64_t K, int64_t lda) {
     EncodeFn fn = encode_fn();
     if (!fn) return false;
     cuuint64_t dims[2] = {static_cast<cuuint64_t>(M), static_cast<cuuint64_t>(K)};
     cuuint64_t strides[1] = {static_cast<cuuint64_t>(lda) * 4};
-    cuuint32_t box[2] = {32, 64};
+    cuuint32_t box[2] = {128, 64};
     cuuint32_t estr[2] = {1, 1};
     return fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(A), dims, strides, box, estr,
-              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 

@@ -346,9 +346,10 @@ __device__ __forceinline__ void add2_rn(float& a, float& b, float c, float d) {
 // MMAJOR = false: A is K-major (row-major m x k, or a 3-D K-major view of an unfolding); each stage
 //                 is two TMA boxes of 32 k x 128 rows.
 // MMAJOR = true : A is M-major (element (i, l) at A[l * lda + i], e.g. the last-mode unfolding of a
-//                 C-order tensor); each stage is four TMA boxes of 32 rows x 64 k, and the splitter
-//                 gathers its row's k values with conflict-free 32-bit loads (one 128-B smem row per
-//                 warp instruction) — no transpose copy.
+//                 C-order tensor); each stage is ONE unswizzled TMA box of 128 rows x 64 k (512 B per
+//                 k-line: the former four 32-row SW128 boxes fetched 128 B per visit of lines up to
+//                 4 MB apart), and the splitter gathers its row's k values with conflict-free 32-bit
+//                 loads (a warp's 32 rows are one 128-B run) — no transpose copy.
 // PAIR          : CTA pair (launch with cluster dims (2,1,1)); see the header comment.
 // TF32          : SHGEMM-TF32 (Cfg's header); mapB0/B1 then describe the FP32 (TF32) copy of Omega.
 // TCEC          : TCEC-SGEMM (Cfg's header): two B tiles per stage, three MMA groups per chunk.
@@ -473,16 +474,14 @@ shgemm_sm100_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_const
                                 uint32_t hi[16], lo[16];
                                 if (!skip_math) {
                                     if constexpr (MMAJOR) {
-                                        const uint8_t* box = a32 + sa * kA32StageBytes + (r >> 5) * (kA32StageBytes / 4);
-                                        const int cidx = (r & 31) >> 2;
-                                        const int word = (r & 3) * 4;
+                                        // unswizzled [64 k][128 rows] stage: this thread's row r at
+                                        // word r of every 512-B k-line (a warp reads one 128-B run)
+                                        const float* colp = reinterpret_cast<const float*>(a32 + sa * kA32StageBytes) + r;
 #pragma unroll
                                         for (int i = 0; i < 8; ++i) {
                                             const int k0 = 32 * kh + 16 * rd + 2 * i;
-                                            const float a0 = *reinterpret_cast<const float*>(box + k0 * 128 + ((cidx ^ (k0 & 7)) << 4) + word);
-                                            const float a1 = *reinterpret_cast<const float*>(
-                                                box + (k0 + 1) * 128 + ((cidx ^ ((k0 + 1) & 7)) << 4) + word);
-                                            split_tf32_x2(a0, a1, hi[2 * i], hi[2 * i + 1], lo[2 * i], lo[2 * i + 1]);
+                                            split_tf32_x2(colp[k0 * kBM], colp[(k0 + 1) * kBM], hi[2 * i], hi[2 * i + 1],
+                                                          lo[2 * i], lo[2 * i + 1]);
                                         }
                                     } else {
                                         const uint8_t* src = a32 + sa * kA32StageBytes + a_line * 128;
@@ -513,18 +512,14 @@ shgemm_sm100_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_const
                         } else {
                         uint32_t hi[16], lo[16];
                         if (!skip_math && MMAJOR) {
-                            // box r/32 holds rows 32*(r/32).. as 64 k-rows of 128 B (SW128); this
-                            // thread's column is r%32: 16-B chunk (r%32)/4, word r%4
-                            const uint8_t* box = a32 + sa * kA32StageBytes + (r >> 5) * (kA32StageBytes / 4);
-                            const int cidx = (r & 31) >> 2;
-                            const int word = (r & 3) * 4;
+                            // unswizzled [64 k][128 rows] stage (one TMA box, 512 B per k-line):
+                            // this thread's row r is word r of every k-line; a warp's 32 rows are
+                            // one conflict-free 128-B run
+                            const float* colp = reinterpret_cast<const float*>(a32 + sa * kA32StageBytes) + r;
 #pragma unroll
                             for (int i = 0; i < 16; ++i) {       // k pairs 32kh + 2i, +1
                                 const int k0 = 32 * kh + 2 * i;
-                                const float a0 = *reinterpret_cast<const float*>(box + k0 * 128 + ((cidx ^ (k0 & 7)) << 4) + word);
-                                const float a1 =
-                                    *reinterpret_cast<const float*>(box + (k0 + 1) * 128 + ((cidx ^ ((k0 + 1) & 7)) << 4) + word);
-                                split2_x2(a0, a1, hi[i], lo[i]);
+                                split2_x2(colp[k0 * kBM], colp[(k0 + 1) * kBM], hi[i], lo[i]);
                             }
                         } else if (!skip_math) {
                             const uint8_t* src = a32 + sa * kA32StageBytes + a_line * 128;
@@ -689,11 +684,9 @@ shgemm_sm100_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_const
                         const int c2 = static_cast<int>(kk / p.k_inner);
                         uint8_t* dst = a32 + sa * kA32StageBytes;
                         if (MMAJOR) {
-                            // 2-D map {M (inner), K}: four boxes of 32 rows x 64 k
-#pragma unroll
-                            for (int b = 0; b < 4; ++b)
-                                tma_load_2d(dst + b * (kA32StageBytes / 4), &mapA, &a_full[sa], m0 + 32 * b,
-                                            static_cast<int>(kk), pol);
+                            // 2-D map {M (inner), K}, no swizzle: one box of 128 rows x 64 k, each
+                            // k-line 512 contiguous bytes (4 KB-4 MB apart in HBM: one visit per line)
+                            tma_load_2d(dst, &mapA, &a_full[sa], m0, static_cast<int>(kk), pol);
                         } else if (p.a_rowpair) {
                             // 4-D map {32, S/32, M, P}: one box of 128 rows x (2 x 32 k), row major
                             tma_load_4d(dst, &mapA, &a_full[sa], 0, c0 >> 5, m0, c2, pol);
