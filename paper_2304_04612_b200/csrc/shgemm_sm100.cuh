@@ -20,7 +20,7 @@
 //                 (D := sum lo.Omega) then 8 hi MMAs, the first with scale-input-d = 11
 //                 (D := hi.Omega + D * 2^-11), so D holds hi.Omega + 2^-11 lo.Omega (Eq 16) for
 //                 the chunk. Part accumulators rotate through NSLOT TMEM slots.
-//  * Promotion  : 8 epilogue warps (4 lane quarters x 2 N-parts) tcgen05.ld each finished D and
+//  * Promotion  : 8 epilogue warps (4 lane quarters x 2 column halves) tcgen05.ld each finished D and
 //                 add it with RN (add.rn.f32x2) into register accumulators: the RZ-avoidance of
 //                 PAPER.md:587 applied per K_c = 128 chunk (and to lo as well: reading R2).
 //  * Epilogue   : after the last chunk, the RN accumulators are written to Y (row-major) with
@@ -169,7 +169,6 @@ struct Cfg {
     static constexpr int NQ = (TF32 && BN <= 64) ? 1 : 2;
     static constexpr int W = NQ == 1 ? BN : ((BN / 2) + 15) / 16 * 16;    // width of part 0
     static constexpr int WLAST = NQ == 1 ? BN : BN - W;                     // width of the last part
-    static constexpr int NPH = 1;                          // parts per epilogue group
     static constexpr int SB = NCH * KC;                    // TMEM A stage slots
     static constexpr int ABASE = kTmemCols - SB * AST;
     static constexpr int NSLOT_fit = ABASE / W;
@@ -364,7 +363,10 @@ shgemm_sm100_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_const
                     const __grid_constant__ CUtensorMap mapB1, const KParams p) {
     using CF = Cfg<BN, PAIR, TF32, TCEC>;
     constexpr int SA = CF::SA, NQ = CF::NQ, W = CF::W, WLAST = CF::WLAST;
-    constexpr int NPH = CF::NPH, NSLOT = CF::NSLOT, ABASE = CF::ABASE;
+    constexpr int NSLOT = CF::NSLOT, ABASE = CF::ABASE;
+    // epilogue mapping (below): both groups drain half of every part for wide tiles and for one-part
+    // tiles (TF32 BN <= 64, where group 1 would otherwise idle); else one part per group
+    constexpr bool SPLITH = CF::WIDE || NQ == 1;
     constexpr int kOm = CF::kOmStageBytes;
     constexpr int NCH = CF::NCH, KC = CF::KC;
     constexpr int SO = CF::SO;
@@ -381,7 +383,7 @@ shgemm_sm100_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_const
     uint64_t* ch_ready = a_empty + SA;       // chunk hi/lo in TMEM + Omega in smem (leader: count 8|16 + 1|2 + tx)
     uint64_t* ch_empty = ch_ready + NCH;     // MMAs done with the chunk slot       (tcgen05.commit)
     uint64_t* acc_full = ch_empty + NCH;     // D slot complete                     (tcgen05.commit)
-    uint64_t* acc_empty = acc_full + NSLOT;  // D slot drained                      (leader: count 4|8)
+    uint64_t* acc_empty = acc_full + NSLOT;  // D slot drained                      (leader: 4|8 warps, SPLITH 8|16)
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + NSLOT);
 
     const uint32_t warp = warp_id();
@@ -412,7 +414,7 @@ shgemm_sm100_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_const
             mbar_init(&ch_ready[i], kPair * (kNumSplitWarps + 1));
             mbar_init(&ch_empty[i], NP);
         }
-        for (int i = 0; i < NSLOT; ++i) { mbar_init(&acc_full[i], 1); mbar_init(&acc_empty[i], 4 * kPair); }
+        for (int i = 0; i < NSLOT; ++i) { mbar_init(&acc_full[i], 1); mbar_init(&acc_empty[i], (SPLITH ? 8 : 4) * kPair); }
         fence_mbar_init();
     }
     if (warp == kWarpProdA && lane == 0) {
@@ -568,10 +570,21 @@ shgemm_sm100_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_const
         }
     } else if (warp < kEpiWarp0 + 8) {
         // ============================================================ RN promotion + epilogue
+        // SPLITH (wide tiles): each N part's accumulator is drained by BOTH epilogue groups, group h
+        // taking the h-th half of its columns, so a part's slot is released after half the per-warp
+        // TMEM loads (the next stage's MMAs wait on it; K_c = 64 there). Otherwise group h drains
+        // all of part h, which overlaps the other part's MMAs (measured 2.7% faster at BN = 256).
         asm volatile("setmaxnreg.inc.sync.aligned.u32 168;");
         const int q = static_cast<int>(warp & 3u);                       // TMEM lane quarter (warp_id % 4)
-        const int h = static_cast<int>((warp - kEpiWarp0) >> 2);         // epilogue group: parts h, h+2, ...
+        const int h = static_cast<int>((warp - kEpiWarp0) >> 2);         // epilogue group
         const uint32_t lane_addr = static_cast<uint32_t>(32 * q) << 16;
+        // per group: the column span of each part it drains (HP0: part 0 / all but the last,
+        // HPL: the last part) and its accumulator count
+        constexpr int HP0 = SPLITH ? W / 2 : W, HPL = SPLITH ? WLAST / 2 : WLAST;
+        constexpr int NACC = SPLITH ? HP0 + (NQ > 1 ? HPL : 0) : W;
+        static_assert(HP0 % 8 == 0 && HPL % 8 == 0, "drained spans must be whole tcgen05.ld x8 groups");
+        // parts drained by this group: SPLITH all of them (its half of each), else part h only
+        auto mine = [&](int part) { return SPLITH || part == h; };
         uint32_t stage = 0;
         long long w_full = 0, t_store = 0;
         const bool skip_ld = (p.dbg & 1u) != 0;
@@ -579,37 +592,36 @@ shgemm_sm100_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_const
             int m_blk, s, n_blk, kb0, kb1;
             coords(tile, m_blk, s, n_blk);
             kb_range(s, p, kb0, kb1);
-            float acc[NPH * W];
+            float acc[NACC];
 #pragma unroll
-            for (int i = 0; i < NPH * W; ++i) acc[i] = 0.0f;
+            for (int i = 0; i < NACC; ++i) acc[i] = 0.0f;
             for (int kb = kb0; kb < kb1; kb += CF::KC, ++stage) {   // one promotion per K_c chunk
 #pragma unroll
-                for (int j = 0; j < NPH; ++j) {
-                    const int part = h + 2 * j;
-                    if (part >= NQ) continue;                      // NQ == 1: group 1 idles
-                    const int width = (part == NQ - 1) ? WLAST : W;
+                for (int part = 0; part < NQ; ++part) {
+                    if (!mine(part)) continue;
+                    const int hw = (part == NQ - 1) ? HPL : HP0;       // this group's columns of the part
+                    const int aoff = SPLITH ? part * HP0 : 0;
                     const uint32_t g = stage * NQ + part;
                     const uint32_t slot = g % NSLOT;
                     mbar_wait_prof(&acc_full[slot], (g / NSLOT) & 1u, w_full);
                     tc_fence_after();
-                    const uint32_t taddr = tmem_base + lane_addr + slot * W;
+                    const uint32_t taddr = tmem_base + lane_addr + slot * W + (SPLITH ? h * hw : 0);
                     if (!skip_ld) {
                         // 16 columns per wait (two tcgen05.ld in flight)
-                        constexpr int LDU = 2;
 #pragma unroll
-                        for (int c = 0; c < W; c += 8 * LDU) {
-                            if (c < width) {
-                                float v[LDU][8];
+                        for (int c = 0; c < HP0; c += 16) {
+                            if (c < hw) {
+                                float v[2][8];
 #pragma unroll
-                                for (int u = 0; u < LDU; ++u)
-                                    if (c + 8 * u < width) tmem_ld8(taddr + c + 8 * u, v[u]);
+                                for (int u = 0; u < 2; ++u)
+                                    if (c + 8 * u < hw) tmem_ld8(taddr + c + 8 * u, v[u]);
                                 tmem_ld_wait();
 #pragma unroll
-                                for (int u = 0; u < LDU; ++u)
+                                for (int u = 0; u < 2; ++u)
 #pragma unroll
                                     for (int i = 0; i < 8; i += 2)
-                                        if (c + 8 * u < width)
-                                            ADD_PAIR(acc[j * W + c + 8 * u + i], acc[j * W + c + 8 * u + i + 1],
+                                        if (c + 8 * u < hw)
+                                            ADD_PAIR(acc[aoff + c + 8 * u + i], acc[aoff + c + 8 * u + i + 1],
                                                      v[u][i], v[u][i + 1]);
                             }
                         }
@@ -622,36 +634,36 @@ shgemm_sm100_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_const
                     }
                 }
             }
-            // ---- store the tile rows owned by this thread (its parts' columns)
+            // ---- store the tile rows owned by this thread (its half of every part's columns)
             const long long ts0 = clock64();
             const int64_t row = static_cast<int64_t>(m_blk) * CF::kTileM + static_cast<int64_t>(crank) * kBM + 32 * q +
                                 static_cast<int>(lane);
             if (row < p.m) {
 #pragma unroll
-                for (int j = 0; j < NPH; ++j) {
-                    const int part = h + 2 * j;
-                    if (part >= NQ) continue;
-                    const int width = (part == NQ - 1) ? WLAST : W;
-                    const int64_t col0 = static_cast<int64_t>(n_blk) * BN + part * W;
+                for (int part = 0; part < NQ; ++part) {
+                    if (!mine(part)) continue;
+                    const int hw = (part == NQ - 1) ? HPL : HP0;
+                    const int aoff = SPLITH ? part * HP0 : 0;
+                    const int64_t col0 = static_cast<int64_t>(n_blk) * BN + part * W + (SPLITH ? h * hw : 0);
                     if (col0 >= p.n) continue;
                     float* dst = p.out + static_cast<int64_t>(s) * p.split_stride + row * p.ldo_out + col0;
-                    const int64_t valid = (p.n - col0) < width ? (p.n - col0) : width;
+                    const int64_t valid = (p.n - col0) < hw ? (p.n - col0) : hw;
                     bool bad = false;
-                    if (p.vec_store && valid == width) {
+                    if (p.vec_store && valid == hw) {
 #pragma unroll
-                        for (int i = 0; i < W; i += 4)
-                            if (i < width)
+                        for (int i = 0; i < HP0; i += 4)
+                            if (i < hw)
                                 *reinterpret_cast<float4*>(dst + i) =
-                                    make_float4(acc[j * W + i], acc[j * W + i + 1], acc[j * W + i + 2], acc[j * W + i + 3]);
+                                    make_float4(acc[aoff + i], acc[aoff + i + 1], acc[aoff + i + 2], acc[aoff + i + 3]);
                     } else {
 #pragma unroll
-                        for (int i = 0; i < W; ++i)
-                            if (i < valid) dst[i] = acc[j * W + i];
+                        for (int i = 0; i < HP0; ++i)
+                            if (i < valid) dst[i] = acc[aoff + i];
                     }
                     if (p.nonfinite) {
 #pragma unroll
-                        for (int i = 0; i < W; ++i)
-                            if (i < valid && !isfinite(acc[j * W + i])) bad = true;
+                        for (int i = 0; i < HP0; ++i)
+                            if (i < valid && !isfinite(acc[aoff + i])) bad = true;
                         if (bad) atomicOr(p.nonfinite, 1);
                     }
                 }
