@@ -32,6 +32,8 @@ DATA_SEED, DATA_STREAM, OMEGA_SEED = 2, 0x100, 0
 
 CONFIGS = {
     # name: (m_total, k, n, description)
+    "cfg1": (512, 512, 32, "BASELINE config 1 shape: A 512x512 FP32 . Omega 512x32 FP16 (fits in L2: L2 flushed "
+                           "between timed steps, only the steps timed)"),
     "cfg4": (4194304, 4096, 256, "BASELINE config 4: tall projection A 4,194,304x4096 FP32 . Omega 4096x256 FP16"),
     "cfg5n64": (32768, 32768, 64, "BASELINE config 5 sweep point n=64 (m=k=32768)"),
     "cfg5n256": (32768, 32768, 256, "BASELINE config 5 sweep point n=256 (m=k=32768)"),
@@ -273,23 +275,17 @@ def main():
     stream = torch.cuda.current_stream()
     L = shg.lib()
     import ctypes
-    sp = ctypes.c_void_p(stream.cuda_stream)
+    tune = shg.Tune()
+    tune.tc = shg.TCS[args.tc]
+    ws_bytes = shg.workspace_size(m, n, k, tc=args.tc)
+    ws = torch.empty(max(1, ws_bytes), dtype=torch.uint8, device="cuda")
 
     def gen():
-        shg._check(L.gen_omega_f16(k, n, OMEGA_SEED, 0, shg._p(om_buf), ldo, sp), "gen_omega_f16")
+        shg._check(L.gen_omega_f16(k, n, OMEGA_SEED, 0, shg._p(om_buf), ldo, shg._stream()), "gen_omega_f16")
 
-    if args.tc == "fp16":
-        def gemm():
-            shg._check(L.shgemm(m, n, k, shg._p(A), k, shg._p(om_buf), ldo, shg._p(Y), n, sp), "shgemm")
-    else:
-        tune = shg.Tune()
-        tune.tc = shg.TCS[args.tc]
-        ws_bytes = shg.workspace_size(m, n, k, tc=args.tc)
-        ws = torch.empty(max(1, ws_bytes), dtype=torch.uint8, device="cuda")
-
-        def gemm():
-            shg._check(L.shgemm_ex(m, n, k, shg._p(A), k, shg._p(om_buf), ldo, shg._p(Y), n, ctypes.byref(tune),
-                                   shg._p(ws), ws_bytes, None, sp), "shgemm_ex")
+    def gemm():
+        shg._check(L.shgemm_ex(m, n, k, shg._p(A), k, shg._p(om_buf), ldo, shg._p(Y), n, ctypes.byref(tune),
+                               shg._p(ws), ws_bytes, None, shg._stream()), "shgemm_ex")
 
     def step():
         gen()
@@ -298,6 +294,29 @@ def main():
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
+    # inputs smaller than L2 (126 MB): the step is launch-latency bound, so it is replayed from CUDA
+    # graphs (no host work between kernels), a 512 MiB buffer is written between timed steps (cold
+    # L2) and only the steps are timed; otherwise the inputs are far larger than L2 and the steps run
+    # back to back as direct launches
+    flush = (4.0 * m * k) < 256e6
+    scrub = torch.empty(512 << 20, dtype=torch.uint8, device="cuda") if flush else None
+    run_gen, run_gemm, graph_launches = gen, gemm, None
+    if flush:
+        side = torch.cuda.Stream()
+        side.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(side):
+            for _ in range(3):
+                step()
+        torch.cuda.current_stream().wait_stream(side)
+        g_gen, g_gemm = torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph()
+        c0 = shg.launch_count()
+        with torch.cuda.graph(g_gen):
+            gen()
+        with torch.cuda.graph(g_gemm):
+            gemm()
+        graph_launches = shg.launch_count() - c0          # library kernels per step (captured once)
+        run_gen, run_gemm = g_gen.replay, g_gemm.replay
+        torch.cuda.synchronize()
     # per-launch events for the dominant kernel (shgemm) and the Omega generator, on the launch stream
     ev = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
     clocks = ClockSampler(local)
@@ -311,18 +330,21 @@ def main():
     t_end = torch.cuda.Event(enable_timing=True)
     t_start.record(stream)
     for i in range(args.steps):
+        if flush:
+            scrub.fill_(i & 0xFF)
         ev[i][0].record(stream)
-        gen()
+        run_gen()
         ev[i][1].record(stream)
-        gemm()
+        run_gemm()
         ev[i][2].record(stream)
     t_end.record(stream)
     torch.cuda.synchronize()
-    launches = shg.launch_count() - launches0
+    launches = shg.launch_count() - launches0 if graph_launches is None else graph_launches * args.steps
     if dist:
         dist.barrier()
     clk = clocks.stop()
-    total_ms = t_start.elapsed_time(t_end)
+    total_ms = (sum(ev[i][0].elapsed_time(ev[i][2]) for i in range(args.steps)) if flush
+                else t_start.elapsed_time(t_end))
     gemm_ms = statistics.mean(ev[i][1].elapsed_time(ev[i][2]) for i in range(args.steps))
     gen_ms = statistics.mean(ev[i][0].elapsed_time(ev[i][1]) for i in range(args.steps))
     if dist:
@@ -367,6 +389,9 @@ def main():
     roof["frac_hbm"] = achieved_gbs / hbm
     roof["frac_tensor_burst"] = 4.0 * m * k * n / (gemm_ms * 1e-3) / 1e12 / tc16
     roof["frac_tensor_sustained"] = 4.0 * m * k * n / (gemm_ms * 1e-3) / 1e12 / tc16_sus
+    # against the spec sheet (2250 TFLOP/s dense fp16/bf16, 8 TB/s HBM3e), for reference
+    spec_tc = 2250.0 * tc_ratio
+    roof["frac_spec_min(tc/2, AI*hbm)"] = useful_tflops / min(spec_tc / 2.0, ai * 8000.0 / 1e3)
 
     out = None
     if rank == 0:
@@ -385,7 +410,9 @@ def main():
                "config": {"workload": args.config, "description": desc, "m": m_total, "k": k, "n": n,
                           "rows_per_gpu": per, "parallelism": f"row-shard x{world} (no collective on the data path)",
                           "dist_backend": backend,
-                          "l2": "inputs larger than L2 (A is %.1f GiB per GPU), no flush" % (4.0 * m * k / 2 ** 30),
+                          "l2": ("L2 flushed between timed steps (512 MiB write), steps replayed from CUDA graphs "
+                                 "and timed alone" if flush else
+                                 "inputs larger than L2 (A is %.1f GiB per GPU), no flush" % (4.0 * m * k / 2 ** 30)),
                           "kernel": "SHGEMM-FP16" if args.tc == "fp16" else "SHGEMM-TF32",
                           "plan": shg.plan(m, n, k, tc=args.tc)},
                "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
