@@ -61,26 +61,4 @@ __global__ void widen_omega_kernel(const uint16_t* __restrict__ Om, int64_t k, i
     }
 }
 
-// out[c * ldo + r] = in[r * ldi + c] for an R x Cc matrix (used by project() for the M-major
-// last-mode unfolding until the native M-major stager lands).
-__global__ void transpose_f32_kernel(const float* __restrict__ in, int64_t R, int64_t Cc, int64_t ldi,
-                                     float* __restrict__ out, int64_t ldo) {
-    __shared__ float tile[32][33];
-    const int64_t tiles_c = (Cc + 31) / 32;
-    const int64_t tiles_r = (R + 31) / 32;
-    for (int64_t tb = blockIdx.x; tb < tiles_r * tiles_c; tb += gridDim.x) {
-        const int64_t br = (tb / tiles_c) * 32, bc = (tb % tiles_c) * 32;
-        for (int y = threadIdx.y; y < 32; y += blockDim.y) {
-            const int64_t r = br + y, c = bc + threadIdx.x;
-            if (r < R && c < Cc) tile[y][threadIdx.x] = in[r * ldi + c];
-        }
-        __syncthreads();
-        for (int y = threadIdx.y; y < 32; y += blockDim.y) {
-            const int64_t c = bc + y, r = br + threadIdx.x;
-            if (r < R && c < Cc) out[c * ldo + r] = tile[threadIdx.x][y];
-        }
-        __syncthreads();
-    }
-}
-
 }  // namespace shg

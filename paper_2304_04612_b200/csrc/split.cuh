@@ -69,14 +69,6 @@ __device__ __forceinline__ void split_tf32_x2(float a0, float a1, uint32_t& h0, 
     l1 = cvt_rn_tf32(r1);
 }
 
-// eight consecutive-k FP32 values -> 16 B of hi and 16 B of lo
-__device__ __forceinline__ void split8(const float4& x0, const float4& x1, uint4& hi, uint4& lo) {
-    split2(x0.x, x0.y, hi.x, lo.x);
-    split2(x0.z, x0.w, hi.y, lo.y);
-    split2(x1.x, x1.y, hi.z, lo.z);
-    split2(x1.z, x1.w, hi.w, lo.w);
-}
-
 // Elementwise split, for the test ABI shg_debug_split (split2_x2: the mainloop's device function).
 static __global__ void debug_split_kernel(const float* __restrict__ a, int64_t count, uint16_t* __restrict__ hi,
                                    uint16_t* __restrict__ lo) {
