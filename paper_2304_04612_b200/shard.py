@@ -4,8 +4,8 @@ Rows of A are independent units: rank g of G owns rows [g*ceil(m/G), min(m, (g+1
 A and of Y = A . Omega. Every rank regenerates the identical Omega from the shared seed with the
 counter-based generator (OMEGA_SPEC.md §2: the value of Omega[i][j] depends only on (seed, stream,
 i, j)), so there is NO collective on the data path. torch.distributed is used only for plumbing:
-a barrier, the max-over-ranks timing, and (outside the hot path) an optional all-gather of Y for a
-downstream QR (NEXT-3 replaces it with TSQR).
+a barrier, the max-over-ranks timing, and (outside the hot path) an optional all-gather of Y; the
+downstream pipelines use distributed.py instead (TSQR + all-reduce, no gather of Y).
 """
 from __future__ import annotations
 
