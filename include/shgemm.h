@@ -292,6 +292,14 @@ shg_status_t shg_probe_tma_read(const float *A, int64_t m, int64_t k, int64_t ld
                                 int box_rows, int splits, int grid, unsigned long long *bytes_out,
                                 shg_stream_t stream);
 
+/* project()/project_shard() with SHGEMM-FP16: generate Omega_(mode) INSIDE the projection kernel
+ * (on != 0) instead of a separate gen_omega launch, when the plan has every tile resident at once
+ * and single-CTA tiles of BN <= 192 ("fused in-producer Omega"): the m-tiles
+ * that share a k range each generate 1/m_tiles of its k-tiled Omega with their epilogue warps and
+ * publish per-tile flags that the Omega stager acquires. Same bits as gen_omega_f16_tiled. Off by
+ * default (measured slower on B200); process-wide; SHG_OMGEN=1 sets the default. */
+void shg_set_inkernel_omega(int on);
+
 /* Number of kernels this library has launched in this process (monotonic). */
 uint64_t shg_launch_count(void);
 

@@ -90,6 +90,8 @@ def lib():
             L.tcec_sgemm_workspace_size.restype = sz
             L.tcec_plan.argtypes = [i64, i64, i64, ctypes.POINTER(Tune), ctypes.POINTER(Plan)]
             L.shg_launch_count.restype = u64
+            L.shg_set_inkernel_omega.argtypes = [i32]
+            L.shg_set_inkernel_omega.restype = None
             L.shg_last_error.restype = ctypes.c_char_p
             L.shg_device_supported.restype = i32
             L.shg_version.restype = ctypes.c_char_p
@@ -124,6 +126,11 @@ def _p(t: torch.Tensor | None):
 
 def _dist(d) -> int:
     return DISTS[d] if isinstance(d, str) else int(d)
+
+
+def set_inkernel_omega(on: bool) -> None:
+    """project(): generate Omega inside the projection kernel (C ABI shg_set_inkernel_omega)."""
+    lib().shg_set_inkernel_omega(1 if on else 0)
 
 
 def launch_count() -> int:

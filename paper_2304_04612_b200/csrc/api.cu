@@ -8,6 +8,7 @@
 #include <atomic>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 
@@ -203,6 +204,17 @@ struct Plan {
 
 int64_t up256(int64_t b) { return (b + 255) / 256 * 256; }
 
+// Cooperative in-kernel Omega generation request (project(): k-tiled Omega generated by the
+// mainloop's epilogue warps instead of a separate gen_omega launch)
+struct OmGen {
+    uint64_t seed;
+    uint32_t stream_id;
+    int dist;
+    uint32_t thr;
+    int64_t row0;           // spec row of local row 0 (multiple of 4)
+    uint32_t* flags;        // ceil(k/64) zero-initialised ready flags
+};
+
 // Omega multicast default (pairs per cluster) when tune->omega_mcast == 0 and the shape allows it
 constexpr int kAutoMcast = 1;
 
@@ -335,7 +347,7 @@ struct AView {
 shg_status_t run_shgemm(int64_t m, int64_t n, int64_t k, const AView& av, const uint16_t* Om, int64_t ldo,
                         float* Y, int64_t ldc, const shg_tune_t* tune, void* ws, size_t ws_bytes, int* nonfinite,
                         cudaStream_t stream, const float* B32 = nullptr, int64_t sbk = 0, int64_t sbn = 0,
-                        bool om_tiled = false) {
+                        bool om_tiled = false, const OmGen* og = nullptr) {
     const bool tcec = B32 != nullptr;
     if (om_tiled && (tcec || (tune && tune->tc != SHG_TC_FP16))) return SHG_ERR_INVALID_VALUE;
     if (m == 0 || n == 0) return SHG_OK;
@@ -453,6 +465,21 @@ shg_status_t run_shgemm(int64_t m, int64_t n, int64_t k, const AView& av, const 
     kp.a_rowpair = rowpair ? 1 : 0;
     kp.b_lo_col = static_cast<int32_t>(pl.noff);
     kp.om_tiled = om_tiled ? 1 : 0;
+    const bool gen = og != nullptr;
+    if (gen) {   // the caller checked om_gen_ok() on this plan
+        if (!om_tiled || pl.pair || pl.tf32 || tcec || pl.n_tiles != 1 || pl.bn > kOmGenMaxBn ||
+            static_cast<int64_t>(pl.m_tiles) * pl.splits > pl.grid)
+            return finish(SHG_ERR_INVALID_VALUE);
+        SHG_CUDA(cudaMemsetAsync(og->flags, 0, static_cast<size_t>(pl.num_kb) * 4, stream));
+        kp.om_gen = 1;
+        kp.om_dist = og->dist;
+        kp.om_stream = og->stream_id;
+        kp.om_thr = og->thr;
+        kp.om_seed = og->seed;
+        kp.om_q0 = og->row0 / 4;
+        kp.om_buf = const_cast<uint16_t*>(Om);
+        kp.om_flags = og->flags;
+    }
     kp.dbg = tune ? static_cast<uint32_t>(tune->debug_flags) : 0u;
     kp.prof = tune ? reinterpret_cast<long long*>(tune->prof) : nullptr;
     if (pl.splits > 1) {
@@ -469,7 +496,8 @@ shg_status_t run_shgemm(int64_t m, int64_t n, int64_t k, const AView& av, const 
         kp.vec_store = (aligned16(Y) && ldc % 4 == 0) ? 1 : 0;
         kp.nonfinite = nonfinite;
     }
-    shg_status_t st = pl.np == 2 ? dispatch_tc_f16_mc2(pl.bn, av.mmajor, mapA, mapB0, mapB1, kp, pl.grid, stream)
+    shg_status_t st = gen ? dispatch_tc_f16_gen(pl.bn, av.mmajor, mapA, mapB0, mapB1, kp, pl.grid, stream)
+                      : pl.np == 2 ? dispatch_tc_f16_mc2(pl.bn, av.mmajor, mapA, mapB0, mapB1, kp, pl.grid, stream)
                       : pl.np == 4 ? dispatch_tc_f16_mc4(pl.bn, av.mmajor, mapA, mapB0, mapB1, kp, pl.grid, stream)
                       : tcec      ? dispatch_tc_tcec(pl.bn, av.mmajor, pl.pair, mapA, mapB0, mapB1, kp, pl.grid, stream)
                       : pl.tf32 ? dispatch_tc_tf32(pl.bn, av.mmajor, pl.pair, mapA, mapB0, mapB1, kp, pl.grid, stream)
@@ -483,6 +511,20 @@ shg_status_t run_shgemm(int64_t m, int64_t n, int64_t k, const AView& av, const 
         if (e != cudaSuccess) return finish(cuda_fail(e, "splitk_reduce_kernel"));
     }
     return finish(SHG_OK);
+}
+
+// In-kernel Omega generation for project(): off by default — measured slower
+// than the separate generator on cfg3 (1.00 / 0.94 / 0.83 ms vs 0.86 / 0.84 / 0.85 per mode,
+// DESIGN.md §9); switched on per process by shg_set_inkernel_omega(1) or SHG_OMGEN=1.
+std::atomic<int> g_omgen{-1};
+bool omgen_enabled() {
+    int v = g_omgen.load(std::memory_order_relaxed);
+    if (v < 0) {
+        const char* e = std::getenv("SHG_OMGEN");
+        v = (e && e[0] == '1') ? 1 : 0;
+        g_omgen.store(v, std::memory_order_relaxed);
+    }
+    return v == 1;
 }
 
 uint32_t sparse_threshold(int dist, int64_t k_total) {
@@ -741,6 +783,7 @@ size_t shg_project_workspace_size_ex(int ndim, const int64_t* dims, int mode, in
     const int64_t M = dims[mode];
     // Omega: k-tiled (FP16) or column-major (TF32) — n * round64(K) halves covers both
     size_t bytes = static_cast<size_t>((n * ((K + 63) / 64 * 64) * 2 + 255) / 256 * 256);
+    bytes += static_cast<size_t>(up256((K + 63) / 64 * 4));       // in-kernel generation flags
     const bool needs_copy = !(mode == 0 || S == 1 || (S % shg::kBK == 0 && S % 4 == 0));
     if (needs_copy) bytes += static_cast<size_t>((M * ((K + 3) / 4 * 4) * 4 + 255) / 256 * 256);
     shg_tune_t tt{};
@@ -782,6 +825,8 @@ shg_status_t project_shard(const float* A, int ndim, const int64_t* dims, int mo
     const int64_t ldo = (K + 7) / 8 * 8;
     uint16_t* Om = reinterpret_cast<uint16_t*>(ws);
     size_t off = static_cast<size_t>((n * ((K + 63) / 64 * 64) * 2 + 255) / 256 * 256);
+    uint32_t* gen_flags = reinterpret_cast<uint32_t*>(ws + off);
+    off += static_cast<size_t>(up256((K + 63) / 64 * 4));
     // SHGEMM-FP16 streams Omega in the k-tiled layout: an unfolding's K reaches 2^20 (cfg3), where
     // each column-major 64-k box would visit n rows 2 MiB apart (measured: the Omega stream, not A,
     // bounded mode 0 at 0.90 ms; 0.69 ms without it)
@@ -821,18 +866,33 @@ shg_status_t project_shard(const float* A, int ndim, const int64_t* dims, int mo
     const bool plain_view = (av.P == 1 && av.S == K);
     om_tiled = tc == SHG_TC_FP16 && aligned16(av.A) && av.row_stride % 4 == 0 && av.slab % 4 == 0 &&
                (plain_view || av.S % shg::kBK == 0);
-    shg_status_t st = om_tiled
-                          ? gen_omega_f16_tiled(K, n, seed, dist, static_cast<uint32_t>(mode), omega_row0, k_total, Om,
-                                                stream)
-                          : gen_omega_f16_ex(K, n, seed, dist, static_cast<uint32_t>(mode), omega_row0, k_total, Om,
-                                             ldo, stream);
-    if (st != SHG_OK) return finish(st);
-    void* sk = ws + off;
-    const size_t sk_bytes = need - off;
     shg_tune_t tt{};
     tt.tc = tc;
+    // Optionally (shg_set_inkernel_omega) Omega is generated INSIDE the projection kernel when every
+    // tile of the plan is resident at once (one tile per CTA) and the tiles are single CTAs of
+    // BN <= 192: the m_tiles CTAs that share a k range each generate 1/m_tiles of its Omega tiles
+    // with their epilogue warps (no separate gen_omega launch, no Omega traffic before the GEMM)
+    bool om_gen = false;
+    if (om_tiled && omega_row0 % 4 == 0 && omgen_enabled()) {
+        const Plan pl = make_plan(M, n, K, true, &tt, std::max(1, dev_info().sms));
+        om_gen = pl.path == 0 && !pl.pair && pl.n_tiles == 1 && pl.bn <= kOmGenMaxBn &&
+                 static_cast<int64_t>(pl.m_tiles) * pl.splits <= pl.grid;
+    }
+    shg_status_t st = SHG_OK;
+    if (!om_gen) {
+        st = om_tiled ? gen_omega_f16_tiled(K, n, seed, dist, static_cast<uint32_t>(mode), omega_row0, k_total, Om,
+                                            stream)
+                      : gen_omega_f16_ex(K, n, seed, dist, static_cast<uint32_t>(mode), omega_row0, k_total, Om,
+                                         ldo, stream);
+        if (st != SHG_OK) return finish(st);
+    } else if (dist == SHG_DIST_VERYSPARSE && k_total < 1) {
+        return finish(SHG_ERR_INVALID_VALUE);
+    }
+    const OmGen og{seed, static_cast<uint32_t>(mode), dist, sparse_threshold(dist, k_total), omega_row0, gen_flags};
+    void* sk = ws + off;
+    const size_t sk_bytes = need - off;
     st = run_shgemm(M, n, K, av, Om, ldo, W, ldw, &tt, sk_bytes ? sk : nullptr, sk_bytes, nullptr, s, nullptr, 0, 0,
-                    om_tiled);
+                    om_tiled, om_gen ? &og : nullptr);
     return finish(st);
 }
 
@@ -987,6 +1047,8 @@ int shg_device_supported(void) {
     if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0) return 0;
     return dev_info().ok ? 1 : 0;
 }
+
+void shg_set_inkernel_omega(int on) { g_omgen.store(on ? 1 : 0, std::memory_order_relaxed); }
 
 const char* shg_version(void) { return "shgemm-b200 0.1.0 sm_100a"; }
 

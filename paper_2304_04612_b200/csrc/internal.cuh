@@ -50,11 +50,11 @@ inline bool valid_bn(int bn) {
     return false;
 }
 
-template <int BN, bool MMAJOR, bool PAIR, bool TF32, bool TCEC = false, int NP = 1>
+template <int BN, bool MMAJOR, bool PAIR, bool TF32, bool TCEC = false, int NP = 1, bool OMGEN = false>
 shg_status_t launch_tc(const CUtensorMap& mapA, const CUtensorMap& mapB0, const CUtensorMap& mapB1,
                        const shg::KParams& kp, int grid, cudaStream_t stream) {
     using CF = shg::Cfg<BN, PAIR, TF32, TCEC>;
-    auto kern = shg::shgemm_sm100_kernel<BN, MMAJOR, PAIR, TF32, TCEC, NP>;
+    auto kern = shg::shgemm_sm100_kernel<BN, MMAJOR, PAIR, TF32, TCEC, NP, OMGEN>;
     static std::once_flag flags[64];
     int dev = 0;
     cudaGetDevice(&dev);
@@ -140,6 +140,10 @@ shg_status_t dispatch_tc_tf32(int bn, bool mmajor, bool pair, const CUtensorMap&
                               const CUtensorMap& b1, const shg::KParams& kp, int grid, cudaStream_t s);
 shg_status_t dispatch_tc_tcec(int bn, bool mmajor, bool pair, const CUtensorMap& a, const CUtensorMap& b0,
                               const CUtensorMap& b1, const shg::KParams& kp, int grid, cudaStream_t s);
+// SHGEMM-FP16 single CTAs with cooperative in-kernel Omega generation (tc_f16_gen.cu), BN <= 192
+shg_status_t dispatch_tc_f16_gen(int bn, bool mmajor, const CUtensorMap& a, const CUtensorMap& b0,
+                                 const CUtensorMap& b1, const shg::KParams& kp, int grid, cudaStream_t s);
+constexpr int kOmGenMaxBn = 192;
 // SHGEMM-FP16 CTA pairs with Omega multicast across np = 2 (tc_f16_mc2.cu) or 4 (tc_f16_mc4.cu) pairs
 shg_status_t dispatch_tc_f16_mc2(int bn, bool mmajor, const CUtensorMap& a, const CUtensorMap& b0,
                                  const CUtensorMap& b1, const shg::KParams& kp, int grid, cudaStream_t s);

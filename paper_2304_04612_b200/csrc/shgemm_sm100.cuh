@@ -36,6 +36,7 @@
 #include <cstdint>
 #include <cstdio>
 #include <cuda.h>
+#include "omega.cuh"
 #include "ptx.cuh"
 #include "split.cuh"
 
@@ -68,6 +69,18 @@ struct KParams {
     int32_t vec_store;      // out rows 16-B aligned and ldo_out % 4 == 0
     int32_t b_lo_col;       // TCEC: column (n) coordinate of dB_low in the B tensor maps (B_low at 0)
     int32_t om_tiled;       // Omega in the k-tiled layout (3-D maps {64, n_pad, k/64}; SHGEMM-FP16 only)
+    // Cooperative in-kernel Omega (om_gen = 1; single CTAs, one tile per CTA, n_tiles == 1): the
+    // epilogue warps of the CTA (m_blk, s) generate the k-tiles t of split s with
+    // (t - first tile of s) % m_tiles == m_blk into om_buf (k-tiled layout) and release flag[t];
+    // the Omega stager acquires flag[t] before its TMA. Every tile is generated once, by one of the
+    // m_tiles CTAs that read it.
+    int32_t om_gen;
+    int32_t om_dist;
+    uint32_t om_stream, om_thr;
+    uint64_t om_seed;
+    int64_t om_q0;          // Philox block of local row 0 (global row / 4; rows are 4-aligned)
+    uint16_t* om_buf;
+    uint32_t* om_flags;
     int* nonfinite;         // optional flag (set to 1 on any non-finite output)
     uint32_t dbg;           // diagnostics: bit0 skip promotion loads, bit1 skip split math, bit2 skip MMAs,
                             //              bit3 skip the Omega TMA (results are wrong when dbg != 0)
@@ -342,6 +355,55 @@ __device__ __forceinline__ void add2_rn(float& a, float& b, float c, float d) {
 #define ADD_PAIR(a, b, c, d) add2_rn((a), (b), (c), (d))
 #endif
 
+// ------------------------------------------------------------------ cooperative Omega (om_gen)
+constexpr int kOmGenLookahead = 16;   // 64-k tiles generated ahead of the epilogue's current chunk
+
+__device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, 256;" ::: "memory"); }
+
+// 64-k tile t of the k-tiled Omega (rows 64t..64t+63 of this operand, all n columns) by the 256
+// epilogue threads (tid 0..255): OMEGA_SPEC blocks q = om_q0 + 16t + ql; rows >= k written as 0.
+__device__ __forceinline__ void gen_omega_tile(const KParams& p, int64_t t, int tid) {
+    const omega::Keys keys = omega::philox_keys(p.om_seed);
+    uint16_t* tile = p.om_buf + t * p.n * 64;
+    const int nb = 16 * static_cast<int>(p.n);
+    for (int b = tid; b < nb; b += 256) {
+        const int ql = b & 15;
+        const int64_t j = b >> 4;
+        const int64_t r0 = t * 64 + 4 * ql;
+        uint2 v = make_uint2(0u, 0u);
+        if (r0 < p.k) {
+            uint16_t o[4];
+            omega::omega4(keys, p.om_stream, p.om_dist, p.om_thr, static_cast<uint64_t>(p.om_q0 + t * 16 + ql),
+                          static_cast<uint32_t>(j), o);
+#pragma unroll
+            for (int u = 1; u < 4; ++u)
+                if (r0 + u >= p.k) o[u] = 0;
+            v.x = static_cast<uint32_t>(o[0]) | (static_cast<uint32_t>(o[1]) << 16);
+            v.y = static_cast<uint32_t>(o[2]) | (static_cast<uint32_t>(o[3]) << 16);
+        }
+        *reinterpret_cast<uint2*>(tile + j * 64 + 4 * ql) = v;
+    }
+    // the tile is read by other CTAs' TMA (async proxy): order these generic writes before the release
+    asm volatile("fence.proxy.async.global;" ::: "memory");
+}
+
+__device__ __forceinline__ void release_flag(uint32_t* f) {
+    __threadfence();
+    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(f), "r"(1u) : "memory");
+}
+
+// wait until flag f is set (bounded: a lost flag traps instead of hanging), then order the
+// following async-proxy (TMA) reads after the acquire
+__device__ __forceinline__ void acquire_flag(const uint32_t* f) {
+    uint32_t v, spins = 0;
+    for (;;) {
+        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(f) : "memory");
+        if (v != 0) break;
+        if (++spins == (1u << 26)) asm volatile("trap;");
+    }
+    asm volatile("fence.proxy.async.global;" ::: "memory");
+}
+
 // MMAJOR = false: A is K-major (row-major m x k, or a 3-D K-major view of an unfolding); each stage
 //                 is two TMA boxes of 32 k x 128 rows.
 // MMAJOR = true : A is M-major (element (i, l) at A[l * lda + i], e.g. the last-mode unfolding of a
@@ -357,7 +419,10 @@ __device__ __forceinline__ void add2_rn(float& a, float& b, float c, float d) {
 //                 of chunk c is loaded by pair (c*KC + t) % NP into the same half of every pair, so
 //                 Omega's L2 reads drop NP-fold (the power-cap lever). Chunk slots are
 //                 released to all pairs (ch_empty counts NP commits).
-template <int BN, bool MMAJOR, bool PAIR, bool TF32 = false, bool TCEC = false, int NP = 1>
+// OMGEN         : cooperative in-kernel Omega (KParams::om_gen; single CTAs, SHGEMM-FP16, k-tiled Omega,
+//                 one tile per CTA): compiled only into the instantiations project() uses for it, so
+//                 the other kernels' epilogues carry no generator registers.
+template <int BN, bool MMAJOR, bool PAIR, bool TF32 = false, bool TCEC = false, int NP = 1, bool OMGEN = false>
 __global__ void __launch_bounds__(kThreads, 1)
 shgemm_sm100_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB0,
                     const __grid_constant__ CUtensorMap mapB1, const KParams p) {
@@ -389,6 +454,7 @@ shgemm_sm100_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_const
     const uint32_t warp = warp_id();
     const uint32_t lane = threadIdx.x & 31u;
     static_assert(NP == 1 || (PAIR && (NP == 2 || NP == 4)), "Omega multicast needs CTA pairs");
+    static_assert(!OMGEN || (!PAIR && !TF32 && !TCEC && BN <= 192), "in-kernel Omega: single-CTA SHGEMM-FP16");
     constexpr int CL = PAIR ? 2 * NP : 1;                         // CTAs per cluster
     const uint32_t crank_cl = PAIR ? cluster_ctarank() : 0u;
     const uint32_t crank = crank_cl & 1u;                         // rank in the pair: 0 = leader (issues the MMAs)
@@ -588,14 +654,32 @@ shgemm_sm100_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_const
         uint32_t stage = 0;
         long long w_full = 0, t_store = 0;
         const bool skip_ld = (p.dbg & 1u) != 0;
+        const int etid = static_cast<int>(threadIdx.x) - kEpiWarp0 * 32;   // 0..255
         for (int tile = cta_of_tile; tile < num_tiles; tile += tile_stride) {
             int m_blk, s, n_blk, kb0, kb1;
             coords(tile, m_blk, s, n_blk);
             kb_range(s, p, kb0, kb1);
+            // cooperative Omega (p.om_gen): this CTA generates the tiles kb0s + m_blk + i * m_tiles of
+            // its split, each before the epilogue reaches the chunk kOmGenLookahead tiles earlier
+            // (a fixed schedule, uniform over the 8 warps: deadlock-free by induction over chunks)
+            const int64_t kb0s = kb_global(kb0, s, p);
+            int64_t gen_next = kb0s + m_blk;
+            const int64_t gen_end = OMGEN ? kb0s + (kb1 - kb0) : 0;
+            auto gen_upto = [&](int64_t limit) {
+                if constexpr (!OMGEN) return;
+                while (gen_next < gen_end && gen_next < limit) {
+                    gen_omega_tile(p, gen_next, etid);
+                    epi_bar();
+                    if (etid == 0) release_flag(p.om_flags + gen_next);
+                    gen_next += p.m_tiles;
+                }
+            };
+            gen_upto(kb0s + kOmGenLookahead);
             float acc[NACC];
 #pragma unroll
             for (int i = 0; i < NACC; ++i) acc[i] = 0.0f;
             for (int kb = kb0; kb < kb1; kb += CF::KC, ++stage) {   // one promotion per K_c chunk
+                gen_upto(kb_global(kb, s, p) + CF::KC + kOmGenLookahead);
 #pragma unroll
                 for (int part = 0; part < NQ; ++part) {
                     if (!mine(part)) continue;
@@ -634,6 +718,7 @@ shgemm_sm100_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_const
                     }
                 }
             }
+            gen_upto(gen_end);
             // ---- store the tile rows owned by this thread (its half of every part's columns)
             const long long ts0 = clock64();
             const int64_t row = static_cast<int64_t>(m_blk) * CF::kTileM + static_cast<int64_t>(crank) * kBM + 32 * q +
@@ -740,6 +825,7 @@ shgemm_sm100_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_const
                                 // NP > 1: one pair per stage loads it for all pairs (multicast)
                                 if (NP > 1 && static_cast<uint32_t>((chunk_ctr * KC + t) % NP) != pp) continue;
                                 const int kcoord = kb_global(kb + t, s, p) * kBK;
+                                if constexpr (OMGEN) acquire_flag(p.om_flags + kcoord / kBK);   // generated in-kernel
                                 // FP16: one 128-B box row = 64 k; TF32: two k-halves of 32 k
 #pragma unroll
                                 for (int hh = 0; hh < (TF32 ? 2 : 1); ++hh) {

@@ -456,3 +456,47 @@ def test_row_shards_concatenate_to_unsharded_bitwise(shg, G):
         torch.cuda.synchronize()
         assert torch.equal(Yg, Y[r0:r0 + rows]), g
     assert len(crcs) == 1
+
+
+@pytest.mark.parametrize("dims,mode,n", [((512, 64, 128), 0, 64), ((512, 64, 128), 1, 48), ((512, 64, 128), 2, 32),
+                                         ((300, 40, 100), 0, 64), ((96, 2048, 8), 1, 16)])
+def test_project_inkernel_omega_bit_exact(shg, orc, dims, mode, n):
+    """project() generates Omega_(mode) inside the mainloop (epilogue warps, flags per 64-k tile)
+    when the plan allows it: the Omega it leaves in the caller's workspace is bit-identical to
+    gen_omega_f16_tiled (and the oracle), and W meets the bars."""
+    from oracle import pipelines as opl
+    T = synth.gaussian(int(np.prod(dims)), 1, seed=13).reshape(dims)
+    Tc = cuda(T)
+    ws = torch.zeros(shg.project_workspace_size(list(dims), mode, n), dtype=torch.uint8, device="cuda")
+    shg.set_inkernel_omega(True)
+    try:
+        launches = shg.launch_count()
+        W = shg.project(Tc, mode, n, seed=4, workspace=ws)
+        torch.cuda.synchronize()
+        assert shg.launch_count() - launches == 2          # mainloop + split-K reduce: no gen_omega launch
+    finally:
+        shg.set_inkernel_omega(False)
+    K = int(np.prod(dims)) // dims[mode]
+    nb = n * ((K + 63) // 64) * 64
+    om_ws = to_np(ws[:2 * nb]).view(np.uint16)
+    om_ref = to_np(shg.gen_omega_tiled(K, n, seed=4, stream_id=mode)).view(np.uint16)
+    np.testing.assert_array_equal(om_ws, om_ref)
+    Ai = np.ascontiguousarray(opl.unfold(T, mode))
+    check_bars(orc, Ai, orc.omega_f16(K, n, seed=4, stream_id=mode), to_np(W))
+
+
+def test_project_inkernel_omega_equals_separate_generation(shg, tmp_path):
+    """W with in-kernel Omega (SHG_OMGEN=1) == W with the separate generator, bit for bit."""
+    import subprocess
+    import sys
+    code = ("import sys, numpy as np, torch; sys.path.insert(0, %r); import paper_2304_04612_b200 as shg, synth;"
+            "T = torch.from_numpy(synth.gaussian(512*64*128, 1, seed=13).reshape(512, 64, 128)).cuda();"
+            "np.save(sys.argv[1], np.stack([shg.project(T, md, 64, seed=4).cpu().numpy()[:64] for md in range(3)]))"
+            % os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    outs = []
+    for flag in ("1", "0"):           # SHG_OMGEN sets the process default of shg_set_inkernel_omega
+        path = str(tmp_path / f"w{flag}.npy")
+        env = dict(os.environ, SHG_OMGEN=flag)
+        subprocess.run([sys.executable, "-c", code, path], check=True, env=env, timeout=300)
+        outs.append(np.load(path))
+    np.testing.assert_array_equal(outs[0], outs[1])
