@@ -1,0 +1,25 @@
+"""Small calls of every kernel family for compute-sanitizer (memcheck / racecheck / synccheck)."""
+import sys
+
+import torch
+
+sys.path.insert(0, '.')
+import paper_2304_04612_b200 as shg  # noqa: E402
+
+g = torch.Generator(device="cuda").manual_seed(0)
+A = torch.randn(600, 700, device="cuda", generator=g)
+for n in (32, 130, 272):
+    Om = shg.gen_omega(700, n, seed=1)
+    shg.shgemm(A, Om)
+    shg.shgemm(A, Om, tc="tf32")
+    shg.shgemm(A, Om, tune={"split_k": 3})
+    shg.tcec_sgemm(A, torch.randn(700, n, device="cuda", generator=g))
+shg.shgemm_at(A, shg.gen_omega(600, 64, seed=2))          # A (600 x 700) read as the M-major At of a 700 x 600
+T = torch.randn(40, 64, 96, device="cuda", generator=g)
+for mode in range(3):
+    shg.project(T, mode, 16)
+shg.set_inkernel_omega(True)
+shg.project(T, 0, 16)
+shg.set_inkernel_omega(False)
+torch.cuda.synchronize()
+print("sanitize-small ok")
