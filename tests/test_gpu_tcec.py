@@ -94,7 +94,8 @@ def test_identity_a_reconstructs_split_of_b(shg, orc):
 
 
 @pytest.mark.parametrize("m,k,n", [(512, 512, 32), (1000, 2048, 272), (256, 4096, 64), (130, 777, 200),
-                                   (4096, 256, 256), (64, 16384, 64)])
+                                   (4096, 256, 256), (64, 16384, 64), (700, 1000, 300), (128, 512, 272),
+                                   (640, 333, 288)])
 @pytest.mark.parametrize("la,lb", [(0, 0), (1, 1)])
 def test_bars_gaussian(shg, orc, m, k, n, la, lb):
     rng = np.random.default_rng(m * 7 + n)
