@@ -196,6 +196,15 @@ shg_status_t gen_omega_f16_ex(int64_t k, int64_t n, uint64_t seed, int dist, uin
                               int64_t row0, int64_t k_total, uint16_t *Omega, int64_t ldo,
                               shg_stream_t stream);
 
+/* project() with Omega_(mode) supplied by the caller, already generated in the k-tiled layout by
+ * gen_omega_f16_tiled(K, n, seed, dist, stream_id = mode, ...) with K = prod_{j != mode} dims[j] —
+ * so the generation can run earlier / on another stream (the RSVD/RP-HOSVD harness overlaps it with
+ * the previous mode's QR). SHGEMM-FP16; needs the tcgen05 path (16-B aligned A view), otherwise
+ * SHG_ERR_INVALID_VALUE. Workspace as project(). */
+shg_status_t project_omega(const float *A, int ndim, const int64_t *dims, int mode, int64_t n,
+                           const uint16_t *Omega_tiled, float *W, int64_t ldw, void *workspace,
+                           size_t workspace_bytes, shg_stream_t stream);
+
 /* gen_omega_f16_ex into the K-TILED layout that project() streams: rows i of Omega are grouped in
  * tiles of 64 (t = i / 64), each tile stored as n contiguous 128-byte rows (one per column j):
  * element (i, j) at Omega[(i / 64) * n * 64 + j * 64 + i % 64]. Omega holds ceil(k/64) * n * 64

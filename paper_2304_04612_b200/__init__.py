@@ -79,6 +79,7 @@ def lib():
             L.shg_project_workspace_size_ex.argtypes = [i32, vp, i32, i64, i32]
             L.project_shard.argtypes = [vp, i32, vp, i32, i64, u64, i32, i32, i64, i64, vp, i64, vp, sz, vp]
             L.gen_omega_f16_tiled.argtypes = [i64, i64, u64, i32, u32, i64, i64, vp, vp]
+            L.project_omega.argtypes = [vp, i32, vp, i32, i64, vp, vp, i64, vp, sz, vp]
             L.shgemm_tiled.argtypes = [i64, i64, i64, vp, i64, vp, vp, i64, ctypes.POINTER(Tune), vp, sz, vp, vp]
             L.shg_project_workspace_size_ex.restype = sz
             L.shg_debug_split_tf32.argtypes = [vp, i64, vp, vp, vp]
@@ -103,7 +104,7 @@ def lib():
             for name in ("shgemm", "shgemm_ex", "shgemm_at", "shgemm_host", "shg_plan", "gen_omega_f16", "gen_omega_f16_ex", "project",
                          "shg_debug_split", "shg_synth_f32", "shg_probe_umma", "shgemm_tf32", "project_ex",
                          "shg_debug_split_tf32", "tcec_sgemm", "tcec_sgemm_ex", "tcec_plan", "project_shard",
-                         "gen_omega_f16_tiled", "shgemm_tiled"):
+                         "gen_omega_f16_tiled", "shgemm_tiled", "project_omega"):
                 getattr(L, name).restype = i32
             _lib = L
     return _lib
@@ -347,11 +348,12 @@ def project_workspace_size(dims, mode: int, n: int, tc="fp16") -> int:
 
 
 def project(T: torch.Tensor, mode: int, n: int, seed: int = 0, dist="gaussian", out=None, workspace=None,
-            stream=None, tc="fp16", omega_row0: int = 0, k_total: int = 0) -> torch.Tensor:
+            stream=None, tc="fp16", omega_row0: int = 0, k_total: int = 0, omega=None) -> torch.Tensor:
     """W = A'_(mode) . Omega_(mode) (Alg 2 line 2) for a C-contiguous FP32 tensor,
     by SHGEMM-FP16 (tc='fp16') or SHGEMM-TF32 (tc='tf32'). For a slab of a larger tensor
     (K-sharding) pass the slab's first global unfolding column as omega_row0 and the full column
-    count as k_total (C ABI `project_shard`)."""
+    count as k_total (C ABI `project_shard`). omega: a precomputed k-tiled Omega_(mode)
+    (gen_omega_tiled(K, n, seed, dist, stream_id=mode); C ABI `project_omega`)."""
     if T.dtype != torch.float32 or not T.is_contiguous():
         raise ValueError("T must be a contiguous float32 tensor")
     dims = list(T.shape)
@@ -360,6 +362,10 @@ def project(T: torch.Tensor, mode: int, n: int, seed: int = 0, dist="gaussian", 
         out = torch.empty((M, n), dtype=torch.float32, device=T.device)
     d = (ctypes.c_int64 * len(dims))(*dims)
     ws_bytes = 0 if workspace is None else workspace.numel() * workspace.element_size()
+    if omega is not None:
+        _check(lib().project_omega(_p(T), len(dims), d, mode, n, _p(omega), _p(out), out.stride(0), _p(workspace),
+                                   ws_bytes, _stream(stream)), "project_omega")
+        return out
     _check(lib().project_shard(_p(T), len(dims), d, mode, n, seed, _dist(dist), _tc(tc), omega_row0, k_total,
                                _p(out), out.stride(0), _p(workspace), ws_bytes, _stream(stream)), "project_shard")
     return out

@@ -796,9 +796,12 @@ size_t shg_project_workspace_size(int ndim, const int64_t* dims, int mode, int64
     return shg_project_workspace_size_ex(ndim, dims, mode, n, SHG_TC_FP16);
 }
 
-shg_status_t project_shard(const float* A, int ndim, const int64_t* dims, int mode, int64_t n, uint64_t seed,
-                           int dist, int tc, int64_t omega_row0, int64_t k_total, float* W, int64_t ldw,
-                           void* workspace, size_t workspace_bytes, shg_stream_t stream) {
+namespace {
+// project_shard's body; om_given != nullptr: Omega_(mode) supplied by the caller in the k-tiled
+// layout (project_omega), no generation
+shg_status_t project_impl(const float* A, int ndim, const int64_t* dims, int mode, int64_t n, uint64_t seed,
+                          int dist, int tc, int64_t omega_row0, int64_t k_total, float* W, int64_t ldw,
+                          void* workspace, size_t workspace_bytes, shg_stream_t stream, const uint16_t* om_given) {
     if (!A || !dims || !W || ndim < 1 || ndim > 8 || mode < 0 || mode >= ndim || n < 0 || ldw < n)
         return SHG_ERR_INVALID_VALUE;
     if (omega_row0 < 0) return SHG_ERR_INVALID_VALUE;
@@ -879,7 +882,11 @@ shg_status_t project_shard(const float* A, int ndim, const int64_t* dims, int mo
                  static_cast<int64_t>(pl.m_tiles) * pl.splits <= pl.grid;
     }
     shg_status_t st = SHG_OK;
-    if (!om_gen) {
+    if (om_given) {                  // caller's k-tiled Omega: the tcgen05 path must read it
+        if (!om_tiled) return finish(SHG_ERR_INVALID_VALUE);
+        om_gen = false;
+        Om = const_cast<uint16_t*>(om_given);
+    } else if (!om_gen) {
         st = om_tiled ? gen_omega_f16_tiled(K, n, seed, dist, static_cast<uint32_t>(mode), omega_row0, k_total, Om,
                                             stream)
                       : gen_omega_f16_ex(K, n, seed, dist, static_cast<uint32_t>(mode), omega_row0, k_total, Om,
@@ -894,6 +901,22 @@ shg_status_t project_shard(const float* A, int ndim, const int64_t* dims, int mo
     st = run_shgemm(M, n, K, av, Om, ldo, W, ldw, &tt, sk_bytes ? sk : nullptr, sk_bytes, nullptr, s, nullptr, 0, 0,
                     om_tiled, om_gen ? &og : nullptr);
     return finish(st);
+}
+}  // namespace
+
+shg_status_t project_shard(const float* A, int ndim, const int64_t* dims, int mode, int64_t n, uint64_t seed,
+                           int dist, int tc, int64_t omega_row0, int64_t k_total, float* W, int64_t ldw,
+                           void* workspace, size_t workspace_bytes, shg_stream_t stream) {
+    return project_impl(A, ndim, dims, mode, n, seed, dist, tc, omega_row0, k_total, W, ldw, workspace,
+                        workspace_bytes, stream, nullptr);
+}
+
+shg_status_t project_omega(const float* A, int ndim, const int64_t* dims, int mode, int64_t n,
+                           const uint16_t* Omega_tiled, float* W, int64_t ldw, void* workspace, size_t workspace_bytes,
+                           shg_stream_t stream) {
+    if (!Omega_tiled) return SHG_ERR_INVALID_VALUE;
+    return project_impl(A, ndim, dims, mode, n, 0, SHG_DIST_GAUSSIAN, SHG_TC_FP16, 0, 0, W, ldw, workspace,
+                        workspace_bytes, stream, Omega_tiled);
 }
 
 shg_status_t project_ex(const float* A, int ndim, const int64_t* dims, int mode, int64_t n, uint64_t seed, int dist,

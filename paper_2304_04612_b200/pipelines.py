@@ -20,7 +20,7 @@ import contextlib
 
 import torch
 
-from . import gen_omega, project, project_workspace_size, shgemm, synth, tcec_sgemm
+from . import gen_omega, gen_omega_tiled, project, project_workspace_size, shgemm, synth, tcec_sgemm
 
 
 @contextlib.contextmanager
@@ -189,13 +189,30 @@ def rp_hosvd(T: torch.Tensor, ranks, seed: int = 0, dist="gaussian", projection=
     t = _Timer(timing)
     Qs, bads = [], []
     ws = None
+    oms, ready = [None] * len(ranks), [None] * len(ranks)
     if projection == "shgemm":   # one persistent scratch buffer (Omega_(i) + split-K partials) for all modes
         nbytes = max(project_workspace_size(list(T.shape), i, J) for i, J in enumerate(ranks))
         ws = torch.empty(nbytes, dtype=torch.uint8, device=T.device)
+        if T.is_contiguous() and T.data_ptr() % 16 == 0:
+            # every Omega_(i) generated up front on a side stream (k-tiled, as project() streams it):
+            # the generator (ALU-bound) fills the gaps of the latency-bound QRs between projections
+            side = torch.cuda.Stream(device=T.device)
+            side.wait_stream(torch.cuda.current_stream())
+            numel = T.numel()
+            with torch.cuda.stream(side):
+                for i, J in enumerate(ranks):
+                    oms[i] = gen_omega_tiled(numel // T.shape[i], J, seed=seed, dist=dist, stream_id=i,
+                                             device=T.device)
+                    ready[i] = torch.cuda.Event()
+                    ready[i].record(side)
     with _fp32_matmul():
         for i, J in enumerate(ranks):
             t.mark("2_projection")
-            if projection == "shgemm":
+            if projection == "shgemm" and oms[i] is not None:
+                torch.cuda.current_stream().wait_event(ready[i])
+                oms[i].record_stream(torch.cuda.current_stream())
+                W = project(T, i, J, workspace=ws, omega=oms[i])
+            elif projection == "shgemm":
                 W = project(T, i, J, seed=seed, dist=dist, workspace=ws)
             elif projection == "sgemm":
                 Ui = unfold(T, i)

@@ -500,3 +500,15 @@ def test_project_inkernel_omega_equals_separate_generation(shg, tmp_path):
         subprocess.run([sys.executable, "-c", code, path], check=True, env=env, timeout=300)
         outs.append(np.load(path))
     np.testing.assert_array_equal(outs[0], outs[1])
+
+
+@pytest.mark.parametrize("dims,mode", [((64, 96, 128), 0), ((64, 96, 128), 1), ((64, 96, 128), 2)])
+def test_project_omega_equals_project(shg, dims, mode):
+    """project_omega (caller's k-tiled Omega) == project (Omega generated inside), bit for bit."""
+    g = torch.Generator(device="cuda").manual_seed(mode)
+    T = torch.randn(*dims, device="cuda", generator=g)
+    K = T.numel() // dims[mode]
+    W1 = shg.project(T, mode, 24, seed=8)
+    W2 = shg.project(T, mode, 24, omega=shg.gen_omega_tiled(K, 24, seed=8, stream_id=mode))
+    torch.cuda.synchronize()
+    assert torch.equal(W1, W2)
