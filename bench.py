@@ -98,8 +98,10 @@ class ClockSampler:
         mx = [float(s[2]) for s in self.samples if s[2].replace(".", "").isdigit()]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         reasons = sorted({names[i] for s in self.samples for i in range(4) if len(s) > 5 + i and s[5 + i].strip() == "Active"})
+        pw = [float(s[3]) for s in self.samples if s[3].replace(".", "").isdigit()]
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.samples)}
+                "reasons": reasons, "samples": len(self.samples),
+                "power_w": statistics.median(pw) if pw else None}
 
 
 def cpu_baseline(m, k, n, budget_s=10.0):
