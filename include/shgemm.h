@@ -215,16 +215,17 @@ shg_status_t project_omega(const float *A, int ndim, const int64_t *dims, int mo
 shg_status_t gen_omega_f16_tiled(int64_t k, int64_t n, uint64_t seed, int dist, uint32_t stream_id, int64_t row0,
                                  int64_t k_total, uint16_t *Omega, shg_stream_t stream);
 
-/* shgemm_ex (SHGEMM-FP16 only: tune->tc must be SHG_TC_FP16) reading a k-tiled Omega written by
- * gen_omega_f16_tiled(k, n, ...). Needs the tcgen05 fast path (A 16-B aligned, lda % 4 == 0);
- * otherwise SHG_ERR_INVALID_VALUE (the CUDA-core fallback reads column-major Omega only). */
+/* shgemm_ex (tune->tc: SHG_TC_FP16, or SHG_TC_TF32 which widens the tiles to a 32-k-tiled FP32
+ * copy) reading a k-tiled Omega written by gen_omega_f16_tiled(k, n, ...). Needs the tcgen05 fast
+ * path (A 16-B aligned, lda % 4 == 0); otherwise SHG_ERR_INVALID_VALUE (the CUDA-core fallback
+ * reads column-major Omega only). */
 shg_status_t shgemm_tiled(int64_t m, int64_t n, int64_t k, const float *A, int64_t lda, const uint16_t *Omega_tiled,
                           float *Y, int64_t ldc, const shg_tune_t *tune, void *workspace, size_t workspace_bytes,
                           int *nonfinite_flag, shg_stream_t stream);
 
 /* ---------------------------------------------------------------------------------------------
- * project — W[I_mode x n] = A'_(mode) . Omega_(mode) (Alg 2 line 2). With SHGEMM-FP16 and
- * an aligned A view, Omega_(mode) is generated in the k-tiled layout (gen_omega_f16_tiled).
+ * project — W[I_mode x n] = A'_(mode) . Omega_(mode) (Alg 2 line 2). With an aligned A
+ * view, Omega_(mode) is generated in the k-tiled layout (gen_omega_f16_tiled).
  *   A        device, C-order tensor with ndim dims (1 <= ndim <= 8), dims[i] >= 1.
  *   mode     0 <= mode < ndim. The unfolding's column index is the C-order linear index over the
  *            remaining modes in ascending order (== torch.movedim(A, mode, 0).reshape(I_mode, -1)).

@@ -143,6 +143,19 @@ bool encode_b(CUtensorMap* map, const uint16_t* Om, int64_t k, int64_t n, int64_
               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// k-tiled FP32 (TF32) copy of Omega (widen_omega_tiled_kernel): dims {32, n, ceil(k/32)}, box {32 k, rows, 1}
+bool encode_b32_tiled(CUtensorMap* map, const float* Om32, int64_t k, int64_t n, int rows) {
+    EncodeFn fn = encode_fn();
+    if (!fn) return false;
+    cuuint64_t dims[3] = {32, static_cast<cuuint64_t>(n), static_cast<cuuint64_t>((k + 31) / 32)};
+    cuuint64_t strides[2] = {128, static_cast<cuuint64_t>(n) * 128};
+    cuuint32_t box[3] = {32, static_cast<cuuint32_t>(rows), 1};
+    cuuint32_t estr[3] = {1, 1, 1};
+    return fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(Om32), dims, strides, box, estr,
+              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 // k-tiled Omega (gen_omega_f16_tiled): dims {64, n, ceil(k/64)}, box {64 k, rows, 1} — each 64-k
 // box is ONE contiguous run of rows x 128 B (the column-major box visits rows 128 B at a time, ldo*2
 // bytes apart: 2 MiB apart for an RP-HOSVD unfolding with k = 2^20, one DRAM page per visit)
@@ -294,7 +307,7 @@ Plan make_plan(int64_t m, int64_t n, int64_t k, bool fast_ok, const shg_tune_t* 
     }
     if (pl.tf32) {   // Omega widened once to TF32 (exact) for the tensor cores' smem operand
         pl.ldo32 = (k + 3) / 4 * 4;
-        pl.om_bytes = pl.ldo32 * n * 4;
+        pl.om_bytes = (k + 31) / 32 * 32 * n * 4;   // column-major (ldo32) or 32-k tiles
     }
     if (pl.tcec) {   // [B_low | pad | dB_low | pad], each n_tiles * BN columns (pads zeroed)
         pl.noff = static_cast<int64_t>(pl.n_tiles) * pl.bn;
@@ -349,7 +362,7 @@ shg_status_t run_shgemm(int64_t m, int64_t n, int64_t k, const AView& av, const 
                         cudaStream_t stream, const float* B32 = nullptr, int64_t sbk = 0, int64_t sbn = 0,
                         bool om_tiled = false, const OmGen* og = nullptr) {
     const bool tcec = B32 != nullptr;
-    if (om_tiled && (tcec || (tune && tune->tc != SHG_TC_FP16))) return SHG_ERR_INVALID_VALUE;
+    if (om_tiled && tcec) return SHG_ERR_INVALID_VALUE;
     if (m == 0 || n == 0) return SHG_OK;
     if (k == 0) {
         SHG_CUDA(cudaMemset2DAsync(Y, ldc * sizeof(float), 0, n * sizeof(float), m, stream));
@@ -444,10 +457,16 @@ shg_status_t run_shgemm(int64_t m, int64_t n, int64_t k, const AView& av, const 
         encb_ok = encode_b(&mapB0, H, k, 2 * pl.noff, pl.ldh, rows0) && encode_b(&mapB1, H, k, 2 * pl.noff, pl.ldh, rows1);
     } else if (pl.tf32) {
         float* om32 = reinterpret_cast<float*>(wsb + up256(pl.sk_bytes));
-        shg::widen_omega_kernel<<<grid_for(k * n, 256), 256, 0, stream>>>(Om, k, n, ldo, om32, pl.ldo32);
+        if (om_tiled) {
+            shg::widen_omega_tiled_kernel<<<grid_for((k + 31) / 32 * 32 * n, 256), 256, 0, stream>>>(Om, k, n, om32);
+        } else {
+            shg::widen_omega_kernel<<<grid_for(k * n, 256), 256, 0, stream>>>(Om, k, n, ldo, om32, pl.ldo32);
+        }
         g_launches.fetch_add(1, std::memory_order_relaxed);
         if (cudaGetLastError() != cudaSuccess) return finish(cuda_fail(cudaErrorLaunchFailure, "widen_omega_kernel"));
-        encb_ok = encode_b32(&mapB0, om32, k, n, pl.ldo32, rows0) && encode_b32(&mapB1, om32, k, n, pl.ldo32, rows1);
+        encb_ok = om_tiled ? encode_b32_tiled(&mapB0, om32, k, n, rows0) && encode_b32_tiled(&mapB1, om32, k, n, rows1)
+                           : encode_b32(&mapB0, om32, k, n, pl.ldo32, rows0) &&
+                                 encode_b32(&mapB1, om32, k, n, pl.ldo32, rows1);
     } else if (om_tiled) {
         encb_ok = encode_b_tiled(&mapB0, Om, k, n, rows0) && encode_b_tiled(&mapB1, Om, k, n, rows1);
     } else {
@@ -636,7 +655,8 @@ shg_status_t shgemm_tiled(int64_t m, int64_t n, int64_t k, const float* A, int64
     if (m == 0 || n == 0) return SHG_OK;
     if (!Y || ldc < n) return SHG_ERR_INVALID_VALUE;
     if (k > 0 && (!A || !Omega_tiled || lda < k)) return SHG_ERR_INVALID_VALUE;
-    if (tune && ((tune->bn > 0 && !valid_bn(tune->bn)) || tune->tc != SHG_TC_FP16)) return SHG_ERR_INVALID_VALUE;
+    if (tune && ((tune->bn > 0 && !valid_bn(tune->bn)) || (tune->tc != SHG_TC_FP16 && tune->tc != SHG_TC_TF32)))
+        return SHG_ERR_INVALID_VALUE;
     AView av{A, k, 1, lda, lda * std::max<int64_t>(m, 1)};
     return run_shgemm(m, n, k, av, Omega_tiled, 8, Y, ldc, tune, workspace, workspace_bytes, nonfinite_flag,
                       reinterpret_cast<cudaStream_t>(stream), nullptr, 0, 0, true);
@@ -867,7 +887,7 @@ shg_status_t project_impl(const float* A, int ndim, const int64_t* dims, int mod
     }
     // the tcgen05 path will run (same predicate as run_shgemm's fast path) -> k-tiled Omega
     const bool plain_view = (av.P == 1 && av.S == K);
-    om_tiled = tc == SHG_TC_FP16 && aligned16(av.A) && av.row_stride % 4 == 0 && av.slab % 4 == 0 &&
+    om_tiled = aligned16(av.A) && av.row_stride % 4 == 0 && av.slab % 4 == 0 &&
                (plain_view || av.S % shg::kBK == 0);
     shg_tune_t tt{};
     tt.tc = tc;
@@ -876,7 +896,7 @@ shg_status_t project_impl(const float* A, int ndim, const int64_t* dims, int mod
     // BN <= 192: the m_tiles CTAs that share a k range each generate 1/m_tiles of its Omega tiles
     // with their epilogue warps (no separate gen_omega launch, no Omega traffic before the GEMM)
     bool om_gen = false;
-    if (om_tiled && omega_row0 % 4 == 0 && omgen_enabled()) {
+    if (om_tiled && tc == SHG_TC_FP16 && omega_row0 % 4 == 0 && omgen_enabled()) {
         const Plan pl = make_plan(M, n, K, true, &tt, std::max(1, dev_info().sms));
         om_gen = pl.path == 0 && !pl.pair && pl.n_tiles == 1 && pl.bn <= kOmGenMaxBn &&
                  static_cast<int64_t>(pl.m_tiles) * pl.splits <= pl.grid;

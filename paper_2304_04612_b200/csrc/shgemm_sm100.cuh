@@ -290,11 +290,11 @@ __device__ __forceinline__ void tma_load_omega_mc(void* smem_dst, const CUtensor
 // Omega tile load; in a pair the transaction bytes land on the leader's (even CTA's) barrier.
 // tiled: Omega in the k-tiled layout (KParams::om_tiled), a 3-D map {64, n, k/64}: the box of a
 // 64-k stage is one contiguous run of rows x 128 B instead of one 128-B visit per column.
-template <bool PAIR>
+template <bool PAIR, bool TF32 = false>
 __device__ __forceinline__ void tma_load_omega(void* smem_dst, const CUtensorMap* map, uint64_t* bar, int32_t c0,
                                                int32_t c1, uint64_t policy, bool tiled = false) {
-    if (tiled) {
-        const int32_t t0 = c0 & 63, t2 = c0 >> 6;
+    if (tiled) {   // FP16: 64-k tiles; TF32 (the exact FP32 widening): 32-k tiles
+        const int32_t t0 = TF32 ? (c0 & 31) : (c0 & 63), t2 = TF32 ? (c0 >> 5) : (c0 >> 6);
         if constexpr (PAIR) {
             asm volatile(
                 "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
@@ -802,7 +802,7 @@ shgemm_sm100_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_const
             // [n0 + W + crank*R1, +R1) (pair: each CTA holds its half of every part)
             if (elect_one()) {
                 const uint64_t pol = policy_evict_last();
-                const bool tiled = !TF32 && p.om_tiled != 0;
+                const bool tiled = p.om_tiled != 0;
                 uint32_t cs = 0, pc = 0;
                 uint32_t chunk_ctr = 0;
                 long long w = 0;
@@ -841,16 +841,16 @@ shgemm_sm100_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_const
                                             tma_load_omega_mc(d2 + CF::R0 * 128, &mapB1, &ch_ready[cs], kc,
                                                               nb0 + W + static_cast<int>(crank) * CF::R1, half_mask, pol);
                                         } else if constexpr (PAIR) {
-                                            tma_load_omega<PAIR>(d2, &mapB0, &ch_ready[cs], kc,
+                                            tma_load_omega<PAIR, TF32>(d2, &mapB0, &ch_ready[cs], kc,
                                                                  nb0 + static_cast<int>(crank) * CF::R0, pol, tiled);
-                                            tma_load_omega<PAIR>(d2 + CF::R0 * 128, &mapB1, &ch_ready[cs], kc,
+                                            tma_load_omega<PAIR, TF32>(d2 + CF::R0 * 128, &mapB1, &ch_ready[cs], kc,
                                                                  nb0 + W + static_cast<int>(crank) * CF::R1, pol, tiled);
                                         } else if constexpr (CF::WIDE) {   // > 256 rows: one box per part
-                                            tma_load_omega<PAIR>(d2, &mapB0, &ch_ready[cs], kc, nb0, pol, tiled);
-                                            tma_load_omega<PAIR>(d2 + CF::R0 * 128, &mapB1, &ch_ready[cs], kc, nb0 + W, pol,
+                                            tma_load_omega<PAIR, TF32>(d2, &mapB0, &ch_ready[cs], kc, nb0, pol, tiled);
+                                            tma_load_omega<PAIR, TF32>(d2 + CF::R0 * 128, &mapB1, &ch_ready[cs], kc, nb0 + W, pol,
                                                                  tiled);
                                         } else {   // the two parts are contiguous rows: one box of BN rows (mapB0)
-                                            tma_load_omega<PAIR>(d2, &mapB0, &ch_ready[cs], kc, nb0, pol, tiled);
+                                            tma_load_omega<PAIR, TF32>(d2, &mapB0, &ch_ready[cs], kc, nb0, pol, tiled);
                                         }
                                     }
                                 }

@@ -61,4 +61,19 @@ __global__ void widen_omega_kernel(const uint16_t* __restrict__ Om, int64_t k, i
     }
 }
 
+// The same widening from the k-tiled FP16 Omega (64-row tiles: (r/64)*n*64 + j*64 + r%64) into a
+// k-tiled FP32 copy of 32-row tiles ((r/32)*n*32 + j*32 + r%32: one SW128 TMA box row per TF32
+// k-half); rows k .. 32*ceil(k/32)-1 of the last tile are 0.
+__global__ void widen_omega_tiled_kernel(const uint16_t* __restrict__ Om, int64_t k, int64_t n,
+                                         float* __restrict__ Om32) {
+    const int64_t kp = (k + 31) / 32 * 32;
+    const int64_t total = kp * n;
+    for (int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; t < total;
+         t += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int64_t j = t / kp, r = t - j * kp;
+        const float v = r < k ? __half2float(__ushort_as_half(Om[(r >> 6) * n * 64 + j * 64 + (r & 63)])) : 0.0f;
+        Om32[(r >> 5) * n * 32 + j * 32 + (r & 31)] = v;
+    }
+}
+
 }  // namespace shg

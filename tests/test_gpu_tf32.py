@@ -166,3 +166,25 @@ def test_tf32_deterministic_and_plan(shg):
     assert torch.equal(Y1, Y2)
     p = shg.plan(700, 200, 3000, tc="tf32")
     assert p["tc"] == 1 and p["kernels"] >= 2 and p["workspace_bytes"] >= 3000 * 200 * 4
+
+
+@pytest.mark.parametrize("m,k,n", [(1024, 4096, 64), (300, 1000, 256), (512, 776, 272)])
+def test_shgemm_tiled_tf32_equals_column_major(shg, m, k, n):
+    """SHGEMM-TF32 reading a k-tiled Omega (widened to 32-k FP32 tiles) == the column-major path."""
+    g = torch.Generator(device="cuda").manual_seed(m)
+    A = torch.randn(m, k, device="cuda", generator=g)
+    y_cm = shg.shgemm(A, shg.gen_omega(k, n, seed=6), tc="tf32")
+    y_t = shg.shgemm_tiled(A, shg.gen_omega_tiled(k, n, seed=6), n, tune={"tc": "tf32"})
+    torch.cuda.synchronize()
+    assert torch.equal(y_cm, y_t)
+
+
+def test_project_tf32_large_k_bars(shg, orc):
+    """project(tc='tf32') on an unfolding with K = 2^18 (k-tiled Omega path), sampled rows vs oracle."""
+    from oracle import pipelines as opl
+    dims = (256, 512, 512)
+    T = synth.gaussian(int(np.prod(dims)), 1, seed=21).reshape(dims)
+    W = to_np(shg.project(cuda(T), 0, 64, seed=3, tc="tf32"))
+    rows = [0, 7, 100, 255]
+    A0 = np.ascontiguousarray(opl.unfold(T, 0)[rows])
+    check_bars(orc, A0, orc.omega_f16(A0.shape[1], 64, seed=3, stream_id=0), W[rows])
