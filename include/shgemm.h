@@ -92,9 +92,9 @@ typedef struct {
     int32_t tc;          /* shg_tc_t: SHG_TC_FP16 (0, default) or SHG_TC_TF32; selects the kernel, not a
                             tuning: the results differ (TF32 keeps |a| >= 65520 finite) */
     int32_t omega_mcast; /* CTA pairs per cluster sharing each Omega stage by TMA multicast (SHGEMM-FP16
-                            CTA pairs only): 0 auto, 1 off, 2 or 4; needs the pair-tile count to be a
-                            multiple (else SHG_ERR_INVALID_VALUE when forced; auto falls back to 1).
-                            Results are bitwise identical for every value. */
+                            CTA pairs, BN <= 256): 0 auto (= 1), 1 off, 2, 3 or 4 (a ragged last group of
+                            pair tiles runs dummy tiles); SHG_ERR_INVALID_VALUE when forced on a plan
+                            without pairs. Results are bitwise identical for every value. */
     /* Diagnostics: device int64[grid * 16] per-CTA wait-cycle counters (layout in
      * csrc/shgemm_sm100.cuh, enum ProfSlot), or NULL. */
     int64_t *prof;

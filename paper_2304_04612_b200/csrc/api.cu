@@ -272,14 +272,14 @@ Plan make_plan(int64_t m, int64_t n, int64_t k, bool fast_ok, const shg_tune_t* 
     }
     pl.pair = pair_ok(pl.bn) && want_pair;
     const int mc = tune ? tune->omega_mcast : 0;   // 0 auto, 1 off, 2 / 4 pairs per cluster
-    if (mc < 0 || mc == 3 || mc > 4) { pl.path = -1; return pl; }
+    if (mc < 0 || mc > 4) { pl.path = -1; return pl; }
     const int tile_m = pl.pair ? 2 * shg::kBM : shg::kBM;
     const int slots = pl.pair ? std::max(1, sms / 2) : sms;     // concurrent tiles
     pl.m_tiles = static_cast<int>((m + tile_m - 1) / tile_m);
     if (mc >= 2) {
-        if (!pl.pair || pl.tf32 || pl.tcec || wide_bn(pl.bn) || pl.m_tiles % mc) { pl.path = -1; return pl; }
+        if (!pl.pair || pl.tf32 || pl.tcec || wide_bn(pl.bn)) { pl.path = -1; return pl; }
         pl.np = mc;
-    } else if (mc == 0 && pl.pair && !pl.tf32 && !pl.tcec && !wide_bn(pl.bn) && kAutoMcast > 1 && pl.m_tiles % kAutoMcast == 0 &&
+    } else if (mc == 0 && pl.pair && !pl.tf32 && !pl.tcec && !wide_bn(pl.bn) && kAutoMcast > 1 &&
                pl.m_tiles >= kAutoMcast * 8) {
         pl.np = kAutoMcast;
     }
@@ -517,6 +517,7 @@ shg_status_t run_shgemm(int64_t m, int64_t n, int64_t k, const AView& av, const 
     }
     shg_status_t st = gen ? dispatch_tc_f16_gen(pl.bn, av.mmajor, mapA, mapB0, mapB1, kp, pl.grid, stream)
                       : pl.np == 2 ? dispatch_tc_f16_mc2(pl.bn, av.mmajor, mapA, mapB0, mapB1, kp, pl.grid, stream)
+                      : pl.np == 3 ? dispatch_tc_f16_mc3(pl.bn, av.mmajor, mapA, mapB0, mapB1, kp, pl.grid, stream)
                       : pl.np == 4 ? dispatch_tc_f16_mc4(pl.bn, av.mmajor, mapA, mapB0, mapB1, kp, pl.grid, stream)
                       : tcec      ? dispatch_tc_tcec(pl.bn, av.mmajor, pl.pair, mapA, mapB0, mapB1, kp, pl.grid, stream)
                       : pl.tf32 ? dispatch_tc_tf32(pl.bn, av.mmajor, pl.pair, mapA, mapB0, mapB1, kp, pl.grid, stream)

@@ -149,5 +149,7 @@ shg_status_t dispatch_tc_f16_mc2(int bn, bool mmajor, const CUtensorMap& a, cons
                                  const CUtensorMap& b1, const shg::KParams& kp, int grid, cudaStream_t s);
 shg_status_t dispatch_tc_f16_mc4(int bn, bool mmajor, const CUtensorMap& a, const CUtensorMap& b0,
                                  const CUtensorMap& b1, const shg::KParams& kp, int grid, cudaStream_t s);
+shg_status_t dispatch_tc_f16_mc3(int bn, bool mmajor, const CUtensorMap& a, const CUtensorMap& b0,
+                                 const CUtensorMap& b1, const shg::KParams& kp, int grid, cudaStream_t s);
 
 }  // namespace shg_api

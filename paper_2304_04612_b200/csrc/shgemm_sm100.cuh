@@ -415,7 +415,7 @@ __device__ __forceinline__ void acquire_flag(const uint32_t* f) {
 // TF32          : SHGEMM-TF32 (Cfg's header); mapB0/B1 then describe the FP32 (TF32) copy of Omega.
 // TCEC          : TCEC-SGEMM (Cfg's header): two B tiles per stage, three MMA groups per chunk.
 // NP            : CTA pairs per cluster (PAIR only). NP > 1 runs NP pairs on NP consecutive m-blocks in
-//                 lockstep (host: m_tiles % NP == 0) and MULTICASTS every Omega stage to them: stage t
+//                 lockstep (a ragged last group runs dummy tiles) and MULTICASTS every Omega stage to them: stage t
 //                 of chunk c is loaded by pair (c*KC + t) % NP into the same half of every pair, so
 //                 Omega's L2 reads drop NP-fold (the power-cap lever). Chunk slots are
 //                 released to all pairs (ch_empty counts NP commits).
@@ -453,7 +453,7 @@ shgemm_sm100_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_const
 
     const uint32_t warp = warp_id();
     const uint32_t lane = threadIdx.x & 31u;
-    static_assert(NP == 1 || (PAIR && (NP == 2 || NP == 4)), "Omega multicast needs CTA pairs");
+    static_assert(NP == 1 || (PAIR && NP >= 2 && NP <= 4), "Omega multicast needs CTA pairs");
     static_assert(!OMGEN || (!PAIR && !TF32 && !TCEC && BN <= 192), "in-kernel Omega: single-CTA SHGEMM-FP16");
     constexpr int CL = PAIR ? 2 * NP : 1;                         // CTAs per cluster
     const uint32_t crank_cl = PAIR ? cluster_ctarank() : 0u;
@@ -502,7 +502,9 @@ shgemm_sm100_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_const
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
 
-    const int num_tiles = (p.m_tiles / NP) * p.splits * p.n_tiles;
+    // m-groups of NP pair tiles; a ragged last group runs dummy tiles past m (TMA zero-fills their
+    // A rows, the epilogue's row < m mask drops their stores) so every pair of a cluster stays in step
+    const int num_tiles = ((p.m_tiles + NP - 1) / NP) * p.splits * p.n_tiles;
     const long long t_kernel0 = clock64();
 
     if (warp < kNumSplitWarps) {

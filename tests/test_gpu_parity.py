@@ -359,7 +359,7 @@ def test_a_box_layouts(shg, orc, m, k, n, tune):
 
 @pytest.mark.parametrize("m,k,n,mmajor", [(2048, 1000, 256, False), (4096, 640, 144, False), (1024, 3000, 200, True),
                                           (2048, 512, 130, False)])
-@pytest.mark.parametrize("mc", [2, 4])
+@pytest.mark.parametrize("mc", [2, 3, 4])
 def test_omega_multicast_bitwise_identical(shg, orc, m, k, n, mmajor, mc):
     """Omega stages multicast to 2 / 4 CTA pairs of a cluster change only who loads Omega, not the
     arithmetic: Y is bitwise identical to the unicast pair kernel (and meets the bars)."""
@@ -380,9 +380,15 @@ def test_omega_multicast_bitwise_identical(shg, orc, m, k, n, mmajor, mc):
     check_bars(orc, A, omega_bits(Om), to_np(ym))
 
 
-def test_omega_multicast_rejects_ragged_pair_tiles(shg):
-    with pytest.raises(shg.SHGError):
-        shg.plan(3 * 256, 256, 512, {"omega_mcast": 2})     # 3 pair tiles: not a multiple of 2
+def test_omega_multicast_ragged_groups_and_rejections(shg):
+    """A pair-tile count that is not a multiple of the pairs per cluster runs dummy tiles in the
+    last group (zero-filled A rows, masked stores): still bitwise equal; BN = 64 has no pairs."""
+    g = torch.Generator(device="cuda").manual_seed(9)
+    A = torch.randn(5 * 256 + 17, 1000, device="cuda", generator=g)       # 6 pair tiles, ragged rows
+    Om = shg.gen_omega(1000, 256, seed=1)
+    y1 = shg.shgemm(A, Om, tune={"omega_mcast": 1})
+    for mc in (3, 4):
+        assert torch.equal(shg.shgemm(A, Om, tune={"omega_mcast": mc}), y1)
     with pytest.raises(shg.SHGError):
         shg.plan(4096, 64, 512, {"omega_mcast": 2})         # BN = 64: single CTAs, no pairs
 
