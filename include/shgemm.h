@@ -319,7 +319,7 @@ const char *shg_last_error(void);
 /* 1 if the current device can run the tcgen05 path (cc 10.0), else 0. */
 int shg_device_supported(void);
 
-/* Library version, e.g. "shgemm-b200 0.1.0 sm_100a". */
+/* Library version, e.g. "shgemm-b200 0.2.0 sm_100a". */
 const char *shg_version(void);
 
 /* Tensor-core semantics probe: ONE CTA runs tcgen05.mma.cta_group::1.kind::f16

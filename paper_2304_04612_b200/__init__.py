@@ -17,8 +17,10 @@ import threading
 
 import torch
 
-__all__ = ["shgemm", "tcec_sgemm", "gen_omega", "project", "split", "synth", "plan", "launch_count", "lib",
-           "probe_umma", "project_workspace_size", "SHGError", "DISTS"]
+__all__ = ["shgemm", "shgemm_at", "shgemm_tiled", "shgemm_host", "tcec_sgemm", "tcec_plan", "tcec_workspace_size",
+           "gen_omega", "gen_omega_tiled", "project", "project_workspace_size", "set_inkernel_omega", "split",
+           "split_tf32", "synth", "plan", "workspace_size", "launch_count", "device_supported", "version", "lib",
+           "probe_umma", "SHGError", "DISTS"]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libshgemm.so")

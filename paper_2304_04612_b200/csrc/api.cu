@@ -1094,6 +1094,6 @@ int shg_device_supported(void) {
 
 void shg_set_inkernel_omega(int on) { g_omgen.store(on ? 1 : 0, std::memory_order_relaxed); }
 
-const char* shg_version(void) { return "shgemm-b200 0.1.0 sm_100a"; }
+const char* shg_version(void) { return "shgemm-b200 0.2.0 sm_100a"; }
 
 }  // extern "C"
