@@ -86,3 +86,32 @@ def test_fuzz(shg, orc, i):
     # (25% of elements) dominates a naive error that is itself near zero; the
     # elementwise (k/8 + 3) u |A||Omega| bar and the 1e-5 bar still apply
     check_bars(orc, A, ob, to_np(Y), ratio=2.0 if k >= 16 else float("inf"))
+
+
+@pytest.mark.parametrize("i", range(48))
+def test_fuzz_project(shg, orc, i):
+    """Random C-order tensors (2-4 modes, ragged extents) through project(): every unfolding view
+    (mode 0, 3-D K-major, copied middle modes, M-major last mode), k-tiled Omega, the separate or the
+    in-kernel generator, every distribution; W against the oracle bars on the unfolding."""
+    from oracle import pipelines as opl
+    r = np.random.default_rng(5000 + i)
+    nd = int(r.integers(2, 5))
+    dims = tuple(int(x) for x in r.integers(2, 40, size=nd))
+    while int(np.prod(dims)) < 2000:
+        dims = tuple(d * 2 for d in dims)
+    mode = int(r.integers(0, nd))
+    n = int(r.choice([8, 16, 33, 64, 100]))
+    dist = int(r.integers(0, 4))
+    inkernel = bool(r.integers(0, 2))
+    T = r.standard_normal(dims).astype(np.float32)
+    shg.set_inkernel_omega(inkernel)
+    try:
+        W = to_np(shg.project(torch.from_numpy(T).cuda(), mode, n, seed=i, dist=dist))
+    finally:
+        shg.set_inkernel_omega(False)
+    Ai = np.ascontiguousarray(opl.unfold(T, mode))
+    K = Ai.shape[1]
+    ob = orc.omega_f16(K, n, seed=i, dist=dist, stream_id=mode)
+    if not np.any(orc.gemm_y64(Ai, ob)):
+        return
+    check_bars(orc, Ai, ob, W, ratio=2.0 if K >= 16 else float("inf"))
