@@ -9,7 +9,8 @@ Recipes (PAPER.md citations):
   eckart_young_floor  closed forms P:684-691 (A_linear: s_p sqrt(N-p); A_exp: tail sum)
   haar()              Haar orthogonal via QR of a Gaussian with sign fix
   spectrum_matrix()   U diag(s) V^T (slatms replaced); 'hadamard' factors for N=16384
-  alg3_tensor()       Alg 3, padding p, normalised to unit RMS (DESIGN.md reading)
+  alg3_tensor()       Alg 3 (P:760-773), padding p, normalised to unit RMS (DESIGN.md reading);
+                      alg3_tensor_torch() the same draws evaluated on the GPU (bench's 1024^3 input)
   cauchy_like()       A_Cauchy + one A A^T A step so that |a| > 65504
   gaussian/uniform    A ~ N(0,1) or U(0,1)
 """
@@ -129,6 +130,21 @@ def alg3_tensor(dims, ranks, pad: int, seed: int, noise: float = 0.0) -> np.ndar
     if noise:
         G = G + noise * g.standard_normal(G.shape)
     return G.astype(np.float32)
+
+
+def alg3_tensor_torch(dims, ranks, pad: int, seed: int, device="cuda"):
+    """alg3_tensor's construction (same random draws) evaluated with torch in FP64 on `device`, FP32
+    result — for the 1024^3 RP-HOSVD input of the bench (the numpy version takes minutes)."""
+    import torch
+    g = rng(seed)
+    G = torch.as_tensor(g.uniform(-1.0, 1.0, size=tuple(ranks)), dtype=torch.float64, device=device)
+    for i, (I, J) in enumerate(zip(dims, ranks)):
+        Oa = g.uniform(-1.0, 1.0, size=(J, J - pad))
+        Ob = g.uniform(-1.0, 1.0, size=(J - pad, I))
+        M = torch.as_tensor(Oa @ Ob, dtype=torch.float64, device=device)
+        G = torch.movedim(torch.tensordot(G, M, dims=([i], [0])), -1, i)
+    G = G / torch.sqrt(torch.mean(G * G))
+    return G.float()
 
 
 def cauchy_like(N: int, seed: int) -> np.ndarray:
