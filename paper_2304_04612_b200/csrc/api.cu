@@ -372,7 +372,7 @@ shg_status_t run_shgemm(int64_t m, int64_t n, int64_t k, const AView& av, const 
     if (!d.ok) return SHG_ERR_UNSUPPORTED_DEVICE;
     const bool plain = (av.P == 1 && av.S == k);
     const bool fast_ok = aligned16(av.A) && aligned16(Om) && (av.row_stride % 4 == 0) && (av.slab % 4 == 0) &&
-                         (tcec || ldo % 8 == 0) && (plain || av.S % shg::kBK == 0) && encode_fn() != nullptr &&
+                         (tcec || ldo % 8 == 0) && (plain || av.S % 32 == 0) && encode_fn() != nullptr &&
                          k < (int64_t(1) << 31) && av.S < (int64_t(1) << 31) && m < (int64_t(1) << 31);
     Plan pl = make_plan(m, n, k, fast_ok, tune, d.sms, tcec);
     if (pl.path < 0) return SHG_ERR_INVALID_VALUE;
@@ -411,7 +411,8 @@ shg_status_t run_shgemm(int64_t m, int64_t n, int64_t k, const AView& av, const 
     // every row of a 128-row box sits in its own 2-MiB page (measured on 1024 x 2^20: 1.24 -> 0.79
     // ms); at shorter strides the two-box layout measured 3-15% faster (profiles/r01_ab_abox.jsonl)
     const int a_box = tune ? tune->a_box : 0;     // 0 auto, 1 128-B row visits, 2 256-B row visits
-    const bool rowpair_ok = !av.mmajor && av.S % 32 == 0;
+    // the 4-D box spans two 32-k chunks: inside one slab only if S % 64 == 0 (or a plain matrix)
+    const bool rowpair_ok = !av.mmajor && av.S % 32 == 0 && (plain || av.S % 64 == 0);
     const bool rowpair = rowpair_ok && (a_box == 2 || (a_box == 0 && av.row_stride * 4 >= (int64_t(2) << 20)));
     if (a_box == 2 && !rowpair_ok) return SHG_ERR_INVALID_VALUE;
     const bool enc_ok = av.mmajor ? encode_a_mmajor(&mapA, av.A, m, k, av.row_stride)
@@ -805,7 +806,7 @@ size_t shg_project_workspace_size_ex(int ndim, const int64_t* dims, int mode, in
     // Omega: k-tiled (FP16) or column-major (TF32) — n * round64(K) halves covers both
     size_t bytes = static_cast<size_t>((n * ((K + 63) / 64 * 64) * 2 + 255) / 256 * 256);
     bytes += static_cast<size_t>(up256((K + 63) / 64 * 4));       // in-kernel generation flags
-    const bool needs_copy = !(mode == 0 || S == 1 || (S % shg::kBK == 0 && S % 4 == 0));
+    const bool needs_copy = !(mode == 0 || S == 1 || S % 32 == 0);
     if (needs_copy) bytes += static_cast<size_t>((M * ((K + 3) / 4 * 4) * 4 + 255) / 256 * 256);
     shg_tune_t tt{};
     tt.tc = tc;
@@ -867,7 +868,7 @@ shg_status_t project_impl(const float* A, int ndim, const int64_t* dims, int mod
     AView av{A, K, 1, K, K * M};
     if (mode == 0) {
         av = AView{A, K, 1, K, K * M};
-    } else if (S % shg::kBK == 0 && S % 4 == 0) {
+    } else if (S % 32 == 0) {
         // A[p][r][s] -> unfold[r][p*S + s]: 3-D view {S, M, P}, row stride S, slab stride M*S
         av = AView{A, S, P, S, M * S};
     } else if (S == 1) {
@@ -889,7 +890,7 @@ shg_status_t project_impl(const float* A, int ndim, const int64_t* dims, int mod
     // the tcgen05 path will run (same predicate as run_shgemm's fast path) -> k-tiled Omega
     const bool plain_view = (av.P == 1 && av.S == K);
     om_tiled = aligned16(av.A) && av.row_stride % 4 == 0 && av.slab % 4 == 0 &&
-               (plain_view || av.S % shg::kBK == 0);
+               (plain_view || av.S % 32 == 0);
     shg_tune_t tt{};
     tt.tc = tc;
     // Optionally (shg_set_inkernel_omega) Omega is generated INSIDE the projection kernel when every

@@ -790,8 +790,16 @@ shgemm_sm100_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_const
                             // 4-D map {32, S/32, M, P}: one box of 128 rows x (2 x 32 k), row major
                             tma_load_4d(dst, &mapA, &a_full[sa], 0, c0 >> 5, m0, c2, pol);
                         } else {
+                            // two 32-k halves; the second continues in the next slab when the
+                            // view's contiguous run S ends mid-stage (S % 32 == 0 unfoldings). Past
+                            // the last k it stays in dim 0 (zero-filled there: a box wholly outside
+                            // the OUTER dimension never completed its transaction bytes)
+                            const int64_t kk2 = kk + 32;
+                            const bool wrap = kk2 < p.k && (c0 + 32) >= p.k_inner;
                             tma_load_3d(dst, &mapA, &a_full[sa], c0, m0, c2, pol);
-                            tma_load_3d(dst + kA32StageBytes / 2, &mapA, &a_full[sa], c0 + 32, m0, c2, pol);
+                            tma_load_3d(dst + kA32StageBytes / 2, &mapA, &a_full[sa],
+                                        wrap ? static_cast<int>(kk2 % p.k_inner) : c0 + 32, m0,
+                                        wrap ? static_cast<int>(kk2 / p.k_inner) : c2, pol);
                         }
                         advance(sa, pa, SA);
                     }

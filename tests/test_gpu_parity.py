@@ -518,3 +518,16 @@ def test_project_omega_equals_project(shg, dims, mode):
     W2 = shg.project(T, mode, 24, omega=shg.gen_omega_tiled(K, 24, seed=8, stream_id=mode))
     torch.cuda.synchronize()
     assert torch.equal(W1, W2)
+
+
+@pytest.mark.parametrize("dims,mode", [((24, 40, 96), 1), ((10, 24, 32), 1), ((6, 7, 160, 32), 2), ((50, 8, 96), 0)])
+def test_project_slab_views_s_multiple_of_32(shg, orc, dims, mode):
+    """Middle-mode unfoldings whose contiguous run S is a multiple of 32 but not of 64 are read in
+    place (a 64-k stage's second 32-k half continues in the next slab), no copy: bars vs oracle."""
+    from oracle import pipelines as opl
+    T = synth.gaussian(int(np.prod(dims)), 1, seed=31).reshape(dims)
+    S = int(np.prod(dims[mode + 1:]))
+    assert S % 32 == 0
+    W = to_np(shg.project(cuda(T), mode, 40, seed=2))
+    Ai = np.ascontiguousarray(opl.unfold(T, mode))
+    check_bars(orc, Ai, orc.omega_f16(Ai.shape[1], 40, seed=2, stream_id=mode), W)
