@@ -467,6 +467,17 @@ def measure_extras(shg, torch, hbm, tc16_burst, tc_ratio, reps=10):
                 "bound": "tensor" if tc16_burst * tc_ratio / 2.0 < fl / by * hbm / 1e3 else "hbm"}
 
     out = {}
+    # context for the power cap: cuBLAS bf16 on cfg4's own shape (one 16-bit product, half the A bytes)
+    m4, k4, n4 = 4194304, 4096, 256
+    Ab = torch.randn(m4, k4, device="cuda", dtype=torch.bfloat16)
+    Bb = torch.randn(k4, n4, device="cuda", dtype=torch.bfloat16)
+    Cb = torch.empty(m4, n4, device="cuda", dtype=torch.bfloat16)
+    ms = med_ms(lambda: torch.matmul(Ab, Bb, out=Cb))
+    out["cublas_bf16_cfg4_shape"] = {"ms": ms, "tensor_tflops": 2.0 * m4 * n4 * k4 / ms / 1e9,
+                                     "note": "torch.matmul bf16, A 4194304x4096 . B 4096x256: ONE product on 16-bit A; "
+                                             "SHGEMM's tensor work is two products on FP32 A (compare its 4mnk/t)"}
+    del Ab, Bb, Cb
+    torch.cuda.empty_cache()
     for name, (m, k, n) in {"cfg2_projection": (16384, 16384, 272), "cfg5_n64": (32768, 32768, 64),
                             "cfg5_n1024": (32768, 32768, 1024)}.items():
         A = shg.synth("gauss", DATA_SEED, 0x101, m, k)
