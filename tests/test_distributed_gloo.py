@@ -106,7 +106,7 @@ def _run(world, job):
     return res
 
 
-@pytest.mark.parametrize("world", [2, 3])
+@pytest.mark.parametrize("world", [2, 3, 4])
 def test_dist_rsvd_matches_oracle_pipeline(orc, world):
     from oracle import pipelines as opl
     m, n, p, s = 301, 200, 12, 6
