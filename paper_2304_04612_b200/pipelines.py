@@ -107,7 +107,7 @@ def omega_fp32(k: int, n: int, seed: int = 0, stream_id: int = 0, device="cuda")
 
 
 def rsvd(A: torch.Tensor, p: int, s: int = 10, seed: int = 0, dist="gaussian", projection="shgemm",
-         timing: bool = False, gemm: str = "sgemm", factor: str = "cusolver"):
+         timing: bool = False, gemm: str = "sgemm", factor: str = "cusolver", check: bool = True):
     """Alg 1: Y = A Omega; Q = QR(Y); B = Q^T A; (U', S, V) = tSVD(B, p); U = Q U'.
     factor='cusolver' (the paper's: Householder QR and SVD from cuSOLVER) or 'gram' (CholeskyQR2 and
     the FP64 Gram-eigh SVD; needs gemm='tcec' for B^T)."""
@@ -145,9 +145,10 @@ def rsvd(A: torch.Tensor, p: int, s: int = 10, seed: int = 0, dist="gaussian", p
         t.mark("5_QU")
         U = Q @ Uh[:, :p]     # 16384 x 272 x 256: launch-bound either way, left on cuBLAS
         t.mark("end")
-    if bad is not None and int(bad) != 0:     # Gram not positive definite: redo with Householder QR
+    if check and bad is not None and int(bad) != 0:     # Gram not positive definite: redo with Householder QR
         return rsvd(A, p, s, seed, dist, projection, timing, gemm, "cusolver")
-    return {"U": U, "S": S[:p], "V": V, "Q": Q, "times_ms": t.result()}
+    # check=False (CUDA-graph capture: no synchronisation allowed): the caller checks "bad"
+    return {"U": U, "S": S[:p], "V": V, "Q": Q, "times_ms": t.result(), "bad": bad}
 
 
 def reconstruction_error(A, U, S, V) -> float:
@@ -181,7 +182,7 @@ def core_tcec(T: torch.Tensor, Qs) -> torch.Tensor:
 
 
 def rp_hosvd(T: torch.Tensor, ranks, seed: int = 0, dist="gaussian", projection="shgemm", timing=False,
-             gemm: str = "sgemm", factor: str = "cusolver"):
+             gemm: str = "sgemm", factor: str = "cusolver", check: bool = True):
     """Alg 2: for each mode W = A'_(i) Omega_(i) (project, stream_id = mode), Q_i = QR(W);
     g = A x_1 Q_1^T ... x_N Q_N^T. factor='gram': CholeskyQR2 for the QRs."""
     if gemm not in ("sgemm", "tcec") or factor not in ("cusolver", "gram"):
@@ -235,9 +236,10 @@ def rp_hosvd(T: torch.Tensor, ranks, seed: int = 0, dist="gaussian", projection=
             for i, Q in enumerate(Qs):
                 g = mode_product(g, Q, i)
         t.mark("end")
-    if bads and int(sum(bads)) != 0:
+    if check and bads and int(sum(bads)) != 0:
         return rp_hosvd(T, ranks, seed, dist, projection, timing, gemm, "cusolver")
-    return {"core": g, "Q": Qs, "times_ms": t.result()}
+    # check=False (CUDA-graph capture: no synchronisation allowed): the caller checks "bad"
+    return {"core": g, "Q": Qs, "times_ms": t.result(), "bad": sum(bads) if bads else None}
 
 
 def hosvd_error(T, core, Qs) -> float:
