@@ -531,3 +531,32 @@ def test_project_slab_views_s_multiple_of_32(shg, orc, dims, mode):
     W = to_np(shg.project(cuda(T), mode, 40, seed=2))
     Ai = np.ascontiguousarray(opl.unfold(T, mode))
     check_bars(orc, Ai, orc.omega_f16(Ai.shape[1], 40, seed=2, stream_id=mode), W)
+
+
+@pytest.mark.parametrize("m,k,n,tune,mmajor", [(1000, 640, 256, None, False), (1000, 640, 272, None, False),
+                                               (100, 640, 64, None, False), (300, 4096, 32, {"split_k": 4}, False),
+                                               (1000, 640, 128, None, True), (700, 512, 200, {"pair": 2}, True)])
+def test_nonfinite_flag_every_plan(shg, m, k, n, tune, mmajor):
+    """The optional non-finite flag across plan shapes (pairs, wide tiles, single CTAs, split-K
+    reduce, M-major): one A element >= 65520 in one row poisons exactly that row, flag set; a clean
+    A leaves the flag 0."""
+    g = torch.Generator(device="cuda").manual_seed(m + n)
+    A = torch.randn(m, k, device="cuda", generator=g)
+    Om = shg.gen_omega(k, n, seed=1)
+    bad = m // 3
+    for poison in (False, True):
+        if poison:
+            A[bad, k // 2] = 70000.0
+        flag = torch.zeros(1, dtype=torch.int32, device="cuda")
+        if mmajor:
+            Y = shg.shgemm_at(A.t().contiguous(), Om, nonfinite=flag, tune=tune)
+        else:
+            Y = shg.shgemm(A, Om, nonfinite=flag, tune=tune)
+        torch.cuda.synchronize()
+        finite_rows = torch.isfinite(Y).all(dim=1)
+        if poison:
+            assert int(flag.item()) == 1 and not bool(finite_rows[bad])
+            finite_rows[bad] = True
+            assert bool(finite_rows.all())
+        else:
+            assert int(flag.item()) == 0 and bool(finite_rows.all())
