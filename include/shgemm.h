@@ -350,6 +350,15 @@ shg_status_t shg_probe_mma2_rate(int n, int iters, int ts, float *out, int clust
  * of the issuing loop. Timed with events under the power cap it measures tensor work per joule. */
 shg_status_t shg_probe_mma_energy(int n, int parts, int iters, long long *out, int clusters, shg_stream_t stream);
 
+/* Box-Muller probe (OMEGA_SPEC §3.1-3.2, the Gaussian Omega of PAPER.md:448-451): for each of
+ * `count` Philox output words w (device uint32), r[i] = the generator's radius sqrt(-2 ln(((w >> 8) + 1)
+ * 2^-24)) and (c[i], s[i]) = its cos/sin of 2 pi (w >> 8) 2^-24, computed by the SAME device functions
+ * gen_omega* use (device float outputs, caller-owned). Lets a test compare the generator's
+ * transcendental steps with the oracle over all 2^24 codes. count = 0 is a no-op;
+ * SHG_ERR_INVALID_VALUE for count < 0 or NULL pointers. */
+shg_status_t shg_probe_boxmuller(const uint32_t *words, int64_t count, float *r, float *c, float *s,
+                                 shg_stream_t stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -75,6 +75,7 @@ def lib():
             L.orc_num_threads.restype = ctypes.c_int
             L.orc_ln_spec_batch.argtypes = [vp, i64, vp]
             L.orc_sincos_spec_batch.argtypes = [vp, i64, vp, vp]
+            L.orc_radius_spec_batch.argtypes = [vp, i64, vp]
             L.orc_f32_to_f16_batch.argtypes = [vp, i64, vp]
             L.orc_gauss_column_f32.argtypes = [u64, u32, u32, i64, i64, vp]
             _lib = L
@@ -118,6 +119,13 @@ def ln_spec_batch(na: np.ndarray) -> np.ndarray:
     na = np.ascontiguousarray(na, dtype=np.uint32)
     out = np.empty(na.size, dtype=np.float32)
     lib().orc_ln_spec_batch(_ptr(na), na.size, _ptr(out))
+    return out
+
+
+def radius_spec_batch(xa: np.ndarray) -> np.ndarray:
+    xa = np.ascontiguousarray(xa, dtype=np.uint32)
+    out = np.empty(xa.size, dtype=np.float32)
+    lib().orc_radius_spec_batch(_ptr(xa), xa.size, _ptr(out))
     return out
 
 

@@ -435,6 +435,11 @@ void orc_ln_spec_batch(const uint32_t *na, int64_t count, float *out) {
     for (int64_t t = 0; t < count; ++t) out[t] = orc_ln_spec(na[t]);
 }
 
+void orc_radius_spec_batch(const uint32_t *xa, int64_t count, float *out) {
+    #pragma omp parallel for schedule(static)
+    for (int64_t t = 0; t < count; ++t) out[t] = orc_radius_spec(xa[t]);
+}
+
 void orc_sincos_spec_batch(const uint32_t *xb, int64_t count, float *c, float *s) {
     #pragma omp parallel for schedule(static)
     for (int64_t t = 0; t < count; ++t) orc_sincos_spec(xb[t], &c[t], &s[t]);

@@ -93,6 +93,7 @@ def lib():
             L.tcec_sgemm_workspace_size.restype = sz
             L.tcec_plan.argtypes = [i64, i64, i64, ctypes.POINTER(Tune), ctypes.POINTER(Plan)]
             L.shg_launch_count.restype = u64
+            L.shg_probe_boxmuller.argtypes = [vp, i64, vp, vp, vp, vp]
             L.shg_set_inkernel_omega.argtypes = [i32]
             L.shg_set_inkernel_omega.restype = None
             L.shg_last_error.restype = ctypes.c_char_p
@@ -401,6 +402,16 @@ def synth(kind: str, seed: int, stream_id: int, m: int, k: int, row0: int = 0, o
     _check(lib().shg_synth_f32(0 if kind == "gauss" else 1, seed, stream_id, m, k, row0, _p(out),
                                out.stride(0) if m > 1 else max(k, 1), _stream(stream)), "shg_synth_f32")
     return out
+
+
+def probe_boxmuller(words: torch.Tensor, stream=None):
+    """(r, c, s) of the generator's Box-Muller steps on device uint32 Philox words (include/shgemm.h)."""
+    w = words.contiguous()
+    assert w.dtype in (torch.int32, torch.uint32) and w.is_cuda
+    r, c, s = (torch.empty(w.numel(), dtype=torch.float32, device=w.device) for _ in range(3))
+    _check(lib().shg_probe_boxmuller(_p(w), w.numel(), _p(r), _p(c), _p(s), _stream(stream)),
+           "shg_probe_boxmuller")
+    return r, c, s
 
 
 def probe_umma(A16: torch.Tensor, B16: torch.Tensor, D_init: torch.Tensor | None = None, mode: int = 0,

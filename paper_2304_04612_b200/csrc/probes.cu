@@ -380,3 +380,28 @@ extern "C" shg_status_t shg_probe_mma_energy(int n, int parts, int iters, long l
     e = cudaLaunchKernelEx(&cfg, shg::probe_mma_energy_kernel, n, parts, iters, out);
     return e == cudaSuccess ? SHG_OK : SHG_ERR_CUDA;
 }
+
+// Box-Muller probe: the generator's radius and angle functions (omega.cuh) evaluated on given
+// Philox words, so the tests can compare them with the oracle over every 24-bit code.
+#include "omega.cuh"
+namespace shg {
+__global__ void probe_boxmuller_kernel(const uint32_t* __restrict__ words, int64_t count, float* __restrict__ r,
+                                       float* __restrict__ c, float* __restrict__ s) {
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < count; i += int64_t(gridDim.x) * blockDim.x) {
+        const uint32_t w = words[i];
+        float cv, sv;
+        omega::bm_angle(w, cv, sv);
+        r[i] = omega::bm_radius(w);
+        c[i] = cv;
+        s[i] = sv;
+    }
+}
+}  // namespace shg
+
+extern "C" shg_status_t shg_probe_boxmuller(const uint32_t* words, int64_t count, float* r, float* c, float* s,
+                                            shg_stream_t stream) {
+    if (count < 0 || (count > 0 && (!words || !r || !c || !s))) return SHG_ERR_INVALID_VALUE;
+    if (count == 0) return SHG_OK;
+    shg::probe_boxmuller_kernel<<<148 * 8, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(words, count, r, c, s);
+    return cudaGetLastError() == cudaSuccess ? SHG_OK : SHG_ERR_CUDA;
+}

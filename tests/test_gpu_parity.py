@@ -61,6 +61,23 @@ def test_omega_bit_exact_1e8(shg, orc):
 
 
 # ------------------------------------------------------------------------------------------ split
+def test_boxmuller_steps_exhaustive(shg, orc):
+    """The generator's radius and cos/sin (OMEGA_SPEC §3.1-3.2; Gaussian Omega) on
+    every one of the 2^24 codes, bit for bit against the oracle's fixed-operation versions; random
+    low 8 bits (ignored by both) on a second pass."""
+    code = np.arange(1 << 24, dtype=np.uint32)
+    for low in (0, None):
+        w = code << np.uint32(8)
+        if low is None:
+            w = w | np.random.default_rng(3).integers(0, 256, code.size).astype(np.uint32)
+        r, c, s = shg.probe_boxmuller(torch.from_numpy(w.view(np.int32)).cuda())
+        torch.cuda.synchronize()
+        np.testing.assert_array_equal(r.cpu().numpy().view(np.uint32), orc.radius_spec_batch(w).view(np.uint32))
+        oc, os_ = orc.sincos_spec_batch(w)
+        np.testing.assert_array_equal(c.cpu().numpy().view(np.uint32), oc.view(np.uint32))
+        np.testing.assert_array_equal(s.cpu().numpy().view(np.uint32), os_.view(np.uint32))
+
+
 def test_split_exhaustive_all_fp32(shg, orc):
     """Device split (the mainloop's device function) == oracle split on all 2^32 FP32 patterns."""
     chunk = 1 << 28

@@ -57,6 +57,23 @@ def test_radius_extremes(orc):
     assert abs(r_max - math.sqrt(2 * 24 * math.log(2))) < 1e-5
 
 
+def test_radius_spec_all_codes(orc):
+    """r = sqrt(-2 ln u), u = ((xa >> 8) + 1) 2^-24, for every 24-bit code vs binary64 libm
+    (OMEGA_SPEC §3.1, Box-Muller radius of the Gaussian Omega); the batch form
+    agrees with the scalar one and ignores the low 8 bits."""
+    code = np.arange(1 << 24, dtype=np.uint32)
+    r = orc.radius_spec_batch(code << np.uint32(8)).astype(np.float64)
+    ref = np.sqrt(-2.0 * np.log((code.astype(np.float64) + 1.0) * 2.0 ** -24))
+    # ln error <= ulp(L) + 1e-7 (test_ln_spec_all_inputs); sqrt halves the relative error, adds 1 rounding
+    dL = np.spacing(np.float32(1.0)) * np.maximum(ref * ref / 2.0, 1e-30) + 1.0e-7
+    bound = dL / np.maximum(ref, 1e-30) + np.spacing(ref.astype(np.float32)).astype(np.float64)
+    ok = ref > 0
+    assert np.all(np.abs(r - ref)[ok] <= bound[ok] * 1.01), float(np.max((np.abs(r - ref) - bound)[ok]))
+    assert r[-1] == 0.0
+    for i in (0, 1, 77, 1 << 23, (1 << 24) - 2):
+        assert r[i] == orc.radius_spec(int(i) << 8 | 0x5A)
+
+
 def _gauss_sample(orc, count, columns=4, seed=12345, stream=0):
     per = count // columns
     return np.concatenate([orc.gauss_column_f32(seed, stream, j, 0, per) for j in range(columns)])
