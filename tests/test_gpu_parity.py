@@ -307,6 +307,40 @@ def test_config4_full_size_sampled(shg, orc):
     check_bars(orc, Arows, omega_bits(Om), Ys)
 
 
+def test_config5_full_size_sampled(shg, orc):
+    """BASELINE config 5 at full size (A 32768^2 FP32 = 4 GiB) for n = 16 (HBM-bound, split-K),
+    n = 1024 and n = 4096 (tensor-bound, several N tiles): 64 sampled rows each against the oracle."""
+    m = k = 32768
+    A = shg.synth("gauss", 5, 0x105, m, k)
+    rng = np.random.default_rng(5)
+    rows = np.unique(np.concatenate([[0, 255, 256, m - 1], rng.integers(0, m, 60)]))
+    ridx = torch.from_numpy(rows).cuda()
+    Arows = to_np(A[ridx])
+    assert np.array_equal(Arows[:3], orc.synth_rows("gauss", 5, 0x105, rows[:3], k))
+    for n in (16, 1024, 4096):
+        Om = shg.gen_omega(k, n, seed=n)
+        Ys = to_np(shg.shgemm(A, Om)[ridx])
+        check_bars(orc, Arows, omega_bits(Om), Ys)
+        del Om
+
+
+def test_config3_project_full_size_sampled(shg, orc):
+    """BASELINE config 3's projections at full size: a 1024^3 FP32 tensor (4 GiB), W = A_(i) Omega_(i)
+    with n = 64 and K = 2^20 for every mode (mode 0 K-major, mode 1 a 3-D slab view, mode 2 M-major in
+    place), in bench.py's launch configuration; 16 sampled rows of each W against the oracle with the
+    oracle's own Omega_(i) (stream_id = mode)."""
+    I = 1024
+    T = shg.synth("gauss", 3, 0x103, I, I * I).view(I, I, I)
+    rng = np.random.default_rng(3)
+    rows = np.unique(np.concatenate([[0, 127, 128, I - 1], rng.integers(0, I, 12)]))
+    ridx = torch.from_numpy(rows).cuda()
+    for mode in range(3):
+        W = shg.project(T, mode, 64, seed=0)
+        U = to_np(torch.movedim(T, mode, 0)[ridx].reshape(len(rows), -1))
+        ob = orc.omega_f16(I * I, 64, seed=0, stream_id=mode)
+        check_bars(orc, U, ob, to_np(W[ridx]))
+
+
 # ------------------------------------------------------------------------------------------ project
 @pytest.mark.parametrize("dims", [(24, 40, 64), (16, 128, 32), (10, 12, 14)])
 def test_project_all_modes(shg, orc, dims):
