@@ -21,5 +21,17 @@ for mode in range(3):
 shg.set_inkernel_omega(True)
 shg.project(T, 0, 16)
 shg.set_inkernel_omega(False)
+# later paths: Omega multicast (2 / 3 pairs per cluster), wide 288, k-tiled Omega, project slab views
+# with S % 32 == 0 (second half of a stage continues in the next slab), row-sharded Omega, probes
+A2 = torch.randn(1100, 512, device="cuda", generator=g)
+Om2 = shg.gen_omega(512, 256, seed=3)
+for mc in (2, 3):
+    shg.shgemm(A2, Om2, tune={"pair": 1, "omega_mcast": mc})
+shg.shgemm(A2, shg.gen_omega(512, 288, seed=4))
+shg.shgemm_tiled(A2, shg.gen_omega_tiled(512, 200, seed=5), 200)
+T2 = torch.randn(6, 32, 96, device="cuda", generator=g)
+shg.project(T2, 1, 24)
+shg.project(T2, 1, 24, omega_row0=64, k_total=1024)
+shg.probe_boxmuller(torch.arange(1 << 12, device="cuda", dtype=torch.int32) << 20)
 torch.cuda.synchronize()
 print("sanitize-small ok")
