@@ -307,6 +307,34 @@ def test_config4_full_size_sampled(shg, orc):
     check_bars(orc, Arows, omega_bits(Om), Ys)
 
 
+@pytest.mark.parametrize("variant", ["fp16", "split_k", "tf32", "mmajor"])
+def test_int64_indexing_large_m(shg, orc, variant):
+    """m * ldc > 2^31 (12.6M rows x 256 columns of Y) and m * k > 2^31 elements of A: the epilogue's
+    row * ldc, the TMA row coordinates and the synthetic generator's offsets stay 64-bit; rows past
+    2^31 / n and the last tile (ragged) checked against the oracle."""
+    m, k, n = 12_600_001 if variant != "mmajor" else 12_600_004, 192, 256    # M-major: lda % 4 == 0
+    Om = shg.gen_omega(k, n, seed=7)
+    if variant == "mmajor":           # A stored k x m (M-major), rows of the product = columns of At
+        At = shg.synth("gauss", 7, 0x107, k, m)
+        Y = shg.shgemm_at(At, Om)
+        A = At.t()
+    else:
+        A = shg.synth("gauss", 7, 0x107, m, k)
+        Y = shg.shgemm(A, Om, tune={"split_k": 2} if variant == "split_k" else None,
+                       tc="tf32" if variant == "tf32" else "fp16")
+    torch.cuda.synchronize()
+    rows = np.array([0, 1, (1 << 31) // n - 1, (1 << 31) // n, (1 << 31) // n + 1, 11_000_000, m - 257,
+                     m - 2, m - 1])
+    ridx = torch.from_numpy(rows).cuda()
+    Arows = to_np(A[ridx])
+    if variant != "mmajor":
+        assert np.array_equal(Arows, orc.synth_rows("gauss", 7, 0x107, rows, k))
+    Ys = to_np(Y[ridx])
+    del A, Y
+    torch.cuda.empty_cache()
+    check_bars(orc, Arows, omega_bits(Om), Ys)
+
+
 def test_config5_full_size_sampled(shg, orc):
     """BASELINE config 5 at full size (A 32768^2 FP32 = 4 GiB) for n = 16 (HBM-bound, split-K),
     n = 1024 and n = 4096 (tensor-bound, several N tiles): 64 sampled rows each against the oracle."""
