@@ -335,6 +335,21 @@ def test_int64_indexing_large_m(shg, orc, variant):
     check_bars(orc, Arows, omega_bits(Om), Ys)
 
 
+def test_project_tensor_over_2g_elements(shg, orc):
+    """A 2100 x 1024 x 1024 tensor (2.25e9 elements > 2^31, 9 GB): every unfolding's projection with
+    n = 16 (mode 0 K-major, mode 1 slab view, mode 2 M-major in place), sampled rows vs the oracle."""
+    dims = (2100, 1024, 1024)
+    T = shg.synth("gauss", 8, 0x108, dims[0], dims[1] * dims[2]).view(*dims)
+    for mode in range(3):
+        I = dims[mode]
+        rows = np.array([0, 1, I // 2, I - 2, I - 1])
+        ridx = torch.from_numpy(rows).cuda()
+        W = shg.project(T, mode, 16, seed=8)
+        U = to_np(torch.movedim(T, mode, 0)[ridx].reshape(len(rows), -1))
+        ob = orc.omega_f16(U.shape[1], 16, seed=8, stream_id=mode)
+        check_bars(orc, U, ob, to_np(W[ridx]))
+
+
 def test_config5_full_size_sampled(shg, orc):
     """BASELINE config 5 at full size (A 32768^2 FP32 = 4 GiB) for n = 16 (HBM-bound, split-K),
     n = 1024 and n = 4096 (tensor-bound, several N tiles): 64 sampled rows each against the oracle."""
