@@ -350,6 +350,47 @@ def test_project_tensor_over_2g_elements(shg, orc):
         check_bars(orc, U, ob, to_np(W[ridx]))
 
 
+def test_concurrent_streams_and_threads(shg):
+    """Eight host threads, each on its own CUDA stream, issue shgemm / project / tcec_sgemm calls
+    with library-allocated split-K workspaces concurrently: results bitwise equal to serial calls
+    (the library keeps no shared mutable state but the launch counter and the per-device occupancy
+    cache)."""
+    import threading
+    g = torch.Generator(device="cuda").manual_seed(21)
+    A = torch.randn(700, 3000, device="cuda", generator=g)
+    B = torch.randn(3000, 100, device="cuda", generator=g)
+    T = torch.randn(20, 30, 40, device="cuda", generator=g)
+    Om = shg.gen_omega(3000, 100, seed=2)
+    calls = [lambda s: shg.shgemm(A, Om, stream=s), lambda s: shg.shgemm(A, Om, tune={"split_k": 5}, stream=s),
+             lambda s: shg.project(T, 1, 12, seed=4, stream=s), lambda s: shg.tcec_sgemm(A, B, stream=s)]
+    ref = [c(None) for c in calls]
+    torch.cuda.synchronize()
+    out = [[None] * len(calls) for _ in range(8)]
+    err = []
+
+    def worker(t):
+        try:
+            s = torch.cuda.Stream()
+            with torch.cuda.stream(s):
+                for rep in range(3):
+                    for i, c in enumerate(calls):
+                        out[t][i] = c(s)
+            s.synchronize()
+        except Exception as e:        # surfaced below
+            err.append(e)
+
+    th = [threading.Thread(target=worker, args=(t,)) for t in range(8)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    torch.cuda.synchronize()
+    assert not err, err
+    for t in range(8):
+        for i in range(len(calls)):
+            assert torch.equal(out[t][i], ref[i]), (t, i)
+
+
 def test_config5_full_size_sampled(shg, orc):
     """BASELINE config 5 at full size (A 32768^2 FP32 = 4 GiB) for n = 16 (HBM-bound, split-K),
     n = 1024 and n = 4096 (tensor-bound, several N tiles): 64 sampled rows each against the oracle."""
