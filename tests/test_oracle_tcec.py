@@ -47,8 +47,10 @@ def test_tcec_transpose_symmetry(orc):
 
 
 def test_tcec_error_bound_and_both_corrections_matter(orc):
-    """|Y_tcec - Y64| <= sum_l (|dA dB| 2^-22 + split representation errors) <= 3u sum |a||b|
-    (u = 2^-24); dropping either correction term costs ~2^-12 relative."""
+    """Per product Eq 9 errs by the two split representation errors (<= 1 FP32 ulp each,
+    <= 2u|a|, 2u|b|) plus the dropped 2^-22 dA_low dB_low (<= u16^2 |a||b| = 4u|a||b|), so
+    |Y_tcec - Y64| <= 8.01u sum_l |a||b| (u = 2^-24) in the worst case (DESIGN R20); on random
+    data of length 512 it is well under 3u. Dropping either correction term costs ~2^-12 relative."""
     rng = np.random.default_rng(5)
     A = rng.standard_normal((64, 512)).astype(np.float32)
     B = rng.standard_normal((512, 32)).astype(np.float32)
@@ -56,6 +58,16 @@ def test_tcec_error_bound_and_both_corrections_matter(orc):
     yt = orc.gemm_ytcec64(A, B)
     absprod = np.abs(A).astype(np.float64) @ np.abs(B).astype(np.float64)
     assert np.all(np.abs(yt - y64) <= 3 * 2.0 ** -24 * absprod)
+    # short products do not average: the worst case needs the full 8u (k = 4, fuzz case 1567 of
+    # tests/test_gpu_fuzz.py reaches 4.7u); 20000 random 1- to 4-term rows stay within 8.01u
+    for kk in (1, 2, 4):
+        A2 = (rng.standard_normal((5000, kk)) * np.exp(rng.uniform(-3, 3, (5000, kk)))).astype(np.float32)
+        B2 = (rng.standard_normal((kk, 8)) * np.exp(rng.uniform(-3, 3, (kk, 8)))).astype(np.float32)
+        ab = np.abs(A2).astype(np.float64) @ np.abs(B2).astype(np.float64)
+        err = np.abs(orc.gemm_ytcec64(A2, B2) - orc.gemm_y64_f32b(A2, B2))
+        assert np.all(err <= 8.01 * 2.0 ** -24 * ab)
+        if kk == 1:     # one product: the split + dropped-term error alone, which exceeds 3u somewhere
+            assert np.max(err / np.maximum(ab, 1e-300)) > 3 * 2.0 ** -24
     assert orc.relative_error(yt, y64) < 2e-7
     # no-correction (A_low B_low only) is far worse: FP16-level
     ha, _ = orc.split(A)
