@@ -104,6 +104,38 @@ def test_split_inequalities_and_quarter_bit_loss(orc):
     assert 0.22 < frac < 0.28, frac
 
 
+def test_split_error_floor_all_binades(orc):
+    """The reconstruction error the GPU bars rely on (DESIGN R22): |hi + lo 2^-11 - a| <= 2u|a|
+    (u = 2^-24) for |a| >= 2^-13 and <= 2^-36 below, where hi or the scaled lo leave the FP16 normal
+    range. Every mantissa of the binades 2^-15 .. 2^-11 (the transition) and 2^16 random
+    mantissas of every other binade from 2^-149 to 2^15, both signs."""
+    u = 2.0 ** -24
+    rng = np.random.default_rng(22)
+    worst_small = 0.0
+    for e in range(-149, 16):
+        if -15 <= e <= -11:
+            mant = np.arange(1 << 23, dtype=np.uint32)
+        else:
+            mant = rng.integers(0, 1 << 23, 1 << 16, dtype=np.uint32)
+        if e >= -126:
+            bits = (np.uint32(e + 127) << np.uint32(23)) | mant
+        else:                       # subnormal FP32: value = mant * 2^-149, binade [2^e, 2^(e+1))
+            lo_m, hi_m = 1 << (e + 149), 1 << (e + 150)
+            bits = (lo_m + mant % (hi_m - lo_m)).astype(np.uint32)
+        a = bits.view(np.float32)
+        a = np.concatenate([a, -a])
+        a = a[np.abs(a) < 65520.0]           # |a| >= 65520: hi = inf (test_split_overflow_and_nan)
+        hi, lo = orc.split(a)
+        rec = orc.f16_bits_as_float(hi).astype(np.float64) + orc.f16_bits_as_float(lo).astype(np.float64) * 2.0 ** -11
+        err = np.abs(rec - a.astype(np.float64))
+        if e >= -13:
+            assert np.all(err <= 2 * u * np.abs(a)), e
+        else:
+            assert np.all(err <= 2.0 ** -36), e
+            worst_small = max(worst_small, float(err.max()))
+    assert worst_small == 2.0 ** -36         # the floor is attained (half the FP16 subnormal step x 2^-11)
+
+
 def test_split_overflow_and_nan(orc):
     """|a| >= 65520 -> hi = +-inf (FP16 range); NaN propagates."""
     a = np.array([65520.0, -1e6, np.inf, np.nan, 65519.0], dtype=np.float32)
