@@ -125,6 +125,20 @@ def _stream(stream=None):
 
 
 def _p(t: torch.Tensor | None):
+    """Device pointer of a tensor on the current CUDA device (the library launches there)."""
+    if t is None:
+        return ctypes.c_void_p(0)
+    if not t.is_cuda:
+        raise ValueError(f"expected a CUDA tensor, got one on {t.device}")
+    if t.device.index != torch.cuda.current_device():
+        raise ValueError(f"tensor on {t.device} but the current device is cuda:{torch.cuda.current_device()}")
+    return ctypes.c_void_p(t.data_ptr())
+
+
+def _h(t: torch.Tensor | None):
+    """Host pointer (shgemm_host's A and Y)."""
+    if t is not None and t.device.type != "cpu":
+        raise ValueError(f"expected a host tensor, got one on {t.device}")
     return ctypes.c_void_p(0 if t is None else t.data_ptr())
 
 
@@ -274,8 +288,8 @@ def shgemm_host(A_host: torch.Tensor, Omega: torch.Tensor, Y_host: torch.Tensor 
     if Y_host is None:
         Y_host = torch.empty((m, n), dtype=torch.float32, pin_memory=True)
     ws_bytes = 0 if workspace is None else workspace.numel() * workspace.element_size()
-    _check(lib().shgemm_host(m, n, k, _p(A_host), A_host.stride(0) if m > 1 else max(k, 1), _p(Omega),
-                             Omega.stride(1) if n > 1 else max(k, 1), _p(Y_host), Y_host.stride(0) if m > 1 else n,
+    _check(lib().shgemm_host(m, n, k, _h(A_host), A_host.stride(0) if m > 1 else max(k, 1), _p(Omega),
+                             Omega.stride(1) if n > 1 else max(k, 1), _h(Y_host), Y_host.stride(0) if m > 1 else n,
                              chunk_rows, _p(workspace), ws_bytes, _stream(stream)), "shgemm_host")
     return Y_host
 

@@ -86,3 +86,18 @@ def test_python_binding_has_no_fallback(shg, monkeypatch, tmp_path):
     with pytest.raises(m.SHGError):
         m.lib()
     importlib.reload(m)
+
+
+def test_binding_rejects_host_tensors_for_device_arguments():
+    """The binding marshals only CUDA tensors on the current device into device-pointer arguments; a
+    host tensor raises before anything reaches the library (no silent host-pointer launch)."""
+    import paper_2304_04612_b200 as shg
+    torch = pytest.importorskip("torch")
+    A = torch.zeros(8, 8)
+    Om = torch.zeros(2, 8, dtype=torch.float16).t()
+    with pytest.raises(ValueError, match="CUDA tensor"):
+        shg.shgemm(A, Om)
+    with pytest.raises(ValueError, match="CUDA tensor"):
+        shg.tcec_sgemm(A, torch.zeros(8, 3))
+    with pytest.raises(ValueError, match="CUDA tensor"):
+        shg.project(torch.zeros(4, 5, 6), 1, 3)
