@@ -73,6 +73,26 @@ class ClockSampler:
         self._t = None
 
     def _run(self):
+        # one nvidia-smi in loop mode (-lms: a sample every 50 ms) instead of a process per sample;
+        # falls back to the per-sample loop if it yields nothing
+        try:
+            proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                                     "--format=csv,noheader,nounits", "-lms", "50"],
+                                    stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            proc = None
+        if proc is not None:
+            reader = threading.Thread(target=self._read, args=(proc,), daemon=True)
+            reader.start()
+            self._stop.wait()
+            proc.terminate()
+            try:
+                proc.wait(timeout=5)
+            except Exception:
+                proc.kill()
+            reader.join(timeout=5)
+            if self.samples:
+                return
         while not self._stop.is_set():
             try:
                 out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
@@ -83,6 +103,12 @@ class ClockSampler:
             except Exception:
                 pass
             self._stop.wait(0.1)
+
+    def _read(self, proc):
+        for line in proc.stdout:
+            parts = [x.strip() for x in line.strip().split(",")]
+            if len(parts) >= 9:
+                self.samples.append(parts)
 
     def start(self):
         self._t = threading.Thread(target=self._run, daemon=True)
