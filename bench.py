@@ -152,7 +152,8 @@ def cpu_baseline(m, k, n, budget_s=10.0):
         rows = min(m, int(rows * max(2.0, min(8.0, (budget_s / 3) / max(dt, 1e-3)))))
     flops = 2.0 * done * k * n
     return {"value": flops / elapsed / 1e12, "unit": "TFLOP/s", "cores": oracle.num_threads(), "kind": "oracle",
-            "sample": f"{done} of {m} rows of A ({k}x{n} Omega), naive FP32 fmaf GEMM, {elapsed:.2f} s"}
+            "sample": f"{done} of {m} rows of A ({k}x{n} Omega), naive FP32 fmaf GEMM, {elapsed:.2f} s",
+            **host_info()}
 
 
 def run_reference(args, cfg_name):
@@ -189,7 +190,7 @@ def run_reference(args, cfg_name):
 
 PIPELINES = {
     "rsvd_cfg2": "BASELINE config 2: Randomized SVD (Alg 1) of a 16384x16384 FP32 matrix (A_exp, s_p=1e-2), rank 256 + 16",
-    "rphosvd_cfg3": "BASELINE config 3: RP-HOSVD (Alg 2) of a 1024^3 FP32 tensor (Alg 3, J=64, p=4), rank 64 per mode",
+    "rphosvd_cfg3": "BASELINE config 3: RP-HOSVD (Alg 2) of a 1024^3 FP32 tensor (Alg 3, J=64, p=4, + 1e-2 N(0,1) noise), rank 64 per mode",
 }
 
 
@@ -209,7 +210,9 @@ def run_pipeline(args):
         err = lambda r: pl.reconstruction_error(X, r["U"], r["S"], r["V"])
         flops = 2.0 * N * N * (p + sov)
     else:
-        X = torch.from_numpy(synth.alg3_tensor((1024, 1024, 1024), (64, 64, 64), pad=4, seed=1)).cuda()
+        # the noisy Alg-3 tensor (multilinear rank 60 + 1e-2 N(0,1)): an approximation-dominated
+        # residual (~1e-2), so the residuals compared are not roundoff (reading c4-12 / c4-18)
+        X = synth.alg3_tensor_torch((1024, 1024, 1024), (64, 64, 64), pad=4, seed=1, noise=1e-2)
         run = lambda proj, gemm, fac: pl.rp_hosvd(X, (64, 64, 64), seed=0, projection=proj, timing=True, gemm=gemm,
                                                   factor=fac)
         err = lambda r: pl.hosvd_error(X, r["core"], r["Q"])
@@ -245,6 +248,120 @@ def run_pipeline(args):
             "paper_context": "A100: 1.28x RSVD, 1.75x RP-HOSVD whole-pipeline speedups (P:12, P:786)"}), flush=True)
 
 
+def _free_port() -> int:
+    import socket
+    with socket.socket(socket.AF_INET, socket.SOCK_STREAM) as sk:
+        sk.bind(("127.0.0.1", 0))
+        return sk.getsockname()[1]
+
+
+def spawn_ranks(n: int) -> int:
+    """Re-run this command as N ranks (torch.distributed.run, 127.0.0.1 rendezvous); returns the
+    launcher's exit code. Each rank binds LOCAL_RANK's GPU; rank 0 prints the JSON line."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), os.path.abspath(__file__)] + sys.argv[1:]
+    env = dict(os.environ, OMP_NUM_THREADS=os.environ.get("OMP_NUM_THREADS", "1"))
+    return subprocess.call(cmd, env=env)
+
+
+def row_partition(m_total: int, world: int, rank: int):
+    """rank g owns rows [g*ceil(m/G), min(m, (g+1)*ceil(m/G)))."""
+    per = (m_total + world - 1) // world
+    row0 = min(m_total, rank * per)
+    return per, row0, max(0, min(m_total, row0 + per) - row0)
+
+
+def dry_run(args):
+    """The multi-rank plumbing without the GPU: process group (gloo on CPU), row partition, the
+    all-reduce(MAX) of a per-rank time, one line from rank 0."""
+    import torch
+    import torch.distributed as dist
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    m_total, k, n, desc = CONFIGS[args.config]
+    per, row0, m = row_partition(m_total, world, rank)
+    rows = torch.tensor([float(m), float(rank + 1)])
+    if world > 1:
+        dist.init_process_group("gloo")
+        dist.all_reduce(rows[:1], op=dist.ReduceOp.SUM)
+        dist.all_reduce(rows[1:], op=dist.ReduceOp.MAX)
+    if rank == 0:
+        print(json.dumps({"metric": METRIC, "value": None, "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps,
+                          "warmup": args.warmup, "dry_run": True, "rows_covered": int(rows[0]),
+                          "max_rank_plus_one": int(rows[1]),
+                          "config": {"workload": args.config, "m": m_total, "k": k, "n": n, "rows_per_gpu": per}}),
+              flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def host_info() -> dict:
+    """CPU model, usable CPUs (sched_getaffinity) and host RAM of this box, for the CPU baseline."""
+    info = {"affinity_cpus": len(os.sched_getaffinity(0)), "os_cpus": os.cpu_count()}
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                info["cpu_model"] = line.split(":", 1)[1].strip()
+                break
+        for line in open("/proc/meminfo"):
+            if line.startswith("MemTotal"):
+                info["host_ram_gib"] = round(int(line.split()[1]) / 2 ** 20, 1)
+                break
+    except OSError:
+        pass
+    return info
+
+
+def oracle_sweep(budget_s: float = 1.5) -> dict:
+    """SURVEY §8(d) oracle timing: the oracle as it stands (naive FP32 fmaf GEMM, OpenMP over rows;
+    its Omega generator) on bounded row samples of configs 1, 2, 3 (one mode-n unfolding projection)
+    and 5 (n = 16..4096); the full-config time is extrapolated linearly in m (rows are independent)
+    and labelled so. Omega generation is timed on a sample of its elements and extrapolated the same way."""
+    import numpy as np
+    import oracle
+    out = {"kind": "oracle", "cores": oracle.num_threads(), **host_info(), "configs": {}}
+    # Omega generator rate (elements / s) on a 32768 x 64 sample
+    t0 = time.perf_counter()
+    oracle.omega_f16(32768, 64, seed=OMEGA_SEED)
+    om_rate = 32768 * 64 / (time.perf_counter() - t0)
+    out["omega_elements_per_s"] = om_rate
+
+    def gemm_rate(m, k, n):
+        om = oracle.omega_f16(k, n, seed=OMEGA_SEED) if k * n <= (1 << 26) else None
+        if om is None:   # Omega too large to regenerate for a rate sample: time the first 2^26 / k rows of k
+            raise ValueError
+        rows0 = 8 * oracle.num_threads()        # >= 2 dynamic chunks of 4 rows per OpenMP thread
+        rows, dt = min(m, rows0), 0.0
+        while True:
+            A = oracle.synth_rows("gauss", DATA_SEED, 0x101, np.arange(rows, dtype=np.int64), k)
+            t = time.perf_counter()
+            oracle.gemm_y32(A, om)
+            dt = time.perf_counter() - t
+            cap = min(m, max(rows0, min(4096, (1 << 26) // k)))   # <= 256 MiB of sampled A
+            if dt > budget_s / 3 or rows >= cap:
+                return rows, dt
+            rows = min(cap, rows * max(2, int((budget_s / 3) / max(dt, 1e-4))))
+
+    shapes = {"cfg1": (512, 512, 32), "cfg2_projection": (16384, 16384, 272),
+              "cfg3_mode_projection": (1024, 1 << 20, 64)}
+    for nn in (16, 32, 64, 128, 256, 512, 1024, 2048, 4096):
+        shapes[f"cfg5_n{nn}"] = (32768, 32768, nn)
+    for name, (m, k, n) in shapes.items():
+        if k * n > (1 << 26):   # cfg5 n >= 4096: the GEMM rate is linear in n at fixed k; sample n = 2048
+            rows, dt = gemm_rate(m, k, (1 << 26) // k)
+            dt *= n / ((1 << 26) // k)
+        else:
+            rows, dt = gemm_rate(m, k, n)
+        t_gemm = dt * m / rows
+        t_gen = k * n / om_rate
+        out["configs"][name] = {"m": m, "k": k, "n": n, "sample_rows": int(rows), "sample_s": dt,
+                                "full_s_extrapolated": t_gemm + t_gen, "gemm_s_extrapolated": t_gemm,
+                                "omega_gen_s_extrapolated": t_gen,
+                                "tflops": 2.0 * m * k * n / (t_gemm + t_gen) / 1e12}
+    return out
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -258,8 +375,25 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-extras", action="store_true",
                     help="skip the short per-config timings of BASELINE configs 2, 3 and 5 (single GPU, cfg4 runs)")
+    ap.add_argument("--dry-run", action="store_true",
+                    help="no GPU work: set up the ranks and the row partition and print the line's shape "
+                         "(CPU test of the multi-rank launch)")
+    ap.add_argument("--cpu-sweep", action="store_true",
+                    help="time the CPU oracle on bounded samples of configs 1, 2, 3 and 5 (all n) and print "
+                         "one JSON line (SURVEY §8(d) oracle timing)")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
+
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # `python bench.py --gpus N` (the driver's form): re-launch this script with one rank per GPU
+        # under torch.distributed.run; rank 0 prints the line for all N ranks
+        sys.exit(spawn_ranks(args.gpus))
+    if args.cpu_sweep:
+        print(json.dumps(oracle_sweep()), flush=True)
+        return
+    if args.dry_run:
+        dry_run(args)
+        return
 
     if args.config in PIPELINES:
         if args.impl == "reference":
@@ -292,10 +426,7 @@ def main():
             dist.init_process_group("gloo")
 
     m_total, k, n, desc = CONFIGS[args.config]
-    # row sharding: rank g owns rows [g*ceil(m/G), min(m, (g+1)*ceil(m/G)))
-    per = (m_total + world - 1) // world
-    row0 = rank * per
-    m = max(0, min(m_total, row0 + per) - row0)
+    per, row0, m = row_partition(m_total, world, rank)
 
     A = shg.synth("gauss", DATA_SEED, DATA_STREAM, m, k, row0=row0)          # resident input
     Y = torch.empty((m, n), dtype=torch.float32, device="cuda")
@@ -307,11 +438,15 @@ def main():
     import ctypes
     tune = shg.Tune()
     tune.tc = shg.TCS[args.tc]
+    # Omega generated straight into the column-major (K-major) layout the tensor cores stream, so the
+    # step is two launches (no transpose pass; shgemm() also takes row-major Omega, bitwise the same Y)
+    tune.omega_layout = shg.OMEGA_COL_MAJOR
     ws_bytes = shg.workspace_size(m, n, k, tc=args.tc)
     ws = torch.empty(max(1, ws_bytes), dtype=torch.uint8, device="cuda")
 
     def gen():
-        shg._check(L.gen_omega_f16(k, n, OMEGA_SEED, 0, shg._p(om_buf), ldo, shg._stream()), "gen_omega_f16")
+        shg._check(L.gen_omega_f16_ex(k, n, OMEGA_SEED, 0, 0, 0, k, shg._p(om_buf), ldo, shg.OMEGA_COL_MAJOR,
+                                      shg._stream()), "gen_omega_f16_ex")
 
     def gemm():
         shg._check(L.shgemm_ex(m, n, k, shg._p(A), k, shg._p(om_buf), ldo, shg._p(Y), n, ctypes.byref(tune),
@@ -386,39 +521,35 @@ def main():
     value = flops_total / (ms_per_step * 1e-3) / 1e12
 
     hbm, tc16, tc16_sus, peak_src = load_peaks()
-    # The timed region runs the kernel back to back for ~0.1-1 s, long enough for the 1000 W software
-    # power cap to settle (observed: reason sw_power_cap, SM clock ~1.1 GHz), so the tensor peak is
-    # the driver's SUSTAINED cuBLAS figure; the burst figure is reported beside it.
-    region_s = total_ms * 1e-3
-    # TF32 tensor cores run at half the FP16/BF16 rate (guide's nominal ratio)
-    tc_ratio = 0.5 if args.tc == "tf32" else 1.0
+    # Roofline (north_star): min(P_FP16 / 2, AI x BW) with the BURST tensor peak (the
+    # kernel is timed alone, one ~19-ms launch per step): HBM-bound for n <= 253, tensor-bound above.
+    # cfg4 (AI = 120.5 flop/B) is HBM-bound, so `frac` = algorithmic bytes per launch / launch time /
+    # measured HBM bandwidth. The sustained-peak tensor fraction is reported beside it, not as `frac`.
+    tc_ratio = 0.5 if args.tc == "tf32" else 1.0            # TF32 tensor rate = half of FP16
     tc16, tc16_sus = tc16 * tc_ratio, tc16_sus * tc_ratio
-    tc_peak = tc16_sus if region_s > 0.1 else tc16
-    tc_peak_kind = ("sustained" if region_s > 0.1 else "burst") + (
-        " (bf16 figure x 0.5 for TF32)" if args.tc == "tf32" else "")
     alg_bytes = 4.0 * m * k + 2.0 * k * n + 4.0 * m * n        # per launch, this rank
     achieved_gbs = alg_bytes / (gemm_ms * 1e-3) / 1e9
     ai = 2.0 * m * k * n / alg_bytes
-    tc_ceiling = tc_peak / 2.0                                  # two MMAs per product
+    tc_ceiling = tc16 / 2.0                                     # two MMAs per product
     useful_tflops = 2.0 * m * k * n / (gemm_ms * 1e-3) / 1e12
+    tc_ach = 4.0 * m * k * n / (gemm_ms * 1e-3) / 1e12         # tensor pipe: hi and lo MMAs
     bound = "hbm" if ai * hbm / 1e3 < tc_ceiling else "tensor"
     if bound == "hbm":
         roof = {"bound": "hbm", "achieved": achieved_gbs, "peak": hbm, "unit": "GB/s", "frac": achieved_gbs / hbm}
     else:
-        # the tensor pipe executes 4mnk flops (hi and lo MMAs); peak = measured dense fp16 (= bf16 rate)
-        tc_ach = 4.0 * m * k * n / (gemm_ms * 1e-3) / 1e12
-        roof = {"bound": "tensor", "achieved": tc_ach, "peak": tc_peak, "unit": "TFLOP/s", "frac": tc_ach / tc_peak}
+        roof = {"bound": "tensor", "achieved": tc_ach, "peak": tc16, "unit": "TFLOP/s", "frac": tc_ach / tc16}
     tag = args.config + ("" if args.tc == "fp16" else "_tf32")
     roof["traffic"] = ncu_traffic(tag if world == 1 else f"{tag}_g{world}")
-    roof["peak_source"] = f"{peak_src} (MEASURED_PEAKS.json); tensor peak {tc_peak_kind}"
+    roof["peak_source"] = (f"{peak_src} (MEASURED_PEAKS.json): hbm_gbs; bf16_tflops (burst) for the bound"
+                           + (" x 0.5 for TF32" if args.tc == "tf32" else ""))
     roof["kernel"] = "shgemm_sm100_kernel"
     roof["kernel_ms"] = gemm_ms
     roof["algorithmic_bytes_per_launch"] = alg_bytes
     roof["algorithmic_flops_per_launch"] = 2.0 * m * k * n
-    roof["frac_of_min(tc/2, AI*hbm)"] = useful_tflops / min(tc_ceiling, ai * hbm / 1e3)
+    roof["frac_of_min(tc_burst/2, AI*hbm)"] = useful_tflops / min(tc_ceiling, ai * hbm / 1e3)
     roof["frac_hbm"] = achieved_gbs / hbm
-    roof["frac_tensor_burst"] = 4.0 * m * k * n / (gemm_ms * 1e-3) / 1e12 / tc16
-    roof["frac_tensor_sustained"] = 4.0 * m * k * n / (gemm_ms * 1e-3) / 1e12 / tc16_sus
+    roof["frac_tensor_burst"] = tc_ach / tc16
+    roof["frac_tensor_sustained"] = tc_ach / tc16_sus       # context: the 1000 W cap
     # against the spec sheet (2250 TFLOP/s dense fp16/bf16, 8 TB/s HBM3e), for reference
     spec_tc = 2250.0 * tc_ratio
     roof["frac_spec_min(tc/2, AI*hbm)"] = useful_tflops / min(spec_tc / 2.0, ai * 8000.0 / 1e3)
@@ -446,6 +577,13 @@ def main():
         cpu = None
         if not args.no_cpu_baseline and world == 1:
             cpu = cpu_baseline(m_total, k, n)
+            if args.config == "cfg4" and not args.no_extras:
+                try:   # the oracle on configs 1, 2, 3, 5 (bounded samples, extrapolated)
+                    sw = oracle_sweep()
+                    cpu["configs"] = sw["configs"]
+                    cpu["omega_elements_per_s"] = sw["omega_elements_per_s"]
+                except Exception as exc:  # noqa: BLE001
+                    cpu["configs_error"] = repr(exc)[:200]
         out = {"metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps,
                "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
                "vs_baseline": None,
@@ -476,9 +614,10 @@ def measure_extras(shg, torch, hbm, tc16_burst, tc_ratio, reps=10):
     of each mode (1024^3 tensor, n = 64, Omega generation included) and cfg5 at n = 64 and 1024."""
     import statistics as st
 
-    def med_ms(fn):
+    def med_ms(fn, spread=False):
         # 5 rounds of `reps` back-to-back calls between two events (the host enqueues ahead of the
-        # device, so host-side call overhead is not timed); median round, per call
+        # device, so host-side call overhead is not timed); median round, per call. Back to back the
+        # GPU settles under the 1000 W cap within a few ms, so this is the SUSTAINED rate.
         for _ in range(3):
             fn()
         torch.cuda.synchronize()
@@ -491,13 +630,33 @@ def measure_extras(shg, torch, hbm, tc16_burst, tc_ratio, reps=10):
             b.record()
             torch.cuda.synchronize()
             ts.append(a.elapsed_time(b) / reps)
+        return (st.median(ts), min(ts), max(ts)) if spread else st.median(ts)
+
+    def iso_ms(fn, n_iso=7):
+        # one call at a time after 50 ms idle (a 64 MiB scrub evicts the previous call's A from L2):
+        # the BURST rate, i.e. a projection as one step of a pipeline sees it
+        scrub = torch.empty(64 << 20, dtype=torch.uint8, device="cuda")
+        ts = []
+        for _ in range(n_iso):
+            scrub.zero_()
+            torch.cuda.synchronize()
+            time.sleep(0.05)
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            fn()
+            b.record()
+            torch.cuda.synchronize()
+            ts.append(a.elapsed_time(b))
         return st.median(ts)
 
-    def roof(m, k, n, ms):
+    def roof(m, k, n, ms, iso=None):
         fl, by = 2.0 * m * k * n, 4.0 * m * k + 2.0 * k * n + 4.0 * m * n
         ceil = min(tc16_burst * tc_ratio / 2.0, fl / by * hbm / 1e3)
-        return {"ms": ms, "tflops": fl / ms / 1e9, "gbs": by / ms / 1e6, "frac_roofline": fl / ms / 1e9 / ceil,
-                "bound": "tensor" if tc16_burst * tc_ratio / 2.0 < fl / by * hbm / 1e3 else "hbm"}
+        d = {"ms": ms, "tflops": fl / ms / 1e9, "gbs": by / ms / 1e6, "frac_roofline": fl / ms / 1e9 / ceil,
+             "bound": "tensor" if tc16_burst * tc_ratio / 2.0 < fl / by * hbm / 1e3 else "hbm"}
+        if iso is not None:   # single call after idle: burst clocks
+            d.update(ms_isolated=iso, frac_roofline_isolated=fl / iso / 1e9 / ceil)
+        return d
 
     out = {}
     # context for the power cap: cuBLAS bf16 on cfg4's own shape (one 16-bit product, half the A bytes)
@@ -511,23 +670,50 @@ def measure_extras(shg, torch, hbm, tc16_burst, tc_ratio, reps=10):
                                              "SHGEMM's tensor work is two products on FP32 A (compare its 4mnk/t)"}
     del Ab, Bb, Cb
     torch.cuda.empty_cache()
-    for name, (m, k, n) in {"cfg2_projection": (16384, 16384, 272), "cfg5_n64": (32768, 32768, 64),
-                            "cfg5_n1024": (32768, 32768, 1024)}.items():
-        A = shg.synth("gauss", DATA_SEED, 0x101, m, k)
-        Om = shg.gen_omega(k, n, seed=OMEGA_SEED)
+    # the power-cap ceiling of SHGEMM's own work: cuBLAS fp16 doing BOTH products
+    # on the same bytes as one GEMM, [A_hi | A_lo] (m x 2k FP16 = the 4mk bytes of FP32 A) times
+    # [Omega; Omega] (2k x n): the tensor flops (4mnk) and A bytes of SHGEMM without its split and
+    # RN promotion (and with a 2-byte output)
+    A2 = torch.randn(m4, 2 * k4, device="cuda", dtype=torch.float16)
+    B2 = torch.randn(2 * k4, n4, device="cuda", dtype=torch.float16)
+    C2 = torch.empty(m4, n4, device="cuda", dtype=torch.float16)
+    ms = med_ms(lambda: torch.matmul(A2, B2, out=C2))
+    out["cublas_fp16_two_products_cfg4_bytes"] = {
+        "ms": ms, "tensor_tflops": 4.0 * m4 * n4 * k4 / ms / 1e9, "useful_tflops_equiv": 2.0 * m4 * n4 * k4 / ms / 1e9,
+        "gbs": (4.0 * m4 * k4 + 4.0 * k4 * n4 + 2.0 * m4 * n4) / ms / 1e6,
+        "note": "torch.matmul fp16, (4194304 x 8192) . (8192 x 256): SHGEMM-FP16's 4mnk tensor flops on its 4mk "
+                "A bytes, no split / promotion: the power-capped ceiling for the method on this box"}
+    del A2, B2, C2
+    torch.cuda.empty_cache()
+    shapes = {"cfg2_projection": (16384, 16384, 272)}
+    for nn in (16, 32, 64, 128, 256, 512, 1024, 2048, 4096):      # BASELINE config 5: the whole sweep
+        shapes[f"cfg5_n{nn}"] = (32768, 32768, nn)
+    A5 = None
+    for name, (m, k, n) in shapes.items():
+        if name.startswith("cfg5"):
+            A5 = shg.synth("gauss", DATA_SEED, 0x101, m, k) if A5 is None else A5
+            A = A5
+        else:
+            A = shg.synth("gauss", DATA_SEED, 0x101, m, k)
+        Om = torch.empty((n, k), dtype=torch.float16, device="cuda").t()
         Y = torch.empty((m, n), device="cuda")
-        ms = med_ms(lambda: (shg.gen_omega(k, n, seed=OMEGA_SEED), shg.shgemm(A, Om, out=Y)))
-        out[name] = dict(roof(m, k, n, ms), m=m, k=k, n=n, step="gen_omega_f16 + shgemm")
+        fn = lambda: (shg.gen_omega(k, n, seed=OMEGA_SEED, out=Om), shg.shgemm(A, Om, out=Y))
+        ms = med_ms(fn)
+        out[name] = dict(roof(m, k, n, ms, iso_ms(fn)), m=m, k=k, n=n, step="gen_omega_f16 + shgemm")
         del A, Om, Y
         torch.cuda.empty_cache()
+    del A5
+    torch.cuda.empty_cache()
     T = shg.synth("gauss", 1, 0x102, 1024, 1024 * 1024).view(1024, 1024, 1024)
     ws = torch.empty(max(shg.project_workspace_size([1024] * 3, md, 64) for md in range(3)), dtype=torch.uint8,
                      device="cuda")
+    W = torch.empty((1024, 64), device="cuda")
     for mode in range(3):
-        ms = med_ms(lambda: shg.project(T, mode, 64, workspace=ws))
-        out[f"cfg3_project_mode{mode}"] = dict(roof(1024, 1 << 20, 64, ms), m=1024, k=1 << 20, n=64,
-                                               step="project() incl. Omega generation")
-    del T, ws
+        fn = lambda: shg.project(T, mode, 64, workspace=ws, out=W)
+        ms, lo, hi = med_ms(fn, spread=True)
+        out[f"cfg3_project_mode{mode}"] = dict(roof(1024, 1 << 20, 64, ms, iso_ms(fn)), m=1024, k=1 << 20, n=64,
+                                               ms_min=lo, ms_max=hi, step="project() incl. Omega generation")
+    del T, ws, W
     torch.cuda.empty_cache()
     try:
         out.update(measure_pipelines(torch))
@@ -561,7 +747,7 @@ def measure_pipelines(torch, reps=3):
                                  "residual_baseline": pl.reconstruction_error(X, base["U"], base["S"], base["V"])}
     del X, prod, base
     torch.cuda.empty_cache()
-    T = synth.alg3_tensor_torch((1024, 1024, 1024), (64, 64, 64), pad=4, seed=1)
+    T = synth.alg3_tensor_torch((1024, 1024, 1024), (64, 64, 64), pad=4, seed=1, noise=1e-2)
     prod = best(lambda: pl.rp_hosvd(T, (64, 64, 64), seed=0, timing=True, gemm="tcec", factor="gram"))
     base = best(lambda: pl.rp_hosvd(T, (64, 64, 64), seed=0, projection="sgemm", timing=True))
     out["rphosvd_cfg3_pipeline"] = {"ms": prod["times_ms"]["total"], "lines_ms": prod["times_ms"],

@@ -34,11 +34,12 @@ int main(int argc, char **argv) {
         fprintf(stderr, "no sm_100 device\n");
         return 4;
     }
-    const int64_t lda = (k + 3) / 4 * 4, ldo = (k + 7) / 8 * 8;
+    /* SURVEY §8(b) layouts: A row-major (lda >= k), Omega row-major (ldo >= n), Y row-major */
+    const int64_t lda = (k + 3) / 4 * 4, ldo = n;
     float *A = NULL, *Y = NULL;
     uint16_t *Om = NULL;
     CHECK_CUDA(cudaMalloc((void **)&A, (size_t)(m * lda) * sizeof(float)));
-    CHECK_CUDA(cudaMalloc((void **)&Om, (size_t)(n * ldo) * sizeof(uint16_t)));
+    CHECK_CUDA(cudaMalloc((void **)&Om, (size_t)(k * ldo) * sizeof(uint16_t)));
     CHECK_CUDA(cudaMalloc((void **)&Y, (size_t)(m * n) * sizeof(float)));
     cudaStream_t st;
     CHECK_CUDA(cudaStreamCreate(&st));

@@ -18,12 +18,18 @@
  *  - All work is enqueued asynchronously on `stream` (a cudaStream_t; NULL = legacy default).
  *    Argument errors are returned synchronously and nothing is enqueued; faults inside kernels
  *    surface at the caller's next synchronization (CUDA convention).
- *  - Layouts: A is row-major m x k with leading dimension lda >= k (elements);
- *    Omega is k x n COLUMN-major (Omega[i][j] at Omega[j*ldo + i], ldo >= k), i.e. K-contiguous,
- *    FP16 stored as uint16_t bit patterns; Y is row-major m x n, ldc >= n.
- *  - Tensor-core fast path preconditions: A, Omega, Y 16-byte aligned, lda % 4 == 0,
- *    ldo % 8 == 0 (TMA row pitch multiple of 16 B). Otherwise a CUDA-core fallback with the same
- *    numerics contract runs (slower).
+ *  - Layouts: A is row-major m x k with leading dimension lda >= k
+ *    (elements); Y is row-major m x n, ldc >= n. Omega (k x n, FP16 stored as uint16_t bit
+ *    patterns) is ROW-major by default, Omega[i][j] at Omega[i*ldo + j] with ldo >= n — the layout
+ *    of shgemm() and gen_omega_f16(). The _ex calls also take it COLUMN-major
+ *    (SHG_OMEGA_COL_MAJOR: Omega[i][j] at Omega[j*ldo + i], ldo >= k), which is the tensor cores'
+ *    K-major B operand and is streamed by TMA as is; a row-major Omega is first transposed into
+ *    that layout in the workspace (transpose_omega_kernel, 4kn bytes of traffic, one launch).
+ *    Both layouts give bitwise-identical Y. The layout is always explicit (an argument or
+ *    shg_tune_t.omega_layout), never guessed from ldo: for n == k both leading dimensions are valid.
+ *  - Tensor-core fast path preconditions: A, Y 16-byte aligned, lda % 4 == 0; a column-major
+ *    Omega also 16-byte aligned with ldo % 8 == 0 (TMA row pitch multiple of 16 B). Otherwise a
+ *    CUDA-core fallback with the same numerics contract runs (slower).
  *  - Numerical exceptions are not errors: |a| >= 65520 overflows the FP16 hi part to +-inf and
  *    the affected Y rows become non-finite — the paper's expected SHGEMM-FP16 failure on
  *    A_Cauchy. NaN propagates. The _ex variants can raise a device flag.
@@ -74,6 +80,11 @@ typedef enum {
  * B[j * ldb + l], ldb >= k; MN_MAJOR = row-major, element (l, j) at B[l * ldb + j], ldb >= n. */
 typedef enum { SHG_LAYOUT_K_MAJOR = 0, SHG_LAYOUT_MN_MAJOR = 1 } shg_layout_t;
 
+/* Omega layouts (k x n FP16). ROW_MAJOR is SURVEY §8(b)'s: Omega[i][j] at Omega[i*ldo + j],
+ * ldo >= n. COL_MAJOR: Omega[i][j] at Omega[j*ldo + i], ldo >= k (the kernel's native K-major
+ * operand: no transpose pass). Any other value: SHG_ERR_INVALID_VALUE. */
+typedef enum { SHG_OMEGA_ROW_MAJOR = 0, SHG_OMEGA_COL_MAJOR = 1 } shg_omega_layout_t;
+
 /* Tunables for shgemm_ex. Zero-initialise for the heuristics. */
 typedef struct {
     int32_t bn;          /* N tile (multiple of 16, <= 256); 0 = heuristic */
@@ -98,6 +109,8 @@ typedef struct {
     /* Diagnostics: device int64[grid * 16] per-CTA wait-cycle counters (layout in
      * csrc/shgemm_sm100.cuh, enum ProfSlot), or NULL. */
     int64_t *prof;
+    int32_t omega_layout; /* shg_omega_layout_t of the Omega argument: SHG_OMEGA_ROW_MAJOR (0, default;
+                             ldo >= n) or SHG_OMEGA_COL_MAJOR (ldo >= k). A NULL tune means row-major. */
 } shg_tune_t;
 
 /* Plan the library would use for an (m, n, k) shgemm on the current device. */
@@ -114,36 +127,42 @@ typedef struct {
 /* ---------------------------------------------------------------------------------------------
  * shgemm — Y[m x n] = A[m x k] . Omega[k x n] by SHGEMM-FP16 (Eqs 14-17).
  *   m, n, k  >= 0. m == 0 or n == 0: no-op. k == 0: Y = 0.
- *   A        device, row-major, lda >= max(k,1).   Omega device, column-major, ldo >= max(k,1).
+ *   A        device, row-major, lda >= max(k,1).   Omega device, ROW-major, ldo >= max(n,1).
  *   Y        device, row-major, ldc >= max(n,1); overwritten (beta = 0).
- * Split-K scratch, when the heuristic uses it, is stream-ordered cudaMallocAsync memory.
+ *   Errors   SHG_ERR_INVALID_VALUE for negative sizes, short leading dimensions or NULL pointers
+ *            (nothing enqueued); SHG_ERR_UNSUPPORTED_DEVICE off sm_100; SHG_ERR_CUDA on a failed launch.
+ * Scratch (the column-major copy of Omega the tensor cores read; split-K planes when the heuristic
+ * splits k) is stream-ordered cudaMallocAsync memory freed on `stream`.
  * ------------------------------------------------------------------------------------------- */
 shg_status_t shgemm(int64_t m, int64_t n, int64_t k, const float *A, int64_t lda, const uint16_t *Omega,
                     int64_t ldo, float *Y, int64_t ldc, shg_stream_t stream);
 
 /* shgemm by SHGEMM-TF32: Eqs 14-17 with toLow = TF32 (RN ties-to-even), so
  * any finite FP32 A below (2 - 2^-11) * 2^127 is accepted (A_Cauchy of P:699-706 stays finite).
- * Same arguments and layouts as shgemm; Omega stays FP16 in memory and is widened exactly to TF32
- * in stream-ordered scratch (k x n x 4 bytes) for the tensor cores. */
+ * Same arguments and layouts as shgemm (row-major Omega, ldo >= n); Omega stays FP16 in memory and
+ * is widened exactly to TF32 in stream-ordered scratch (k x n x 4 bytes) for the tensor cores. */
 shg_status_t shgemm_tf32(int64_t m, int64_t n, int64_t k, const float *A, int64_t lda, const uint16_t *Omega,
                          int64_t ldo, float *Y, int64_t ldc, shg_stream_t stream);
 
-/* shgemm with tunables (tune->tc selects SHGEMM-FP16 or -TF32), caller workspace
- * (>= shg_workspace_size bytes, or NULL), and an optional device int flag set to 1 if any output
- * is non-finite (never cleared by the library). */
+/* shgemm with tunables (tune->tc selects SHGEMM-FP16 or -TF32; tune->omega_layout the Omega
+ * layout, row-major when tune is NULL), caller workspace (>= shg_workspace_size bytes for the same
+ * tune, or NULL), and an optional device int flag set to 1 if any output is non-finite (never
+ * cleared by the library). */
 shg_status_t shgemm_ex(int64_t m, int64_t n, int64_t k, const float *A, int64_t lda, const uint16_t *Omega,
                        int64_t ldo, float *Y, int64_t ldc, const shg_tune_t *tune, void *workspace,
                        size_t workspace_bytes, int *nonfinite_flag, shg_stream_t stream);
 
 /* shgemm_ex for an M-major A ("A transposed"): element (i, l) of A is At[l * ldat + i], i.e. At is
  * the k x m row-major transpose of A, ldat >= m (fast path: At 16-B aligned, ldat % 4 == 0). This
- * is how project() reads the last-mode unfolding of a C-order tensor in place. */
+ * is how project() reads the last-mode unfolding of a C-order tensor in place. Omega layout from
+ * tune->omega_layout as for shgemm_ex. */
 shg_status_t shgemm_at(int64_t m, int64_t n, int64_t k, const float *At, int64_t ldat, const uint16_t *Omega,
                        int64_t ldo, float *Y, int64_t ldc, const shg_tune_t *tune, void *workspace,
                        size_t workspace_bytes, int *nonfinite_flag, shg_stream_t stream);
 
-/* Bytes of workspace shgemm_ex needs for (m, n, k) with `tune` (NULL = heuristics): split-K
- * partial planes, plus the TF32 copy of Omega when tune->tc == SHG_TC_TF32. */
+/* Bytes of workspace shgemm_ex needs for (m, n, k) with `tune` (NULL = heuristics, row-major Omega):
+ * split-K partial planes, plus the TF32 copy of Omega when tune->tc == SHG_TC_TF32, or the
+ * column-major copy of a row-major FP16 Omega. */
 size_t shg_workspace_size(int64_t m, int64_t n, int64_t k, const shg_tune_t *tune);
 
 /* Fill *plan for (m, n, k) with `tune` (NULL = heuristics), without launching anything. */
@@ -185,15 +204,18 @@ shg_status_t tcec_plan(int64_t m, int64_t n, int64_t k, const shg_tune_t *tune, 
 
 /* ---------------------------------------------------------------------------------------------
  * gen_omega_f16 — Omega[i][j] = OMEGA_SPEC(seed, stream_id = 0, dist, i, j) for 0 <= i < k,
- * 0 <= j < n, written column-major with ldo >= k (FP16 bits). Bit-identical to the CPU oracle.
+ * 0 <= j < n (the random matrix of Eq 1 / Alg 1 line 1, drawn in FP32 and rounded RN
+ * to FP16), written ROW-major with ldo >= n (FP16 bits). Bit-identical to the CPU oracle.
+ * Errors: SHG_ERR_INVALID_VALUE for negative sizes, dist outside shg_dist_t, ldo < n or NULL Omega.
  * ------------------------------------------------------------------------------------------- */
 shg_status_t gen_omega_f16(int64_t k, int64_t n, uint64_t seed, int dist, uint16_t *Omega, int64_t ldo,
                            shg_stream_t stream);
 
 /* As gen_omega_f16 with an explicit Philox stream id, a row offset (local row r holds spec row
- * row0 + r; used for K-sharding) and the full-Omega row count k_total for SHG_DIST_VERYSPARSE. */
+ * row0 + r; used for K-sharding), the full-Omega row count k_total for SHG_DIST_VERYSPARSE, and the
+ * output layout (shg_omega_layout_t: ROW_MAJOR ldo >= n, COL_MAJOR ldo >= k). */
 shg_status_t gen_omega_f16_ex(int64_t k, int64_t n, uint64_t seed, int dist, uint32_t stream_id,
-                              int64_t row0, int64_t k_total, uint16_t *Omega, int64_t ldo,
+                              int64_t row0, int64_t k_total, uint16_t *Omega, int64_t ldo, int layout,
                               shg_stream_t stream);
 
 /* project() with Omega_(mode) supplied by the caller, already generated in the k-tiled layout by
@@ -262,17 +284,22 @@ shg_status_t project_shard(const float *A, int ndim, const int64_t *dims, int mo
 
 /* ---------------------------------------------------------------------------------------------
  * shgemm_host — Y = A . Omega with A and Y in HOST memory (pinned for overlap; pageable works but
- * serialises), Omega on the device. A is streamed to the device in row chunks of `chunk_rows`
- * (0 = heuristic) through two staging buffers: H2D copy of chunk c+1 and D2H copy of chunk c-1
- * overlap the SHGEMM of chunk c on internal streams that are ordered after / before `stream`.
- * workspace: device scratch >= shg_host_workspace_size(n, k, chunk_rows) bytes, or NULL
- * (stream-ordered allocation). Returns when everything is enqueued; synchronize `stream`.
+ * serialises), Omega on the device in `omega_layout` (shg_omega_layout_t). A is streamed to the
+ * device in row chunks of `chunk_rows` (0 = heuristic) through two staging buffers: H2D copy of
+ * chunk c+1 and D2H copy of chunk c-1 overlap the SHGEMM of chunk c on two side streams created
+ * for this call and ordered after / before `stream` by events created for this call, so
+ * concurrent calls from several host threads (on their own streams) do not serialise on shared
+ * library state. workspace: device scratch >= shg_host_workspace_size(n, k, chunk_rows,
+ * omega_layout) bytes (covers every chunk height up to chunk_rows, including a short last chunk),
+ * or NULL (stream-ordered allocation). Returns when everything is enqueued; synchronize `stream`.
+ * On an error after work was enqueued, the side streams are still joined to `stream` and owned
+ * scratch is freed on it before returning.
  * ------------------------------------------------------------------------------------------- */
 shg_status_t shgemm_host(int64_t m, int64_t n, int64_t k, const float *A_host, int64_t lda,
-                         const uint16_t *Omega, int64_t ldo, float *Y_host, int64_t ldc, int64_t chunk_rows,
-                         void *workspace, size_t workspace_bytes, shg_stream_t stream);
+                         const uint16_t *Omega, int64_t ldo, int omega_layout, float *Y_host, int64_t ldc,
+                         int64_t chunk_rows, void *workspace, size_t workspace_bytes, shg_stream_t stream);
 
-size_t shg_host_workspace_size(int64_t n, int64_t k, int64_t chunk_rows);
+size_t shg_host_workspace_size(int64_t n, int64_t k, int64_t chunk_rows, int omega_layout);
 
 /* ---------------------------------------------------------------------------------------------
  * Test / bench support (not part of the method).

@@ -39,7 +39,7 @@ class Tune(ctypes.Structure):
     _fields_ = [("bn", ctypes.c_int32), ("split_k", ctypes.c_int32), ("max_ctas", ctypes.c_int32),
                 ("force_simt", ctypes.c_int32), ("debug_flags", ctypes.c_int32), ("pair", ctypes.c_int32),
                 ("a_box", ctypes.c_int32), ("tc", ctypes.c_int32), ("omega_mcast", ctypes.c_int32),
-                ("prof", ctypes.c_void_p)]
+                ("prof", ctypes.c_void_p), ("omega_layout", ctypes.c_int32)]
 
 
 class Plan(ctypes.Structure):
@@ -66,13 +66,13 @@ def lib():
             L.shg_workspace_size.restype = sz
             L.shg_plan.argtypes = [i64, i64, i64, ctypes.POINTER(Tune), ctypes.POINTER(Plan)]
             L.gen_omega_f16.argtypes = [i64, i64, u64, i32, vp, i64, vp]
-            L.gen_omega_f16_ex.argtypes = [i64, i64, u64, i32, u32, i64, i64, vp, i64, vp]
+            L.gen_omega_f16_ex.argtypes = [i64, i64, u64, i32, u32, i64, i64, vp, i64, i32, vp]
             L.project.argtypes = [vp, i32, vp, i32, i64, u64, i32, vp, i64, vp, sz, vp]
             L.shg_project_workspace_size.argtypes = [i32, vp, i32, i64]
             L.shg_project_workspace_size.restype = sz
             L.shgemm_at.argtypes = [i64, i64, i64, vp, i64, vp, i64, vp, i64, ctypes.POINTER(Tune), vp, sz, vp, vp]
-            L.shgemm_host.argtypes = [i64, i64, i64, vp, i64, vp, i64, vp, i64, i64, vp, sz, vp]
-            L.shg_host_workspace_size.argtypes = [i64, i64, i64]
+            L.shgemm_host.argtypes = [i64, i64, i64, vp, i64, vp, i64, i32, vp, i64, i64, vp, sz, vp]
+            L.shg_host_workspace_size.argtypes = [i64, i64, i64, i32]
             L.shg_host_workspace_size.restype = sz
             L.shg_debug_split.argtypes = [vp, i64, vp, vp, vp]
             L.shg_synth_f32.argtypes = [i32, u64, u32, i64, i64, i64, vp, i64, vp]
@@ -165,16 +165,49 @@ def version() -> str:
 
 
 # ----------------------------------------------------------------------------------------- Omega
+# shg_omega_layout_t (include/shgemm.h): Omega k x n row-major (ldo >= n) or column-major
+# (ldo >= k, the tensor cores' K-major operand, no transpose pass)
+OMEGA_ROW_MAJOR, OMEGA_COL_MAJOR = 0, 1
+_LAYOUTS = {"row": OMEGA_ROW_MAJOR, "col": OMEGA_COL_MAJOR}
+
+
+def omega_layout(Omega: torch.Tensor):
+    """(shg_omega_layout_t, ldo) of a (k, n) float16 tensor for the C ABI: column-major if
+    stride(0) == 1, row-major if stride(1) == 1; the layout is passed explicitly, never inferred
+    from ldo by the library."""
+    k, n = Omega.shape
+    if k <= 1 and n <= 1:
+        return OMEGA_COL_MAJOR, max(k, 1)
+    if n <= 1 or (k > 1 and Omega.stride(0) == 1):
+        return OMEGA_COL_MAJOR, (Omega.stride(1) if n > 1 else max(k, 1))
+    if k <= 1 or Omega.stride(1) == 1:
+        return OMEGA_ROW_MAJOR, (Omega.stride(0) if k > 1 else max(n, 1))
+    raise ValueError(f"Omega must have one contiguous dimension (strides {Omega.stride()})")
+
+
 def gen_omega(k: int, n: int, seed: int = 0, dist="gaussian", stream_id: int = 0, row0: int = 0,
-              k_total: int | None = None, device=None, stream=None) -> torch.Tensor:
-    """Omega (k x n, FP16) of OMEGA_SPEC.md, returned as a column-major view (strides (1, ldo))."""
-    device = torch.device("cuda") if device is None else torch.device(device)
-    ldo = (k + 7) // 8 * 8 if k > 0 else 8
-    buf = torch.empty((n, ldo), dtype=torch.float16, device=device)
+              k_total: int | None = None, device=None, stream=None, out: torch.Tensor | None = None,
+              layout: str = "col") -> torch.Tensor:
+    """Omega (k x n, FP16) of OMEGA_SPEC.md. layout='col' (default): a column-major view (strides
+    (1, ldo), ldo = k rounded up to 8: the layout the tensor cores stream without a copy);
+    layout='row': a row-major (k, n) tensor (SURVEY §8(b)'s). With `out` (a (k, n) float16 tensor,
+    either layout) the values are written there."""
+    if out is None:
+        device = torch.device("cuda") if device is None else torch.device(device)
+        if layout == "row":
+            out = torch.empty((k, n), dtype=torch.float16, device=device)
+        elif layout == "col":
+            ldo = (k + 7) // 8 * 8 if k > 0 else 8
+            out = torch.empty((n, ldo), dtype=torch.float16, device=device)[:, :k].t()
+        else:
+            raise ValueError("layout must be 'row' or 'col'")
+    elif out.dtype != torch.float16 or tuple(out.shape) != (k, n):
+        raise ValueError("out must be a (k, n) float16 tensor")
+    lay, ldo = omega_layout(out)
     _check(lib().gen_omega_f16_ex(k, n, seed & (2 ** 64 - 1), _dist(dist), stream_id, row0,
-                                  k if k_total is None else k_total, _p(buf), ldo, _stream(stream)),
+                                  k if k_total is None else k_total, _p(out), ldo, lay, _stream(stream)),
            "gen_omega_f16_ex")
-    return buf[:, :k].t()
+    return out
 
 
 def gen_omega_tiled(k: int, n: int, seed: int = 0, dist="gaussian", stream_id: int = 0, row0: int = 0,
@@ -189,14 +222,24 @@ def gen_omega_tiled(k: int, n: int, seed: int = 0, dist="gaussian", stream_id: i
     return buf
 
 
+def _check_out(out, m, n, device):
+    """A caller's Y: (m, n) float32 with unit column stride (every wrapper writes m rows of n)."""
+    if out is None:
+        return torch.empty((m, n), dtype=torch.float32, device=device)
+    if out.dtype != torch.float32 or tuple(out.shape) != (m, n) or (m and n > 1 and out.stride(1) != 1):
+        raise ValueError(f"out must be ({m}, {n}) float32 row-major, got {tuple(out.shape)} {out.dtype}")
+    return out
+
+
 def shgemm_tiled(A: torch.Tensor, Omega_tiled: torch.Tensor, n: int, out=None, tune=None, workspace=None,
                  stream=None) -> torch.Tensor:
     """Y = A . Omega with Omega in the k-tiled layout (gen_omega_tiled(k, n, ...))."""
     m, k = A.shape
     if A.dtype != torch.float32 or (m and k and A.stride(1) != 1):
         raise ValueError("A must be float32 row-major")
-    if out is None:
-        out = torch.empty((m, n), dtype=torch.float32, device=A.device)
+    if Omega_tiled.dtype != torch.float16 or Omega_tiled.numel() < ((k + 63) // 64) * n * 64:
+        raise ValueError("Omega_tiled must be float16 with ceil(k/64) * n * 64 elements")
+    out = _check_out(out, m, n, A.device)
     ws_bytes = 0 if workspace is None else workspace.numel() * workspace.element_size()
     _check(lib().shgemm_tiled(m, n, k, _p(A), A.stride(0) if m > 1 else max(k, 1), _p(Omega_tiled), _p(out),
                               out.stride(0) if m > 1 else max(n, 1), _tune(tune), _p(workspace), ws_bytes, None,
@@ -217,22 +260,25 @@ def _tc(tc) -> int:
     return int(tc)
 
 
-def _tune(tune, tc=None):
-    if tune is None and tc is None:
+def _tune(tune, tc=None, omega_layout=None):
+    if tune is None and tc is None and omega_layout in (None, OMEGA_ROW_MAJOR):
         return None
     t = Tune()
     for key, val in dict(tune or {}).items():
         setattr(t, key, _tc(val) if key == "tc" else int(val))
     if tc is not None:
         t.tc = _tc(tc)
+    if omega_layout is not None:
+        t.omega_layout = omega_layout
     return ctypes.byref(t)
 
 
 def shgemm(A: torch.Tensor, Omega: torch.Tensor, out: torch.Tensor | None = None, tune=None,
            nonfinite: torch.Tensor | None = None, workspace: torch.Tensor | None = None,
            stream=None, tc=None) -> torch.Tensor:
-    """Y = A . Omega. A: (m, k) float32, row-major (stride(1) == 1). Omega: (k, n) float16,
-    column-major (stride(0) == 1), e.g. from gen_omega(). Returns Y (m, n) float32 row-major.
+    """Y = A . Omega. A: (m, k) float32, row-major (stride(1) == 1). Omega: (k, n) float16, either
+    column-major (stride(0) == 1, e.g. gen_omega(): streamed as is) or row-major (stride(1) == 1:
+    transposed into the workspace first; bitwise the same Y). Returns Y (m, n) float32 row-major.
     tc: 'fp16' (SHGEMM-FP16, default) or 'tf32' (SHGEMM-TF32, full FP32 exponent range)."""
     if A.dtype != torch.float32 or Omega.dtype != torch.float16:
         raise TypeError("A must be float32 and Omega float16")
@@ -242,17 +288,12 @@ def shgemm(A: torch.Tensor, Omega: torch.Tensor, out: torch.Tensor | None = None
         raise ValueError(f"shape mismatch {tuple(A.shape)} x {tuple(Omega.shape)}")
     if m and k and A.stride(1) != 1:
         raise ValueError("A must be row-major (stride(1) == 1)")
-    if k and n and Omega.stride(0) != 1:
-        raise ValueError("Omega must be column-major (stride(0) == 1)")
-    if out is None:
-        out = torch.empty((m, n), dtype=torch.float32, device=A.device)
-    elif out.dtype != torch.float32 or tuple(out.shape) != (m, n) or (m and n and out.stride(1) != 1):
-        raise ValueError("out must be (m, n) float32 row-major")
+    lay, ldo = omega_layout(Omega)
+    out = _check_out(out, m, n, A.device)
     lda = A.stride(0) if m > 1 else max(k, 1)
-    ldo = Omega.stride(1) if n > 1 else max(k, 1)
     ldc = out.stride(0) if m > 1 else max(n, 1)
     ws_bytes = 0 if workspace is None else workspace.numel() * workspace.element_size()
-    _check(lib().shgemm_ex(m, n, k, _p(A), lda, _p(Omega), ldo, _p(out), ldc, _tune(tune, tc), _p(workspace),
+    _check(lib().shgemm_ex(m, n, k, _p(A), lda, _p(Omega), ldo, _p(out), ldc, _tune(tune, tc, lay), _p(workspace),
                            ws_bytes, _p(nonfinite), _stream(stream)), "shgemm_ex")
     return out
 
@@ -266,46 +307,54 @@ def shgemm_at(At: torch.Tensor, Omega: torch.Tensor, out: torch.Tensor | None = 
         raise ValueError("shape/dtype mismatch")
     if m and k and At.stride(1) != 1:
         raise ValueError("At must be row-major")
-    if k and n and Omega.stride(0) != 1:
-        raise ValueError("Omega must be column-major (stride(0) == 1)")
-    if out is None:
-        out = torch.empty((m, n), dtype=torch.float32, device=At.device)
+    lay, ldo = omega_layout(Omega)
+    out = _check_out(out, m, n, At.device)
     ws_bytes = 0 if workspace is None else workspace.numel() * workspace.element_size()
-    _check(lib().shgemm_at(m, n, k, _p(At), At.stride(0) if k > 1 else max(m, 1), _p(Omega),
-                           Omega.stride(1) if n > 1 else max(k, 1), _p(out), out.stride(0) if m > 1 else max(n, 1),
-                           _tune(tune, tc), _p(workspace), ws_bytes, _p(nonfinite), _stream(stream)), "shgemm_at")
+    _check(lib().shgemm_at(m, n, k, _p(At), At.stride(0) if k > 1 else max(m, 1), _p(Omega), ldo, _p(out),
+                           out.stride(0) if m > 1 else max(n, 1), _tune(tune, tc, lay), _p(workspace), ws_bytes,
+                           _p(nonfinite), _stream(stream)), "shgemm_at")
     return out
 
 
 def shgemm_host(A_host: torch.Tensor, Omega: torch.Tensor, Y_host: torch.Tensor | None = None,
                 chunk_rows: int = 0, workspace: torch.Tensor | None = None, stream=None) -> torch.Tensor:
     """Y = A . Omega with A (m, k) float32 and Y (m, n) float32 in (pinned) host memory, Omega on the
-    device; A is streamed through the device in overlapped row chunks (include/shgemm.h)."""
+    device (either layout); A is streamed through the device in overlapped row chunks
+    (include/shgemm.h)."""
     m, k = A_host.shape
-    n = Omega.shape[1]
+    k2, n = Omega.shape
     if A_host.device.type != "cpu" or Omega.device.type != "cuda":
         raise ValueError("A_host must be a host tensor and Omega a device tensor")
+    if A_host.dtype != torch.float32 or (m and k > 1 and A_host.stride(1) != 1) or k2 != k:
+        raise ValueError("A_host must be (m, k) float32 row-major matching Omega (k, n)")
+    if Omega.dtype != torch.float16:
+        raise TypeError("Omega must be float16")
+    lay, ldo = omega_layout(Omega)
     if Y_host is None:
         Y_host = torch.empty((m, n), dtype=torch.float32, pin_memory=True)
+    elif (Y_host.device.type != "cpu" or Y_host.dtype != torch.float32 or tuple(Y_host.shape) != (m, n)
+          or (m and n > 1 and Y_host.stride(1) != 1)):
+        raise ValueError("Y_host must be an (m, n) float32 row-major host tensor")
     ws_bytes = 0 if workspace is None else workspace.numel() * workspace.element_size()
-    _check(lib().shgemm_host(m, n, k, _h(A_host), A_host.stride(0) if m > 1 else max(k, 1), _p(Omega),
-                             Omega.stride(1) if n > 1 else max(k, 1), _h(Y_host), Y_host.stride(0) if m > 1 else n,
-                             chunk_rows, _p(workspace), ws_bytes, _stream(stream)), "shgemm_host")
+    _check(lib().shgemm_host(m, n, k, _h(A_host), A_host.stride(0) if m > 1 else max(k, 1), _p(Omega), ldo, lay,
+                             _h(Y_host), Y_host.stride(0) if m > 1 else max(n, 1), chunk_rows, _p(workspace),
+                             ws_bytes, _stream(stream)), "shgemm_host")
     return Y_host
 
 
-def host_workspace_size(n: int, k: int, chunk_rows: int = 0) -> int:
-    return int(lib().shg_host_workspace_size(n, k, chunk_rows))
+def host_workspace_size(n: int, k: int, chunk_rows: int = 0, layout: str = "col") -> int:
+    return int(lib().shg_host_workspace_size(n, k, chunk_rows, _LAYOUTS[layout]))
 
 
-def plan(m: int, n: int, k: int, tune=None, tc=None) -> dict:
+def plan(m: int, n: int, k: int, tune=None, tc=None, layout: str = "col") -> dict:
     p = Plan()
-    _check(lib().shg_plan(m, n, k, _tune(tune, tc), ctypes.byref(p)), "shg_plan")
+    _check(lib().shg_plan(m, n, k, _tune(tune, tc, _LAYOUTS[layout]), ctypes.byref(p)), "shg_plan")
     return {f: getattr(p, f) for f, _ in Plan._fields_}
 
 
-def workspace_size(m: int, n: int, k: int, tune=None, tc=None) -> int:
-    return int(lib().shg_workspace_size(m, n, k, _tune(tune, tc)))
+def workspace_size(m: int, n: int, k: int, tune=None, tc=None, layout: str = "col") -> int:
+    """Workspace bytes of shgemm() for an Omega in `layout` ('col' as gen_omega() returns, or 'row')."""
+    return int(lib().shg_workspace_size(m, n, k, _tune(tune, tc, _LAYOUTS[layout])))
 
 
 # ---------------------------------------------------------------------------------- TCEC-SGEMM
@@ -375,16 +424,17 @@ def project(T: torch.Tensor, mode: int, n: int, seed: int = 0, dist="gaussian", 
         raise ValueError("T must be a contiguous float32 tensor")
     dims = list(T.shape)
     M = dims[mode]
-    if out is None:
-        out = torch.empty((M, n), dtype=torch.float32, device=T.device)
+    out = _check_out(out, M, n, T.device)
     d = (ctypes.c_int64 * len(dims))(*dims)
     ws_bytes = 0 if workspace is None else workspace.numel() * workspace.element_size()
     if omega is not None:
-        _check(lib().project_omega(_p(T), len(dims), d, mode, n, _p(omega), _p(out), out.stride(0), _p(workspace),
+        _check(lib().project_omega(_p(T), len(dims), d, mode, n, _p(omega), _p(out),
+                                   out.stride(0) if M > 1 else max(n, 1), _p(workspace),
                                    ws_bytes, _stream(stream)), "project_omega")
         return out
     _check(lib().project_shard(_p(T), len(dims), d, mode, n, seed, _dist(dist), _tc(tc), omega_row0, k_total,
-                               _p(out), out.stride(0), _p(workspace), ws_bytes, _stream(stream)), "project_shard")
+                               _p(out), out.stride(0) if M > 1 else max(n, 1), _p(workspace), ws_bytes,
+                               _stream(stream)), "project_shard")
     return out
 
 

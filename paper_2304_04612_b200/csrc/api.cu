@@ -213,6 +213,7 @@ struct Plan {
     // workspace = [split-K planes, 256-B aligned][TF32 copy of Omega | TCEC split of B]
     int64_t ws_bytes = 0, ld_ws = 0, sk_bytes = 0, om_bytes = 0, ldo32 = 0;
     int64_t ldh = 0, noff = 0;  // TCEC: split B column-major, ld ldh; dB_low starts at column noff
+    int64_t ldt = 0;            // row-major FP16 Omega: leading dimension of its column-major copy
 };
 
 int64_t up256(int64_t b) { return (b + 255) / 256 * 256; }
@@ -232,7 +233,10 @@ struct OmGen {
 constexpr int kAutoMcast = 1;
 
 
-Plan make_plan(int64_t m, int64_t n, int64_t k, bool fast_ok, const shg_tune_t* tune, int sms, bool tcec = false) {
+// om_rm: Omega is row-major; the FP16 tensor-core path then reads a column-major copy
+// made in the workspace by transpose_omega_kernel (TF32 widens either layout directly)
+Plan make_plan(int64_t m, int64_t n, int64_t k, bool fast_ok, const shg_tune_t* tune, int sms, bool tcec = false,
+               bool om_rm = false) {
     Plan pl;
     pl.tf32 = !tcec && tune && tune->tc == SHG_TC_TF32;
     pl.tcec = tcec;
@@ -312,6 +316,9 @@ Plan make_plan(int64_t m, int64_t n, int64_t k, bool fast_ok, const shg_tune_t* 
     if (pl.tcec) {   // [B_low | pad | dB_low | pad], each n_tiles * BN columns (pads zeroed)
         pl.noff = static_cast<int64_t>(pl.n_tiles) * pl.bn;
         pl.om_bytes = 2 * pl.noff * pl.ldh * 2;
+    } else if (om_rm && !pl.tf32) {   // column-major copy of a row-major Omega (ldt % 8 == 0: TMA pitch)
+        pl.ldt = (k + 7) / 8 * 8;
+        pl.om_bytes = n * pl.ldt * 2;
     }
     pl.ws_bytes = (pl.om_bytes ? up256(pl.sk_bytes) : pl.sk_bytes) + pl.om_bytes;
     return pl;
@@ -357,11 +364,14 @@ struct AView {
 };
 
 // B32 != nullptr selects TCEC-SGEMM: B element (l, j) at B32[l * sbk + j * sbn] (FP32), Om unused.
+// om_rm: Om is ROW-major (element (l, j) at Om[l * ldo + j]); otherwise column-major (Om[j * ldo + l])
+// or, with om_tiled, the k-tiled layout of gen_omega_f16_tiled.
 shg_status_t run_shgemm(int64_t m, int64_t n, int64_t k, const AView& av, const uint16_t* Om, int64_t ldo,
                         float* Y, int64_t ldc, const shg_tune_t* tune, void* ws, size_t ws_bytes, int* nonfinite,
                         cudaStream_t stream, const float* B32 = nullptr, int64_t sbk = 0, int64_t sbn = 0,
-                        bool om_tiled = false, const OmGen* og = nullptr) {
+                        bool om_tiled = false, const OmGen* og = nullptr, bool om_rm = false) {
     const bool tcec = B32 != nullptr;
+    if (om_rm && (om_tiled || tcec)) return SHG_ERR_INVALID_VALUE;
     if (om_tiled && tcec) return SHG_ERR_INVALID_VALUE;
     if (m == 0 || n == 0) return SHG_OK;
     if (k == 0) {
@@ -371,10 +381,12 @@ shg_status_t run_shgemm(int64_t m, int64_t n, int64_t k, const AView& av, const 
     DevInfo& d = dev_info();
     if (!d.ok) return SHG_ERR_UNSUPPORTED_DEVICE;
     const bool plain = (av.P == 1 && av.S == k);
-    const bool fast_ok = aligned16(av.A) && aligned16(Om) && (av.row_stride % 4 == 0) && (av.slab % 4 == 0) &&
-                         (tcec || ldo % 8 == 0) && (plain || av.S % 32 == 0) && encode_fn() != nullptr &&
+    // a row-major Omega is copied (transposed) into the workspace first, so its alignment and ldo do not matter
+    const bool om_ok = tcec || om_rm || (aligned16(Om) && ldo % 8 == 0);
+    const bool fast_ok = aligned16(av.A) && om_ok && (av.row_stride % 4 == 0) && (av.slab % 4 == 0) &&
+                         (plain || av.S % 32 == 0) && encode_fn() != nullptr &&
                          k < (int64_t(1) << 31) && av.S < (int64_t(1) << 31) && m < (int64_t(1) << 31);
-    Plan pl = make_plan(m, n, k, fast_ok, tune, d.sms, tcec);
+    Plan pl = make_plan(m, n, k, fast_ok, tune, d.sms, tcec, om_rm);
     if (pl.path < 0) return SHG_ERR_INVALID_VALUE;
     if (pl.path == 1 && tcec) {
         if (!plain) return SHG_ERR_INVALID_VALUE;
@@ -400,8 +412,8 @@ shg_status_t run_shgemm(int64_t m, int64_t n, int64_t k, const AView& av, const 
         // callers materialise non-plain views first; the CUDA-core fallback reads column-major Omega
         if (!plain || om_tiled) return SHG_ERR_INVALID_VALUE;
         const int64_t sa_row = av.mmajor ? 1 : av.row_stride, sa_col = av.mmajor ? av.row_stride : 1;
-        shg::shgemm_simt_kernel<<<grid_for(m * n, 256), 256, 0, stream>>>(m, n, k, av.A, sa_row, sa_col, Om, ldo, Y,
-                                                                         ldc, nonfinite, pl.tf32);
+        shg::shgemm_simt_kernel<<<grid_for(m * n, 256), 256, 0, stream>>>(
+            m, n, k, av.A, sa_row, sa_col, Om, om_rm ? ldo : 1, om_rm ? 1 : ldo, Y, ldc, nonfinite, pl.tf32);
         g_launches.fetch_add(1, std::memory_order_relaxed);
         SHG_CUDA(cudaGetLastError());
         return SHG_OK;
@@ -461,7 +473,8 @@ shg_status_t run_shgemm(int64_t m, int64_t n, int64_t k, const AView& av, const 
         if (om_tiled) {
             shg::widen_omega_tiled_kernel<<<grid_for((k + 31) / 32 * 32 * n, 256), 256, 0, stream>>>(Om, k, n, om32);
         } else {
-            shg::widen_omega_kernel<<<grid_for(k * n, 256), 256, 0, stream>>>(Om, k, n, ldo, om32, pl.ldo32);
+            shg::widen_omega_kernel<<<grid_for(k * n, 256), 256, 0, stream>>>(Om, k, n, om_rm ? ldo : 1,
+                                                                            om_rm ? 1 : ldo, om32, pl.ldo32);
         }
         g_launches.fetch_add(1, std::memory_order_relaxed);
         if (cudaGetLastError() != cudaSuccess) return finish(cuda_fail(cudaErrorLaunchFailure, "widen_omega_kernel"));
@@ -470,6 +483,15 @@ shg_status_t run_shgemm(int64_t m, int64_t n, int64_t k, const AView& av, const 
                                  encode_b32(&mapB1, om32, k, n, pl.ldo32, rows1);
     } else if (om_tiled) {
         encb_ok = encode_b_tiled(&mapB0, Om, k, n, rows0) && encode_b_tiled(&mapB1, Om, k, n, rows1);
+    } else if (om_rm) {
+        uint16_t* Ot = reinterpret_cast<uint16_t*>(wsb + up256(pl.sk_bytes));
+        const int64_t tiles = ((k + 31) / 32) * ((n + 31) / 32);
+        const int sms = std::max(1, d.sms);
+        shg::transpose_omega_kernel<<<static_cast<int>(std::min<int64_t>(tiles, int64_t(sms) * 8)), dim3(32, 8), 0,
+                                      stream>>>(Om, k, n, ldo, Ot, pl.ldt);
+        g_launches.fetch_add(1, std::memory_order_relaxed);
+        if (cudaGetLastError() != cudaSuccess) return finish(cuda_fail(cudaErrorLaunchFailure, "transpose_omega_kernel"));
+        encb_ok = encode_b(&mapB0, Ot, k, n, pl.ldt, rows0) && encode_b(&mapB1, Ot, k, n, pl.ldt, rows1);
     } else {
         encb_ok = encode_b(&mapB0, Om, k, n, ldo, rows0) && encode_b(&mapB1, Om, k, n, ldo, rows1);
     }
@@ -560,31 +582,6 @@ uint32_t sparse_threshold(int dist, int64_t k_total) {
 
 
 // ------------------------------------------------------------------ host-streaming support
-struct HostStreams {
-    cudaStream_t s[2] = {nullptr, nullptr};
-    cudaEvent_t ev_start = nullptr, ev_done[2] = {nullptr, nullptr};
-    bool ok = false;
-};
-
-HostStreams& host_streams() {
-    static HostStreams hs[64];
-    static std::once_flag flags[64];
-    int dev = 0;
-    cudaGetDevice(&dev);
-    dev = std::min(std::max(dev, 0), 63);
-    std::call_once(flags[dev], [dev]() {
-        HostStreams& h = hs[dev];
-        bool ok = true;
-        for (int i = 0; i < 2; ++i) {
-            ok &= cudaStreamCreateWithFlags(&h.s[i], cudaStreamNonBlocking) == cudaSuccess;
-            ok &= cudaEventCreateWithFlags(&h.ev_done[i], cudaEventDisableTiming) == cudaSuccess;
-        }
-        ok &= cudaEventCreateWithFlags(&h.ev_start, cudaEventDisableTiming) == cudaSuccess;
-        h.ok = ok;
-    });
-    return hs[dev];
-}
-
 int64_t host_chunk_rows(int64_t m, int64_t k, int64_t chunk_rows) {
     int64_t r = chunk_rows > 0 ? chunk_rows : (int64_t(256) << 20) / (std::max<int64_t>(k, 1) * 4);
     r = std::max<int64_t>(128, (r + 127) / 128 * 128);
@@ -592,38 +589,68 @@ int64_t host_chunk_rows(int64_t m, int64_t k, int64_t chunk_rows) {
     return r;
 }
 
+// Device workspace of shgemm_host: [column-major copy of a row-major Omega][2 x (A chunk, Y chunk,
+// split-K scratch)]. The split-K scratch is sized for EVERY chunk height up to `chunk` (a short last
+// chunk has fewer m-tiles, may plan more splits and need more scratch than a full one); heights
+// that round up to the same multiple of 128 share the plan's split count and need no more bytes
+// than that multiple, so the multiples of 128 cover all heights.
 struct HostWs {
-    int64_t chunk, lda_s, ldy_s;
-    size_t a_bytes, y_bytes, sk_bytes, total;
+    int64_t chunk, lda_s, ldy_s, ldt;
+    size_t om_bytes, a_bytes, y_bytes, sk_bytes, total;
 };
 
-HostWs host_ws(int64_t m, int64_t n, int64_t k, int64_t chunk_rows) {
+HostWs host_ws(int64_t m, int64_t n, int64_t k, int64_t chunk_rows, bool om_rm) {
     HostWs w{};
     w.chunk = host_chunk_rows(m, k, chunk_rows);
     w.lda_s = (k + 3) / 4 * 4;
     w.ldy_s = (n + 3) / 4 * 4;
+    w.ldt = (k + 7) / 8 * 8;
     auto up = [](size_t b) { return (b + 255) / 256 * 256; };
+    w.om_bytes = om_rm ? up(static_cast<size_t>(n * w.ldt * 2)) : 0;
     w.a_bytes = up(static_cast<size_t>(w.chunk * w.lda_s * 4));
     w.y_bytes = up(static_cast<size_t>(w.chunk * w.ldy_s * 4));
-    const Plan pl = make_plan(w.chunk, n, k, true, nullptr, std::max(1, dev_info().sms));
-    w.sk_bytes = up(static_cast<size_t>(pl.ws_bytes));
-    w.total = 2 * (w.a_bytes + w.y_bytes + w.sk_bytes);
+    shg_tune_t col{};
+    col.omega_layout = SHG_OMEGA_COL_MAJOR;
+    size_t sk = 0;
+    const int sms = std::max(1, dev_info().sms);
+    for (int64_t rows = 128; rows <= w.chunk; rows += 128)
+        sk = std::max(sk, static_cast<size_t>(make_plan(rows, n, k, true, &col, sms).ws_bytes));
+    w.sk_bytes = up(sk);
+    w.total = w.om_bytes + 2 * (w.a_bytes + w.y_bytes + w.sk_bytes);
     return w;
 }
+
+bool omega_layout_ok(const shg_tune_t* t) {
+    return !t || t->omega_layout == SHG_OMEGA_ROW_MAJOR || t->omega_layout == SHG_OMEGA_COL_MAJOR;
+}
+bool omega_row_major(const shg_tune_t* t) { return !t || t->omega_layout == SHG_OMEGA_ROW_MAJOR; }
 
 }  // namespace
 
 extern "C" {
 
 shg_status_t gen_omega_f16_ex(int64_t k, int64_t n, uint64_t seed, int dist, uint32_t stream_id, int64_t row0,
-                              int64_t k_total, uint16_t* Omega, int64_t ldo, shg_stream_t stream) {
+                              int64_t k_total, uint16_t* Omega, int64_t ldo, int layout, shg_stream_t stream) {
     if (k < 0 || n < 0 || row0 < 0 || dist < 0 || dist > 3) return SHG_ERR_INVALID_VALUE;
+    if (layout != SHG_OMEGA_ROW_MAJOR && layout != SHG_OMEGA_COL_MAJOR) return SHG_ERR_INVALID_VALUE;
     if (k == 0 || n == 0) return SHG_OK;
-    if (!Omega || ldo < k) return SHG_ERR_INVALID_VALUE;
+    if (!Omega || ldo < (layout == SHG_OMEGA_ROW_MAJOR ? n : k)) return SHG_ERR_INVALID_VALUE;
     if (dist == SHG_DIST_VERYSPARSE && k_total < 1) return SHG_ERR_INVALID_VALUE;
-    const bool vec = ((reinterpret_cast<uintptr_t>(Omega) & 7u) == 0) && (ldo % 4 == 0) && (row0 % 4 == 0);
     const int64_t nq = ((row0 + k - 1) >> 2) - (row0 >> 2) + 1;
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    if (layout == SHG_OMEGA_ROW_MAJOR) {
+        const int sms = std::max(1, dev_info().sms);
+        const int64_t gx = (n + 31) / 32;
+        const int64_t gy = std::max<int64_t>(1, std::min<int64_t>((nq + 7) / 8, (int64_t(sms) * 16 + gx - 1) / gx));
+        if (gx > 2147483647 || gy > 65535) return SHG_ERR_INVALID_VALUE;
+        shg::omega::gen_omega_rowmajor_kernel<<<dim3(static_cast<unsigned>(gx), static_cast<unsigned>(gy)), dim3(32, 8),
+                                                0, s>>>(k, n, seed, stream_id, row0, dist,
+                                                        sparse_threshold(dist, k_total), Omega, ldo);
+        g_launches.fetch_add(1, std::memory_order_relaxed);
+        SHG_CUDA(cudaGetLastError());
+        return SHG_OK;
+    }
+    const bool vec = ((reinterpret_cast<uintptr_t>(Omega) & 7u) == 0) && (ldo % 4 == 0) && (row0 % 4 == 0);
     shg::omega::gen_omega_kernel<<<omega_grid(nq, n), 256, 0, s>>>(k, n, seed, stream_id, row0, dist,
                                                                   sparse_threshold(dist, k_total), Omega, ldo, vec);
     g_launches.fetch_add(1, std::memory_order_relaxed);
@@ -666,7 +693,7 @@ shg_status_t shgemm_tiled(int64_t m, int64_t n, int64_t k, const float* A, int64
 
 shg_status_t gen_omega_f16(int64_t k, int64_t n, uint64_t seed, int dist, uint16_t* Omega, int64_t ldo,
                            shg_stream_t stream) {
-    return gen_omega_f16_ex(k, n, seed, dist, 0u, 0, k, Omega, ldo, stream);
+    return gen_omega_f16_ex(k, n, seed, dist, 0u, 0, k, Omega, ldo, SHG_OMEGA_ROW_MAJOR, stream);
 }
 
 shg_status_t shgemm_ex(int64_t m, int64_t n, int64_t k, const float* A, int64_t lda, const uint16_t* Omega,
@@ -675,12 +702,14 @@ shg_status_t shgemm_ex(int64_t m, int64_t n, int64_t k, const float* A, int64_t 
     if (m < 0 || n < 0 || k < 0) return SHG_ERR_INVALID_VALUE;
     if (m == 0 || n == 0) return SHG_OK;
     if (!Y || ldc < n) return SHG_ERR_INVALID_VALUE;
-    if (k > 0 && (!A || !Omega || lda < k || ldo < k)) return SHG_ERR_INVALID_VALUE;
+    if (!omega_layout_ok(tune)) return SHG_ERR_INVALID_VALUE;
+    const bool om_rm = omega_row_major(tune);
+    if (k > 0 && (!A || !Omega || lda < k || ldo < (om_rm ? n : k))) return SHG_ERR_INVALID_VALUE;
     if (tune && tune->bn > 0 && !valid_bn(tune->bn)) return SHG_ERR_INVALID_VALUE;
     if (tune && tune->tc != SHG_TC_FP16 && tune->tc != SHG_TC_TF32) return SHG_ERR_INVALID_VALUE;
     AView av{A, k, 1, lda, lda * std::max<int64_t>(m, 1)};
     return run_shgemm(m, n, k, av, Omega, ldo, Y, ldc, tune, workspace, workspace_bytes, nonfinite_flag,
-                      reinterpret_cast<cudaStream_t>(stream));
+                      reinterpret_cast<cudaStream_t>(stream), nullptr, 0, 0, false, nullptr, om_rm);
 }
 
 shg_status_t shgemm(int64_t m, int64_t n, int64_t k, const float* A, int64_t lda, const uint16_t* Omega,
@@ -701,12 +730,14 @@ shg_status_t shgemm_at(int64_t m, int64_t n, int64_t k, const float* At, int64_t
     if (m < 0 || n < 0 || k < 0) return SHG_ERR_INVALID_VALUE;
     if (m == 0 || n == 0) return SHG_OK;
     if (!Y || ldc < n) return SHG_ERR_INVALID_VALUE;
-    if (k > 0 && (!At || !Omega || ldat < m || ldo < k)) return SHG_ERR_INVALID_VALUE;
+    if (!omega_layout_ok(tune)) return SHG_ERR_INVALID_VALUE;
+    const bool om_rm = omega_row_major(tune);
+    if (k > 0 && (!At || !Omega || ldat < m || ldo < (om_rm ? n : k))) return SHG_ERR_INVALID_VALUE;
     if (tune && tune->bn > 0 && !valid_bn(tune->bn)) return SHG_ERR_INVALID_VALUE;
     if (tune && tune->tc != SHG_TC_FP16 && tune->tc != SHG_TC_TF32) return SHG_ERR_INVALID_VALUE;
     AView av{At, k, 1, ldat, 0, true};
     return run_shgemm(m, n, k, av, Omega, ldo, Y, ldc, tune, workspace, workspace_bytes, nonfinite_flag,
-                      reinterpret_cast<cudaStream_t>(stream));
+                      reinterpret_cast<cudaStream_t>(stream), nullptr, 0, 0, false, nullptr, om_rm);
 }
 
 shg_status_t tcec_sgemm_ex(int64_t m, int64_t n, int64_t k, const float* A, int64_t lda, int a_layout, const float* B,
@@ -765,14 +796,15 @@ shg_status_t tcec_plan(int64_t m, int64_t n, int64_t k, const shg_tune_t* tune, 
 
 size_t shg_workspace_size(int64_t m, int64_t n, int64_t k, const shg_tune_t* tune) {
     if (m <= 0 || n <= 0 || k <= 0) return 0;
-    const Plan pl = make_plan(m, n, k, true, tune, std::max(1, dev_info().sms));
+    const Plan pl = make_plan(m, n, k, true, tune, std::max(1, dev_info().sms), false, omega_row_major(tune));
     return static_cast<size_t>(pl.ws_bytes);
 }
 
 shg_status_t shg_plan(int64_t m, int64_t n, int64_t k, const shg_tune_t* tune, shg_plan_t* out) {
     if (!out || m < 0 || n < 0 || k < 0) return SHG_ERR_INVALID_VALUE;
     const int sms = std::max(1, dev_info().sms);
-    const Plan pl = make_plan(m, n, k, true, tune, sms);
+    if (!omega_layout_ok(tune)) return SHG_ERR_INVALID_VALUE;
+    const Plan pl = make_plan(m, n, k, true, tune, sms, false, omega_row_major(tune));
     if (pl.path < 0) return SHG_ERR_INVALID_VALUE;
     std::memset(out, 0, sizeof(*out));
     out->path = pl.path;
@@ -785,7 +817,7 @@ shg_status_t shg_plan(int64_t m, int64_t n, int64_t k, const shg_tune_t* tune, s
         out->cta_pair = pl.pair ? 1 : 0;
         out->tc = pl.tf32 ? SHG_TC_TF32 : SHG_TC_FP16;
         out->omega_mcast = pl.np;
-        out->kernels = 1 + (pl.splits > 1 ? 1 : 0) + (pl.tf32 ? 1 : 0);
+        out->kernels = 1 + (pl.splits > 1 ? 1 : 0) + (pl.tf32 || pl.ldt > 0 ? 1 : 0);
     } else {
         out->kernels = pl.path == 1 ? 1 : (k == 0 && m > 0 && n > 0 ? 0 : 0);
     }
@@ -912,7 +944,7 @@ shg_status_t project_impl(const float* A, int ndim, const int64_t* dims, int mod
         st = om_tiled ? gen_omega_f16_tiled(K, n, seed, dist, static_cast<uint32_t>(mode), omega_row0, k_total, Om,
                                             stream)
                       : gen_omega_f16_ex(K, n, seed, dist, static_cast<uint32_t>(mode), omega_row0, k_total, Om,
-                                         ldo, stream);
+                                         ldo, SHG_OMEGA_COL_MAJOR, stream);
         if (st != SHG_OK) return finish(st);
     } else if (dist == SHG_DIST_VERYSPARSE && k_total < 1) {
         return finish(SHG_ERR_INVALID_VALUE);
@@ -951,59 +983,108 @@ shg_status_t project(const float* A, int ndim, const int64_t* dims, int mode, in
     return project_ex(A, ndim, dims, mode, n, seed, dist, SHG_TC_FP16, W, ldw, workspace, workspace_bytes, stream);
 }
 
-size_t shg_host_workspace_size(int64_t n, int64_t k, int64_t chunk_rows) {
+size_t shg_host_workspace_size(int64_t n, int64_t k, int64_t chunk_rows, int omega_layout) {
     if (n <= 0 || k <= 0) return 0;
-    return host_ws(0, n, k, chunk_rows).total;
+    if (omega_layout != SHG_OMEGA_ROW_MAJOR && omega_layout != SHG_OMEGA_COL_MAJOR) return 0;
+    return host_ws(0, n, k, chunk_rows, omega_layout == SHG_OMEGA_ROW_MAJOR).total;
 }
 
 shg_status_t shgemm_host(int64_t m, int64_t n, int64_t k, const float* A_host, int64_t lda, const uint16_t* Omega,
-                         int64_t ldo, float* Y_host, int64_t ldc, int64_t chunk_rows, void* workspace,
-                         size_t workspace_bytes, shg_stream_t stream) {
+                         int64_t ldo, int omega_layout, float* Y_host, int64_t ldc, int64_t chunk_rows,
+                         void* workspace, size_t workspace_bytes, shg_stream_t stream) {
     if (m < 0 || n < 0 || k < 0 || chunk_rows < 0) return SHG_ERR_INVALID_VALUE;
+    if (omega_layout != SHG_OMEGA_ROW_MAJOR && omega_layout != SHG_OMEGA_COL_MAJOR) return SHG_ERR_INVALID_VALUE;
+    const bool om_rm = omega_layout == SHG_OMEGA_ROW_MAJOR;
     if (m == 0 || n == 0) return SHG_OK;
-    if (!Y_host || ldc < n || (k > 0 && (!A_host || !Omega || lda < k || ldo < k))) return SHG_ERR_INVALID_VALUE;
+    if (!Y_host || ldc < n || (k > 0 && (!A_host || !Omega || lda < k || ldo < (om_rm ? n : k))))
+        return SHG_ERR_INVALID_VALUE;
     cudaStream_t us = reinterpret_cast<cudaStream_t>(stream);
     if (k == 0) {
         for (int64_t i = 0; i < m; ++i) std::memset(Y_host + i * ldc, 0, n * sizeof(float));
         return SHG_OK;
     }
-    HostStreams& hs = host_streams();
-    if (!hs.ok) return cuda_fail(cudaErrorUnknown, "stream/event creation");
-    const HostWs w = host_ws(m, n, k, chunk_rows);
+    const HostWs w = host_ws(m, n, k, chunk_rows, om_rm);
+    if (workspace && workspace_bytes < w.total) return SHG_ERR_WORKSPACE;
+    // per-call side streams and events: concurrent calls (other threads, other user streams) share no
+    // library state, so one call's record/wait can never order another call's work
+    cudaStream_t side[2] = {nullptr, nullptr};
+    cudaEvent_t ev_start = nullptr, ev_done[2] = {nullptr, nullptr};
     void* own = nullptr;
+    bool joined = false;
+    // every exit after the first enqueue goes through here: the user stream waits for whatever the
+    // side streams have enqueued (so no copy into the workspace or the caller's buffers is still in
+    // flight once the caller synchronises `stream`), owned scratch is freed on `stream`, and the
+    // streams / events are released (destroying them with work pending is legal; the work completes)
+    auto cleanup = [&](shg_status_t st) -> shg_status_t {
+        for (int b = 0; b < 2; ++b) {
+            if (side[b] && ev_done[b] && !joined) {
+                if (cudaEventRecord(ev_done[b], side[b]) == cudaSuccess) cudaStreamWaitEvent(us, ev_done[b], 0);
+            }
+        }
+        joined = true;
+        if (own) {
+            const cudaError_t e = cudaFreeAsync(own, us);
+            if (st == SHG_OK && e != cudaSuccess) st = cuda_fail(e, "cudaFreeAsync");
+        }
+        for (int b = 0; b < 2; ++b) {
+            if (side[b]) cudaStreamDestroy(side[b]);
+            if (ev_done[b]) cudaEventDestroy(ev_done[b]);
+        }
+        if (ev_start) cudaEventDestroy(ev_start);
+        return st;
+    };
+    auto fail = [&](cudaError_t e, const char* what) { return cleanup(cuda_fail(e, what)); };
+    cudaError_t e = cudaSuccess;
+    for (int b = 0; b < 2 && e == cudaSuccess; ++b) {
+        e = cudaStreamCreateWithFlags(&side[b], cudaStreamNonBlocking);
+        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ev_done[b], cudaEventDisableTiming);
+    }
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ev_start, cudaEventDisableTiming);
+    if (e != cudaSuccess) return fail(e, "shgemm_host stream/event creation");
     uint8_t* ws = static_cast<uint8_t*>(workspace);
     if (!ws) {
-        SHG_CUDA(cudaMallocAsync(&own, w.total, us));
+        e = cudaMallocAsync(&own, w.total, us);
+        if (e != cudaSuccess) return fail(e, "cudaMallocAsync");
         ws = static_cast<uint8_t*>(own);
-    } else if (workspace_bytes < w.total) {
-        return SHG_ERR_WORKSPACE;
     }
-    SHG_CUDA(cudaEventRecord(hs.ev_start, us));
-    for (int b = 0; b < 2; ++b) SHG_CUDA(cudaStreamWaitEvent(hs.s[b], hs.ev_start, 0));
+    // a row-major Omega is transposed ONCE into the column-major layout the chunks stream
+    const uint16_t* Om = Omega;
+    int64_t ldo_c = ldo;
+    if (om_rm) {
+        uint16_t* Ot = reinterpret_cast<uint16_t*>(ws);
+        const int64_t tiles = ((k + 31) / 32) * ((n + 31) / 32);
+        shg::transpose_omega_kernel<<<static_cast<int>(std::min<int64_t>(tiles, int64_t(std::max(1, dev_info().sms)) * 8)),
+                                      dim3(32, 8), 0, us>>>(Omega, k, n, ldo, Ot, w.ldt);
+        g_launches.fetch_add(1, std::memory_order_relaxed);
+        e = cudaGetLastError();
+        if (e != cudaSuccess) return fail(e, "transpose_omega_kernel");
+        Om = Ot;
+        ldo_c = w.ldt;
+    }
+    if ((e = cudaEventRecord(ev_start, us)) != cudaSuccess) return fail(e, "cudaEventRecord");
+    for (int b = 0; b < 2; ++b)
+        if ((e = cudaStreamWaitEvent(side[b], ev_start, 0)) != cudaSuccess) return fail(e, "cudaStreamWaitEvent");
+    shg_tune_t col{};
+    col.omega_layout = SHG_OMEGA_COL_MAJOR;
     const int64_t nchunks = (m + w.chunk - 1) / w.chunk;
     for (int64_t c = 0; c < nchunks; ++c) {
         const int b = static_cast<int>(c & 1);
-        cudaStream_t s = hs.s[b];
-        uint8_t* base = ws + b * (w.a_bytes + w.y_bytes + w.sk_bytes);
+        cudaStream_t s = side[b];
+        uint8_t* base = ws + w.om_bytes + b * (w.a_bytes + w.y_bytes + w.sk_bytes);
         float* As = reinterpret_cast<float*>(base);
         float* Ys = reinterpret_cast<float*>(base + w.a_bytes);
         void* sk = w.sk_bytes ? base + w.a_bytes + w.y_bytes : nullptr;
         const int64_t r0 = c * w.chunk;
         const int64_t rows = std::min(w.chunk, m - r0);
-        SHG_CUDA(cudaMemcpy2DAsync(As, w.lda_s * 4, A_host + r0 * lda, lda * 4, k * 4, rows,
-                                   cudaMemcpyHostToDevice, s));
-        shg_status_t st = shgemm_ex(rows, n, k, As, w.lda_s, Omega, ldo, Ys, w.ldy_s, nullptr, sk, w.sk_bytes,
-                                    nullptr, reinterpret_cast<shg_stream_t>(s));
-        if (st != SHG_OK) return st;
-        SHG_CUDA(cudaMemcpy2DAsync(Y_host + r0 * ldc, ldc * 4, Ys, w.ldy_s * 4, n * 4, rows,
-                                   cudaMemcpyDeviceToHost, s));
+        e = cudaMemcpy2DAsync(As, w.lda_s * 4, A_host + r0 * lda, lda * 4, k * 4, rows, cudaMemcpyHostToDevice, s);
+        if (e != cudaSuccess) return fail(e, "cudaMemcpy2DAsync(H2D)");
+        const shg_status_t st = shgemm_ex(rows, n, k, As, w.lda_s, Om, ldo_c, Ys, w.ldy_s, &col, sk, w.sk_bytes,
+                                          nullptr, reinterpret_cast<shg_stream_t>(s));
+        if (st != SHG_OK) return cleanup(st);
+        e = cudaMemcpy2DAsync(Y_host + r0 * ldc, ldc * 4, Ys, w.ldy_s * 4, n * 4, rows, cudaMemcpyDeviceToHost, s);
+        if (e != cudaSuccess) return fail(e, "cudaMemcpy2DAsync(D2H)");
     }
-    for (int b = 0; b < 2; ++b) {
-        SHG_CUDA(cudaEventRecord(hs.ev_done[b], hs.s[b]));
-        SHG_CUDA(cudaStreamWaitEvent(us, hs.ev_done[b], 0));
-    }
-    if (own) SHG_CUDA(cudaFreeAsync(own, us));
-    return SHG_OK;
+    return cleanup(SHG_OK);
 }
 
 shg_status_t shg_probe_tma_read(const float* A, int64_t m, int64_t k, int64_t lda, int layout, int box_k,

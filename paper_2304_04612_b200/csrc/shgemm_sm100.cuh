@@ -767,7 +767,12 @@ shgemm_sm100_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_const
         if (warp == kWarpProdA) {
             // ======================================================== A stager (TMA, FP32, own rows)
             if (elect_one()) {
-                const uint64_t pol = policy_evict_first();
+                // A is streamed once: evict_first, unless several N tiles of an m-block read the same
+                // A stages (n > BN). Those tiles are consecutive in the n-fastest tile order, so
+                // they run concurrently on neighbouring CTAs; evict_normal keeps a stage in L2
+                // until its last reader has fetched it, so A comes from HBM once instead of
+                // n_tiles times (PAPER.md:652 counts mnk/b_n loads of A on the A100 design).
+                const uint64_t pol = p.n_tiles > 1 ? policy_evict_normal() : policy_evict_first();
                 uint32_t sa = 0, pa = 0;
                 long long w = 0;
                 for (int tile = cta_of_tile; tile < num_tiles; tile += tile_stride) {

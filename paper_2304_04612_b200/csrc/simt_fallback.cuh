@@ -10,16 +10,17 @@
 namespace shg {
 
 // A element (i, l) at A[i * sa_row + l * sa_col] (row-major: sa_row = lda, sa_col = 1;
-// M-major: sa_row = 1, sa_col = lda).
+// M-major: sa_row = 1, sa_col = lda). Omega element (l, j) at Om[l * so_k + j * so_n] (column-major:
+// so_k = 1, so_n = ldo; row-major: so_k = ldo, so_n = 1).
 __global__ void shgemm_simt_kernel(int64_t m, int64_t n, int64_t k, const float* __restrict__ A, int64_t sa_row,
-                                   int64_t sa_col, const uint16_t* __restrict__ Om, int64_t ldo, float* __restrict__ Y,
-                                   int64_t ldc, int* nonfinite, bool tf32) {
+                                   int64_t sa_col, const uint16_t* __restrict__ Om, int64_t so_k, int64_t so_n,
+                                   float* __restrict__ Y, int64_t ldc, int* nonfinite, bool tf32) {
     const int64_t total = m * n;
     for (int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; t < total;
          t += static_cast<int64_t>(gridDim.x) * blockDim.x) {
         const int64_t i = t / n, j = t - (t / n) * n;
         const float* a = A + i * sa_row;
-        const uint16_t* w = Om + j * ldo;
+        const uint16_t* w = Om + j * so_n;
         float acc = 0.0f;
         for (int64_t k0 = 0; k0 < k; k0 += 64) {
             const int64_t k1 = k0 + 64 < k ? k0 + 64 : k;
@@ -37,7 +38,7 @@ __global__ void shgemm_simt_kernel(int64_t m, int64_t n, int64_t k, const float*
                     hf = __half2float(__ushort_as_half(static_cast<uint16_t>(h & 0xFFFFu)));
                     lf = __half2float(__ushort_as_half(static_cast<uint16_t>(lo & 0xFFFFu)));
                 }
-                const float wf = __half2float(__ushort_as_half(w[l]));
+                const float wf = __half2float(__ushort_as_half(w[l * so_k]));
                 s_hi = __fmaf_rn(hf, wf, s_hi);
                 s_lo = __fmaf_rn(lf, wf, s_lo);
             }
@@ -50,14 +51,42 @@ __global__ void shgemm_simt_kernel(int64_t m, int64_t n, int64_t k, const float*
 
 // SHGEMM-TF32's B operand: Omega's FP16 values widened exactly to FP32/TF32 bit patterns (P:498:
 // "converted to TF32 ... before input to Tensor Cores"; tcgen05 reads B from shared memory, so the
-// widening is done once in global memory instead of per tile in registers). Column-major k x n.
-__global__ void widen_omega_kernel(const uint16_t* __restrict__ Om, int64_t k, int64_t n, int64_t ldo,
+// widening is done once in global memory instead of per tile in registers). Input element (r, j)
+// at Om[r * so_k + j * so_n] (either layout); output column-major k x n (ldo32).
+__global__ void widen_omega_kernel(const uint16_t* __restrict__ Om, int64_t k, int64_t n, int64_t so_k, int64_t so_n,
                                    float* __restrict__ Om32, int64_t ldo32) {
     const int64_t total = k * n;
     for (int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; t < total;
          t += static_cast<int64_t>(gridDim.x) * blockDim.x) {
         const int64_t j = t / k, r = t - (t / k) * k;
-        Om32[j * ldo32 + r] = __half2float(__ushort_as_half(Om[j * ldo + r]));
+        Om32[j * ldo32 + r] = __half2float(__ushort_as_half(Om[r * so_k + j * so_n]));
+    }
+}
+
+// A ROW-major Omega (element (l, j) at Om[l * ldo + j]) copied bit for bit into the
+// column-major layout (Ot[j * ldt + l]) that the tensor-core path streams as its K-major B operand
+// (tcgen05 reads B from shared memory through TMA, which cannot transpose 2-byte elements). 32 x 32
+// tiles through shared memory: both the reads (along j) and the writes (along l) are coalesced.
+// blockDim = (32, 8); rows l in [k, ldt) are not written.
+__global__ void transpose_omega_kernel(const uint16_t* __restrict__ Om, int64_t k, int64_t n, int64_t ldo,
+                                       uint16_t* __restrict__ Ot, int64_t ldt) {
+    __shared__ uint16_t tile[32][33];
+    const int64_t tk_n = (k + 31) / 32, tn_n = (n + 31) / 32;
+    const int tx = static_cast<int>(threadIdx.x), ty = static_cast<int>(threadIdx.y);
+    for (int64_t t = blockIdx.x; t < tk_n * tn_n; t += gridDim.x) {
+        const int64_t tk = t / tn_n, tn = t - tk * tn_n;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const int64_t l = tk * 32 + ty + 8 * i, j = tn * 32 + tx;
+            tile[ty + 8 * i][tx] = (l < k && j < n) ? Om[l * ldo + j] : uint16_t(0);
+        }
+        __syncthreads();
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const int64_t j = tn * 32 + ty + 8 * i, l = tk * 32 + tx;
+            if (l < k && j < n) Ot[j * ldt + l] = tile[tx][ty + 8 * i];
+        }
+        __syncthreads();
     }
 }
 

@@ -181,6 +181,25 @@ def core_tcec(T: torch.Tensor, Qs) -> torch.Tensor:
     return g
 
 
+def _tc_view(dims, mode) -> bool:
+    """True if project() reads the mode-`mode` unfolding of a 16-B-aligned C-order tensor with `dims`
+    on the tcgen05 path (the only path that streams a caller's k-tiled Omega; csrc/api.cu
+    project_impl): mode 0 is a K-major matrix with row stride K (K % 4 == 0), the last mode an M-major
+    view with row stride M (M % 4 == 0), a middle mode a 3-D view (S % 32 == 0) or a padded copy."""
+    M, K = dims[mode], 1
+    for i, d in enumerate(dims):
+        if i != mode:
+            K *= d
+    S = 1
+    for d in dims[mode + 1:]:
+        S *= d
+    if mode == 0:
+        return K % 4 == 0
+    if S == 1:
+        return M % 4 == 0
+    return True
+
+
 def rp_hosvd(T: torch.Tensor, ranks, seed: int = 0, dist="gaussian", projection="shgemm", timing=False,
              gemm: str = "sgemm", factor: str = "cusolver", check: bool = True):
     """Alg 2: for each mode W = A'_(i) Omega_(i) (project, stream_id = mode), Q_i = QR(W);
@@ -202,6 +221,8 @@ def rp_hosvd(T: torch.Tensor, ranks, seed: int = 0, dist="gaussian", projection=
             numel = T.numel()
             with torch.cuda.stream(side):
                 for i, J in enumerate(ranks):
+                    if not _tc_view(list(T.shape), i):   # project() generates its own Omega there
+                        continue
                     oms[i] = gen_omega_tiled(numel // T.shape[i], J, seed=seed, dist=dist, stream_id=i,
                                              device=T.device)
                     ready[i] = torch.cuda.Event()

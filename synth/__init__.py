@@ -132,9 +132,11 @@ def alg3_tensor(dims, ranks, pad: int, seed: int, noise: float = 0.0) -> np.ndar
     return G.astype(np.float32)
 
 
-def alg3_tensor_torch(dims, ranks, pad: int, seed: int, device="cuda"):
+def alg3_tensor_torch(dims, ranks, pad: int, seed: int, device="cuda", noise: float = 0.0):
     """alg3_tensor's construction (same random draws) evaluated with torch in FP64 on `device`, FP32
-    result — for the 1024^3 RP-HOSVD input of the bench (the numpy version takes minutes)."""
+    result — for the 1024^3 RP-HOSVD input of the bench (the numpy version takes minutes). noise > 0
+    adds noise * N(0,1) from torch's generator seeded with `seed` (the noisy variant of reading c4-18;
+    NOT the numpy variant's draws: both sides of a parity test must use this one tensor)."""
     import torch
     g = rng(seed)
     G = torch.as_tensor(g.uniform(-1.0, 1.0, size=tuple(ranks)), dtype=torch.float64, device=device)
@@ -144,6 +146,11 @@ def alg3_tensor_torch(dims, ranks, pad: int, seed: int, device="cuda"):
         M = torch.as_tensor(Oa @ Ob, dtype=torch.float64, device=device)
         G = torch.movedim(torch.tensordot(G, M, dims=([i], [0])), -1, i)
     G = G / torch.sqrt(torch.mean(G * G))
+    if noise:
+        gen = torch.Generator(device=device).manual_seed(seed)
+        G = G.float()
+        G.add_(torch.randn(G.shape, generator=gen, device=device, dtype=torch.float32), alpha=noise)
+        return G
     return G.float()
 
 

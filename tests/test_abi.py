@@ -78,6 +78,45 @@ def test_argument_validation_without_gpu(shg):
     assert L.tcec_sgemm(4, 0, 4, None, 4, 0, None, 4, 0, None, 4, None) == 0  # n == 0: no-op
 
 
+def test_omega_layout_is_explicit_and_validated(shg):
+    """shgemm()/gen_omega_f16() take a ROW-major Omega (ldo >= n); the _ex calls take
+    the layout explicitly (shg_tune_t.omega_layout / the layout argument). A leading dimension valid
+    only for the other layout is rejected, and so is an unknown layout value."""
+    L = shg.lib()
+    v = ctypes.c_void_p(16)
+    m, n, k = 8, 16, 64
+    # row-major: ldo >= n is valid (here ldo = 16 < k = 64, which column-major would reject)
+    assert L.shgemm(m, n, k, v, k, v, n - 1, v, n, None) == 1              # ldo < n
+    tune = shg.Tune()
+    tune.omega_layout = shg.OMEGA_COL_MAJOR
+    assert L.shgemm_ex(m, n, k, v, k, v, n, v, n, ctypes.byref(tune), None, 0, None, None) == 1   # col: ldo < k
+    tune.omega_layout = 2
+    assert L.shgemm_ex(m, n, k, v, k, v, k, v, n, ctypes.byref(tune), None, 0, None, None) == 1   # bad layout
+    assert L.shgemm_at(m, n, k, v, m, v, k, v, n, ctypes.byref(tune), None, 0, None, None) == 1
+    # gen_omega_f16: row-major, ldo >= n; gen_omega_f16_ex: explicit layout
+    assert L.gen_omega_f16(k, n, 0, 0, v, n - 1, None) == 1
+    assert L.gen_omega_f16_ex(k, n, 0, 0, 0, 0, k, v, n, shg.OMEGA_COL_MAJOR, None) == 1      # col: ldo < k
+    assert L.gen_omega_f16_ex(k, n, 0, 0, 0, 0, k, v, k, 5, None) == 1                         # bad layout
+    assert L.gen_omega_f16_ex(0, n, 0, 0, 0, 0, 1, None, 0, shg.OMEGA_ROW_MAJOR, None) == 0    # k == 0: no-op
+    # shgemm_host: layout argument
+    assert L.shgemm_host(m, n, k, v, k, v, n, 3, v, n, 0, None, 0, None) == 1
+    assert L.shgemm_host(m, n, k, v, k, v, n - 1, shg.OMEGA_ROW_MAJOR, v, n, 0, None, 0, None) == 1
+    assert L.shg_host_workspace_size(n, k, 0, 7) == 0
+
+
+def test_binding_omega_layout_from_strides(shg):
+    torch = pytest.importorskip("torch")
+    k, n = 40, 24
+    col = torch.zeros(n, 48, dtype=torch.float16)[:, :k].t()
+    assert shg.omega_layout(col) == (shg.OMEGA_COL_MAJOR, 48)
+    row = torch.zeros(k, 32, dtype=torch.float16)[:, :n]
+    assert shg.omega_layout(row) == (shg.OMEGA_ROW_MAJOR, 32)
+    assert shg.omega_layout(torch.zeros(k, 1, dtype=torch.float16)) == (shg.OMEGA_COL_MAJOR, k)
+    assert shg.omega_layout(torch.zeros(1, n, dtype=torch.float16)) == (shg.OMEGA_ROW_MAJOR, n)
+    with pytest.raises(ValueError):
+        shg.omega_layout(torch.zeros(k, 2 * n, dtype=torch.float16)[:, ::2])
+
+
 def test_python_binding_has_no_fallback(shg, monkeypatch, tmp_path):
     import importlib
     import paper_2304_04612_b200 as m

@@ -42,3 +42,34 @@ def test_gpu_arm_contract():
     r = d["roofline"]
     assert r["bound"] in ("hbm", "tensor") and 0 < r["frac"] <= 1.05 and r["peak"] > 0
     assert d["e2e"]["h2d_bytes_per_step"] > 0 and d["e2e"]["d2h_bytes_per_step"] > 0
+
+
+def test_gpus_flag_spawns_ranks_gloo():
+    """`bench.py --gpus 2` without WORLD_SIZE (the driver's form) re-launches itself as 2 ranks
+    (torch.distributed.run, 127.0.0.1): rank 0 prints one line with n_gpus == 2 and the rows of both
+    shards (SURVEY §8e row partition) summed over the process group."""
+    env_ws = os.environ.pop("WORLD_SIZE", None)
+    try:
+        d = run_bench("--gpus", "2", "--dry-run", "--steps", "2", "--warmup", "3", timeout=300)
+    finally:
+        if env_ws is not None:
+            os.environ["WORLD_SIZE"] = env_ws
+    assert d["n_gpus"] == 2 and d["dry_run"] is True
+    assert d["rows_covered"] == d["config"]["m"] == 4194304
+    assert d["config"]["rows_per_gpu"] == 2097152 and d["max_rank_plus_one"] == 2
+
+
+def test_row_partition_covers_rows_once():
+    sys.path.insert(0, ROOT)
+    import bench
+    for m in (1, 7, 512, 4194304, 4194305):
+        for g in (1, 2, 3, 4, 8):
+            spans = [bench.row_partition(m, g, r) for r in range(g)]
+            covered = []
+            for per, row0, rows in spans:
+                covered.extend(range(row0, row0 + rows)) if m < 10000 else covered.append((row0, rows))
+            if m < 10000:
+                assert covered == list(range(m))
+            else:
+                assert sum(r for _, r in covered) == m
+                assert all(covered[i][0] + covered[i][1] == covered[i + 1][0] for i in range(g - 1) if covered[i + 1][1])

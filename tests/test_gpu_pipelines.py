@@ -66,6 +66,49 @@ def test_rp_hosvd_matches_oracle_pipeline(shg, pl):
     assert pl.hosvd_error(torch.from_numpy(T0).cuda(), r0["core"], r0["Q"]) <= 1e-5
 
 
+@pytest.mark.parametrize("variant", ["paper", "product"])
+def test_rp_hosvd_config3_full_size_noisy(shg, pl, variant):
+    """BASELINE config 3 at full size (1024^3 FP32, rank 64 per mode) on the NOISY Alg-3 tensor
+    (multilinear rank 60 + 1e-2 N(0,1) noise, reading c4-18: an approximation-dominated residual,
+    e ~ 1e-2, so the 1e-4 relative bar of north_star means something). The GPU pipeline (SHGEMM
+    projections; 'product' also TCEC-SGEMM core and CholeskyQR2) against the FP32 oracle pipeline
+    (oracle/pipelines.rp_hosvd: naive FP32 projections with the same Omega_(i), Householder QR,
+    FP32 mode products) on the same tensor: |e_gpu - e_or| <= 1e-4 e_or."""
+    from oracle import pipelines as opl
+    T = synth.alg3_tensor_torch((1024, 1024, 1024), (64, 64, 64), pad=4, seed=1, noise=1e-2)
+    kw = {"gemm": "tcec", "factor": "gram"} if variant == "product" else {}
+    r = pl.rp_hosvd(T, (64, 64, 64), seed=0, **kw)
+    e_gpu = pl.hosvd_error(T, r["core"], r["Q"])
+    T_h = to_np(T)
+    del T, r
+    torch.cuda.empty_cache()
+    e_or = opl.rp_hosvd(T_h, (64, 64, 64), seed=0, precision="f32")["residual"]
+    assert e_gpu > 1e-3, e_gpu
+    assert abs(e_gpu - e_or) <= 1e-4 * e_or, (e_gpu, e_or)
+
+
+def test_rp_hosvd_config3_full_size_exact_rank(shg, pl):
+    """The exact-rank Alg-3 tensor at 1024^3 (multilinear rank 60 < 64): recovered to roundoff."""
+    T = synth.alg3_tensor_torch((1024, 1024, 1024), (64, 64, 64), pad=4, seed=1)
+    for kw in ({}, {"gemm": "tcec", "factor": "gram"}):
+        r = pl.rp_hosvd(T, (64, 64, 64), seed=0, **kw)
+        assert pl.hosvd_error(T, r["core"], r["Q"]) <= 1e-5
+
+
+@pytest.mark.parametrize("dims", [(50, 50, 50), (64, 9, 9), (30, 7, 33), (13, 40, 22)])
+def test_rp_hosvd_odd_dims(shg, pl, dims):
+    """Unfoldings off the tcgen05 fast path (mode 0 with K % 4 != 0, last mode with I_N % 4 != 0):
+    rp_hosvd precomputes Omega_(i) only where project() can stream it and matches the
+    oracle pipeline."""
+    from oracle import pipelines as opl
+    ranks = tuple(min(8, d) for d in dims)
+    T = synth.alg3_tensor(dims, ranks, pad=2, seed=3, noise=1e-2)
+    r = pl.rp_hosvd(torch.from_numpy(T).cuda(), ranks, seed=1)
+    e_gpu = pl.hosvd_error(torch.from_numpy(T).cuda(), r["core"], r["Q"])
+    e_or = opl.rp_hosvd(T, ranks, seed=1, precision="f32")["residual"]
+    assert abs(e_gpu - e_or) <= 1e-4 * e_or, (e_gpu, e_or)
+
+
 def test_rsvd_config2_full_size(shg, pl):
     """BASELINE config 2: RSVD of a 16384^2 FP32 matrix with a prescribed spectrum, rank 256 + 16.
     GPU pipeline vs the oracle FP32 pipeline on the same input and Omega; Eckart-Young floor."""
