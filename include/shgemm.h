@@ -102,15 +102,20 @@ typedef struct {
                             SHG_ERR_INVALID_VALUE). Ignored for M-major A (shgemm_at). */
     int32_t tc;          /* shg_tc_t: SHG_TC_FP16 (0, default) or SHG_TC_TF32; selects the kernel, not a
                             tuning: the results differ (TF32 keeps |a| >= 65520 finite) */
-    int32_t omega_mcast; /* CTA pairs per cluster sharing each Omega stage by TMA multicast (SHGEMM-FP16
-                            CTA pairs, BN <= 256): 0 auto (= 1), 1 off, 2, 3 or 4 (a ragged last group of
-                            pair tiles runs dummy tiles); SHG_ERR_INVALID_VALUE when forced on a plan
-                            without pairs. Results are bitwise identical for every value. */
+    int32_t omega_mcast; /* 0 or 1 (Omega stages are loaded per CTA pair). The round-1 option of multicasting
+                            them to 2-4 pairs of a cluster was measured without a steady-state gain and
+                            removed; other values: SHG_ERR_INVALID_VALUE. */
     /* Diagnostics: device int64[grid * 16] per-CTA wait-cycle counters (layout in
      * csrc/shgemm_sm100.cuh, enum ProfSlot), or NULL. */
     int64_t *prof;
     int32_t omega_layout; /* shg_omega_layout_t of the Omega argument: SHG_OMEGA_ROW_MAJOR (0, default;
                              ldo >= n) or SHG_OMEGA_COL_MAJOR (ldo >= k). A NULL tune means row-major. */
+    int32_t stream_k;     /* work schedule: 0 auto, 1 force stream-K, 2 whole tiles. Stream-K cuts the
+                             (tile, k-block) iterations into one equal contiguous range per SM (pair)
+                             and sums the partial tiles in-kernel in fixed k order (deterministic);
+                             auto uses it when whole tiles would leave the last wave < 92% busy
+                             (one N tile, >= half as many tiles as SMs (pairs), k >= 1024). Forcing it
+                             on a plan with several N tiles or split_k > 1: SHG_ERR_INVALID_VALUE. */
 } shg_tune_t;
 
 /* Plan the library would use for an (m, n, k) shgemm on the current device. */
@@ -120,7 +125,8 @@ typedef struct {
     int32_t kernels;     /* kernel launches one call makes */
     int32_t cta_pair;    /* 1 if the mainloop runs as CTA pairs (cluster of 2, cta_group::2) */
     int32_t tc;          /* shg_tc_t the plan runs */
-    int32_t omega_mcast; /* CTA pairs per cluster sharing Omega stages (1 = no multicast) */
+    int32_t omega_mcast; /* always 1 (no Omega multicast) */
+    int32_t stream_k;    /* 1 if the plan uses the stream-K schedule (shg_tune_t.stream_k) */
     int64_t workspace_bytes;
 } shg_plan_t;
 

@@ -39,7 +39,7 @@ class Tune(ctypes.Structure):
     _fields_ = [("bn", ctypes.c_int32), ("split_k", ctypes.c_int32), ("max_ctas", ctypes.c_int32),
                 ("force_simt", ctypes.c_int32), ("debug_flags", ctypes.c_int32), ("pair", ctypes.c_int32),
                 ("a_box", ctypes.c_int32), ("tc", ctypes.c_int32), ("omega_mcast", ctypes.c_int32),
-                ("prof", ctypes.c_void_p), ("omega_layout", ctypes.c_int32)]
+                ("prof", ctypes.c_void_p), ("omega_layout", ctypes.c_int32), ("stream_k", ctypes.c_int32)]
 
 
 class Plan(ctypes.Structure):
@@ -47,7 +47,7 @@ class Plan(ctypes.Structure):
                 ("m_tiles", ctypes.c_int32), ("split_k", ctypes.c_int32), ("grid", ctypes.c_int32),
                 ("stages_a", ctypes.c_int32), ("stages_b", ctypes.c_int32), ("smem_bytes", ctypes.c_int32),
                 ("kernels", ctypes.c_int32), ("cta_pair", ctypes.c_int32), ("tc", ctypes.c_int32),
-                ("omega_mcast", ctypes.c_int32), ("workspace_bytes", ctypes.c_int64)]
+                ("omega_mcast", ctypes.c_int32), ("stream_k", ctypes.c_int32), ("workspace_bytes", ctypes.c_int64)]
 
 
 def lib():

@@ -8,8 +8,8 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libshgemm.so")
-SOURCES = ["api.cu", "probes.cu", "tc_f16.cu", "tc_tf32.cu", "tc_tcec.cu", "tc_f16_mc2.cu", "tc_f16_mc4.cu",
-           "tc_f16_gen.cu", "tc_f16_mc3.cu"]
+SOURCES = ["api.cu", "probes.cu", "tc_f16.cu", "tc_f16_mm.cu", "tc_tf32.cu", "tc_tcec.cu",
+           "tc_f16_gen.cu"]
 HEADERS = ["ptx.cuh", "omega.cuh", "split.cuh", "shgemm_sm100.cuh", "simt_fallback.cuh", "probe_tma.cuh", "tcec.cuh",
            "internal.cuh"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")

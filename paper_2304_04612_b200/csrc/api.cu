@@ -209,7 +209,8 @@ struct Plan {
     bool pair = false;
     bool tf32 = false;        // SHGEMM-TF32 (tune->tc == SHG_TC_TF32)
     bool tcec = false;        // TCEC-SGEMM (FP32 B split into B_low / dB_low)
-    int np = 1;               // CTA pairs per cluster sharing Omega stages by multicast
+    bool sk = false;          // stream-K schedule (KParams::sk): equal k-ranges per SM (pair), in-kernel fix-up
+    int64_t sk_planes = 0;    // stream-K: bytes of the partial planes (the counters follow, 256-B aligned)
     // workspace = [split-K planes, 256-B aligned][TF32 copy of Omega | TCEC split of B]
     int64_t ws_bytes = 0, ld_ws = 0, sk_bytes = 0, om_bytes = 0, ldo32 = 0;
     int64_t ldh = 0, noff = 0;  // TCEC: split B column-major, ld ldh; dB_low starts at column noff
@@ -229,14 +230,15 @@ struct OmGen {
     uint32_t* flags;        // ceil(k/64) zero-initialised ready flags
 };
 
-// Omega multicast default (pairs per cluster) when tune->omega_mcast == 0 and the shape allows it
-constexpr int kAutoMcast = 1;
+// Stream-K is planned when whole tiles would leave the last wave under this fraction of the
+// units busy (e.g. 64 pair tiles of RSVD's projection on 74 pairs: 0.86)
+constexpr double kSkMinWaveEff = 0.92;
 
 
 // om_rm: Omega is row-major; the FP16 tensor-core path then reads a column-major copy
 // made in the workspace by transpose_omega_kernel (TF32 widens either layout directly)
 Plan make_plan(int64_t m, int64_t n, int64_t k, bool fast_ok, const shg_tune_t* tune, int sms, bool tcec = false,
-               bool om_rm = false) {
+               bool om_rm = false, bool allow_sk = true) {
     Plan pl;
     pl.tf32 = !tcec && tune && tune->tc == SHG_TC_TF32;
     pl.tcec = tcec;
@@ -275,39 +277,52 @@ Plan make_plan(int64_t m, int64_t n, int64_t k, bool fast_ok, const shg_tune_t* 
         for (int b : kBNs) if (b >= need) { pl.bn = b; break; }
     }
     pl.pair = pair_ok(pl.bn) && want_pair;
-    const int mc = tune ? tune->omega_mcast : 0;   // 0 auto, 1 off, 2 / 4 pairs per cluster
-    if (mc < 0 || mc > 4) { pl.path = -1; return pl; }
+    // Omega multicast across CTA pairs of a cluster was removed in round 2 (no steady-state gain,
+    // DESIGN.md §5): 0 and 1 mean unicast, anything else is rejected
+    const int mc = tune ? tune->omega_mcast : 0;
+    if (mc < 0 || mc > 1) { pl.path = -1; return pl; }
+    const int sk_mode = tune ? tune->stream_k : 0;   // 0 auto, 1 force on, 2 off
+    if (sk_mode < 0 || sk_mode > 2) { pl.path = -1; return pl; }
     const int tile_m = pl.pair ? 2 * shg::kBM : shg::kBM;
-    const int slots = pl.pair ? std::max(1, sms / 2) : sms;     // concurrent tiles
+    int cap = (tune && tune->max_ctas > 0) ? tune->max_ctas : sms;
+    const int cl = pl.pair ? 2 : 1;                 // CTAs per cluster (= per work unit)
+    cap = std::max(cl, cap / cl * cl);
+    const int slots = std::max(1, cap / cl);        // concurrent tiles (work units)
     pl.m_tiles = static_cast<int>((m + tile_m - 1) / tile_m);
-    if (mc >= 2) {
-        if (!pl.pair || pl.tf32 || pl.tcec || wide_bn(pl.bn)) { pl.path = -1; return pl; }
-        pl.np = mc;
-    } else if (mc == 0 && pl.pair && !pl.tf32 && !pl.tcec && !wide_bn(pl.bn) && kAutoMcast > 1 &&
-               pl.m_tiles >= kAutoMcast * 8) {
-        pl.np = kAutoMcast;
-    }
     pl.num_kb = static_cast<int>((k + shg::kBK - 1) / shg::kBK);
     const int64_t mn_tiles = static_cast<int64_t>(pl.m_tiles) * pl.n_tiles;
+    // stream-K (KParams::sk): when whole tiles quantise badly onto the units (the last wave mostly
+    // idle) but there are at least half as many tiles as units; one N tile (the N tiles of an
+    // m-block then share A in L2 by running together); >= 4 k-blocks per unit
+    const int64_t waves = (mn_tiles + slots - 1) / slots;
+    const double wave_eff = static_cast<double>(mn_tiles) / static_cast<double>(waves * slots);
+    const bool sk_fits = allow_sk && pl.n_tiles == 1 && mn_tiles * pl.num_kb >= int64_t(4) * slots &&
+                         !(tune && tune->split_k > 1);
+    pl.sk = sk_fits && (sk_mode == 1 || (sk_mode == 0 && wave_eff < kSkMinWaveEff && 2 * mn_tiles >= slots &&
+                                          pl.num_kb >= 16));
+    if (sk_mode == 1 && !sk_fits) { pl.path = -1; return pl; }
     int splits = 1;
     if (tune && tune->split_k > 0) {
         splits = tune->split_k;
-    } else if (mn_tiles < slots) {
-        // fill the SMs with k-splits, keeping >= 4 k-blocks (256 k) per split
+    } else if (!pl.sk && mn_tiles < slots && pl.num_kb >= 16) {
+        // fill the SMs with k-splits, keeping >= 4 k-blocks (256 k) per split; not for k < 1024,
+        // where the partial planes and the extra reduce launch cost more than the idle SMs
+        // (cfg1, 512 x 512 x 32: split 1/2/4/8 all within 2 us, profiles/r01_small_split.jsonl)
         splits = static_cast<int>(std::max<int64_t>(1, slots / mn_tiles));
         splits = static_cast<int>(std::min<int64_t>(splits, std::max<int64_t>(1, pl.num_kb / 4)));
     }
     splits = std::max(1, std::min(splits, pl.num_kb));
     pl.splits = splits;
     const int64_t tiles = mn_tiles * splits;
-    int cap = (tune && tune->max_ctas > 0) ? tune->max_ctas : sms;
-    const int cl = pl.pair ? 2 * pl.np : 1;        // CTAs per cluster
-    cap = std::max(cl, cap / cl * cl);
-    pl.grid = static_cast<int>(std::min<int64_t>(tiles * (pl.pair ? 2 : 1), cap));
+    pl.grid = pl.sk ? slots * cl : static_cast<int>(std::min<int64_t>(tiles * cl, cap));
     pl.grid = std::max(cl, pl.grid / cl * cl);
     if (splits > 1) {
         pl.ld_ws = (n + 3) / 4 * 4;
         pl.sk_bytes = static_cast<int64_t>(splits) * m * pl.ld_ws * 4;
+    } else if (pl.sk) {
+        // 2 partial slots per unit x CTAs per unit x (BN x 128) floats, then one counter per tile and CTA
+        pl.sk_planes = up256(static_cast<int64_t>(2) * (pl.grid / cl) * cl * pl.bn * shg::kBM * 4);
+        pl.sk_bytes = pl.sk_planes + up256(mn_tiles * cl * 4);
     }
     if (pl.tf32) {   // Omega widened once to TF32 (exact) for the tensor cores' smem operand
         pl.ldo32 = (k + 3) / 4 * 4;
@@ -386,7 +401,7 @@ shg_status_t run_shgemm(int64_t m, int64_t n, int64_t k, const AView& av, const 
     const bool fast_ok = aligned16(av.A) && om_ok && (av.row_stride % 4 == 0) && (av.slab % 4 == 0) &&
                          (plain || av.S % 32 == 0) && encode_fn() != nullptr &&
                          k < (int64_t(1) << 31) && av.S < (int64_t(1) << 31) && m < (int64_t(1) << 31);
-    Plan pl = make_plan(m, n, k, fast_ok, tune, d.sms, tcec, om_rm);
+    Plan pl = make_plan(m, n, k, fast_ok, tune, d.sms, tcec, om_rm, og == nullptr);
     if (pl.path < 0) return SHG_ERR_INVALID_VALUE;
     if (pl.path == 1 && tcec) {
         if (!plain) return SHG_ERR_INVALID_VALUE;
@@ -508,6 +523,14 @@ shg_status_t run_shgemm(int64_t m, int64_t n, int64_t k, const AView& av, const 
     kp.b_lo_col = static_cast<int32_t>(pl.noff);
     kp.om_tiled = om_tiled ? 1 : 0;
     const bool gen = og != nullptr;
+    kp.sk = pl.sk ? 1 : 0;
+    if (pl.sk) {
+        kp.sk_total = static_cast<int64_t>(pl.m_tiles) * pl.n_tiles * pl.num_kb;
+        kp.sk_ws = reinterpret_cast<float*>(wsb);
+        kp.sk_cnt = reinterpret_cast<uint32_t*>(wsb + pl.sk_planes);
+        const cudaError_t e = cudaMemsetAsync(kp.sk_cnt, 0, static_cast<size_t>(pl.sk_bytes - pl.sk_planes), stream);
+        if (e != cudaSuccess) return finish(cuda_fail(e, "cudaMemsetAsync(stream-K counters)"));
+    }
     if (gen) {   // the caller checked om_gen_ok() on this plan
         if (!om_tiled || pl.pair || pl.tf32 || tcec || pl.n_tiles != 1 || pl.bn > kOmGenMaxBn ||
             static_cast<int64_t>(pl.m_tiles) * pl.splits > pl.grid)
@@ -539,9 +562,6 @@ shg_status_t run_shgemm(int64_t m, int64_t n, int64_t k, const AView& av, const 
         kp.nonfinite = nonfinite;
     }
     shg_status_t st = gen ? dispatch_tc_f16_gen(pl.bn, av.mmajor, mapA, mapB0, mapB1, kp, pl.grid, stream)
-                      : pl.np == 2 ? dispatch_tc_f16_mc2(pl.bn, av.mmajor, mapA, mapB0, mapB1, kp, pl.grid, stream)
-                      : pl.np == 3 ? dispatch_tc_f16_mc3(pl.bn, av.mmajor, mapA, mapB0, mapB1, kp, pl.grid, stream)
-                      : pl.np == 4 ? dispatch_tc_f16_mc4(pl.bn, av.mmajor, mapA, mapB0, mapB1, kp, pl.grid, stream)
                       : tcec      ? dispatch_tc_tcec(pl.bn, av.mmajor, pl.pair, mapA, mapB0, mapB1, kp, pl.grid, stream)
                       : pl.tf32 ? dispatch_tc_tf32(pl.bn, av.mmajor, pl.pair, mapA, mapB0, mapB1, kp, pl.grid, stream)
                                 : dispatch_tc_f16(pl.bn, av.mmajor, pl.pair, mapA, mapB0, mapB1, kp, pl.grid, stream);
@@ -788,6 +808,8 @@ shg_status_t tcec_plan(int64_t m, int64_t n, int64_t k, const shg_tune_t* tune, 
         out->stages_b = so_for_tcec(pl.bn, pl.pair);
         out->smem_bytes = smem_for_tcec(pl.bn, pl.pair);
         out->cta_pair = pl.pair ? 1 : 0;
+        out->stream_k = pl.sk ? 1 : 0;
+        out->omega_mcast = 1;
         out->kernels = 2 + (pl.splits > 1 ? 1 : 0);
     }
     out->workspace_bytes = pl.ws_bytes;
@@ -816,7 +838,8 @@ shg_status_t shg_plan(int64_t m, int64_t n, int64_t k, const shg_tune_t* tune, s
         out->smem_bytes = smem_for(pl.bn, pl.pair, pl.tf32);
         out->cta_pair = pl.pair ? 1 : 0;
         out->tc = pl.tf32 ? SHG_TC_TF32 : SHG_TC_FP16;
-        out->omega_mcast = pl.np;
+        out->omega_mcast = 1;
+        out->stream_k = pl.sk ? 1 : 0;
         out->kernels = 1 + (pl.splits > 1 ? 1 : 0) + (pl.tf32 || pl.ldt > 0 ? 1 : 0);
     } else {
         out->kernels = pl.path == 1 ? 1 : (k == 0 && m > 0 && n > 0 ? 0 : 0);
@@ -931,7 +954,7 @@ shg_status_t project_impl(const float* A, int ndim, const int64_t* dims, int mod
     // with their epilogue warps (no separate gen_omega launch, no Omega traffic before the GEMM)
     bool om_gen = false;
     if (om_tiled && tc == SHG_TC_FP16 && omega_row0 % 4 == 0 && omgen_enabled()) {
-        const Plan pl = make_plan(M, n, K, true, &tt, std::max(1, dev_info().sms));
+        const Plan pl = make_plan(M, n, K, true, &tt, std::max(1, dev_info().sms), false, false, false);
         om_gen = pl.path == 0 && !pl.pair && pl.n_tiles == 1 && pl.bn <= kOmGenMaxBn &&
                  static_cast<int64_t>(pl.m_tiles) * pl.splits <= pl.grid;
     }

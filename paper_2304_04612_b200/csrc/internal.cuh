@@ -50,11 +50,11 @@ inline bool valid_bn(int bn) {
     return false;
 }
 
-template <int BN, bool MMAJOR, bool PAIR, bool TF32, bool TCEC = false, int NP = 1, bool OMGEN = false>
+template <int BN, bool MMAJOR, bool PAIR, bool TF32, bool TCEC = false, bool OMGEN = false>
 shg_status_t launch_tc(const CUtensorMap& mapA, const CUtensorMap& mapB0, const CUtensorMap& mapB1,
                        const shg::KParams& kp, int grid, cudaStream_t stream) {
     using CF = shg::Cfg<BN, PAIR, TF32, TCEC>;
-    auto kern = shg::shgemm_sm100_kernel<BN, MMAJOR, PAIR, TF32, TCEC, NP, OMGEN>;
+    auto kern = shg::shgemm_sm100_kernel<BN, MMAJOR, PAIR, TF32, TCEC, OMGEN>;
     static std::once_flag flags[64];
     int dev = 0;
     cudaGetDevice(&dev);
@@ -77,14 +77,15 @@ shg_status_t launch_tc(const CUtensorMap& mapA, const CUtensorMap& mapB0, const 
     cfg.stream = stream;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = PAIR ? 2 * NP : 1;
+    attr[0].val.clusterDim.x = PAIR ? 2 : 1;
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     // The grid is persistent: every cluster must be co-resident, or the clusters that do not fit
-    // run as a second wave. Clusters of 2*NP CTAs must sit in one GPC, so fewer than
-    // #SMs / (2*NP) may fit (GPC sizes are not multiples of 2*NP): clamp to the occupancy query.
+    // run as a second wave. Clusters must sit in one GPC, so fewer than #SMs / 2 may fit (a GPC
+    // with an odd SM count): clamp to the occupancy query. (The kernel reads its unit count from
+    // gridDim, so a stream-K schedule follows the clamped grid.)
     static int max_clusters[64];
     static std::once_flag occ_flags[64];
     const int di = std::min(std::max(dev, 0), 63);
@@ -96,7 +97,7 @@ shg_status_t launch_tc(const CUtensorMap& mapA, const CUtensorMap& mapB0, const 
         }
         max_clusters[di] = nc;
     });
-    constexpr int kCl = PAIR ? 2 * NP : 1;
+    constexpr int kCl = PAIR ? 2 : 1;
     if (max_clusters[di] > 0 && grid > max_clusters[di] * kCl) cfg.gridDim = dim3(max_clusters[di] * kCl);
     SHG_CUDA(cudaLaunchKernelEx(&cfg, kern, mapA, mapB0, mapB1, kp));
     g_launches.fetch_add(1, std::memory_order_relaxed);
@@ -136,6 +137,8 @@ constexpr int kTcecMaxBnSingle = 128;
 // Defined in tc_f16.cu / tc_tf32.cu / tc_tcec.cu (one instantiation set per translation unit).
 shg_status_t dispatch_tc_f16(int bn, bool mmajor, bool pair, const CUtensorMap& a, const CUtensorMap& b0,
                              const CUtensorMap& b1, const shg::KParams& kp, int grid, cudaStream_t s);
+shg_status_t dispatch_tc_f16_mmajor(int bn, bool pair, const CUtensorMap& a, const CUtensorMap& b0,
+                                    const CUtensorMap& b1, const shg::KParams& kp, int grid, cudaStream_t s);
 shg_status_t dispatch_tc_tf32(int bn, bool mmajor, bool pair, const CUtensorMap& a, const CUtensorMap& b0,
                               const CUtensorMap& b1, const shg::KParams& kp, int grid, cudaStream_t s);
 shg_status_t dispatch_tc_tcec(int bn, bool mmajor, bool pair, const CUtensorMap& a, const CUtensorMap& b0,
@@ -144,12 +147,4 @@ shg_status_t dispatch_tc_tcec(int bn, bool mmajor, bool pair, const CUtensorMap&
 shg_status_t dispatch_tc_f16_gen(int bn, bool mmajor, const CUtensorMap& a, const CUtensorMap& b0,
                                  const CUtensorMap& b1, const shg::KParams& kp, int grid, cudaStream_t s);
 constexpr int kOmGenMaxBn = 192;
-// SHGEMM-FP16 CTA pairs with Omega multicast across np = 2 (tc_f16_mc2.cu) or 4 (tc_f16_mc4.cu) pairs
-shg_status_t dispatch_tc_f16_mc2(int bn, bool mmajor, const CUtensorMap& a, const CUtensorMap& b0,
-                                 const CUtensorMap& b1, const shg::KParams& kp, int grid, cudaStream_t s);
-shg_status_t dispatch_tc_f16_mc4(int bn, bool mmajor, const CUtensorMap& a, const CUtensorMap& b0,
-                                 const CUtensorMap& b1, const shg::KParams& kp, int grid, cudaStream_t s);
-shg_status_t dispatch_tc_f16_mc3(int bn, bool mmajor, const CUtensorMap& a, const CUtensorMap& b0,
-                                 const CUtensorMap& b1, const shg::KParams& kp, int grid, cudaStream_t s);
-
 }  // namespace shg_api

@@ -82,6 +82,14 @@ struct KParams {
     uint16_t* om_buf;
     uint32_t* om_flags;
     int* nonfinite;         // optional flag (set to 1 on any non-finite output)
+    // Stream-K schedule (sk = 1; splits == 1): T = m_tiles * n_tiles * num_kb k-block iterations cut
+    // into gridDim/CL equal ranges (next_piece); partial pieces publish their sums in sk_ws
+    // (2 slots per unit x CTAs per unit x BN x 128 floats) and count them in sk_cnt (one zeroed
+    // uint32 per tile and CTA of the unit); the last piece of a tile sums the slots in k order.
+    int32_t sk;
+    int64_t sk_total;
+    float* sk_ws;
+    uint32_t* sk_cnt;
     uint32_t dbg;           // diagnostics: bit0 skip promotion loads, bit1 skip split math, bit2 skip MMAs,
                             //              bit3 skip the Omega TMA (results are wrong when dbg != 0)
     long long* prof;        // diagnostics: per-CTA wait-cycle counters [gridDim.x][16] (ProfSlot)
@@ -206,25 +214,75 @@ struct Cfg {
     static_assert(!(TF32 && TCEC), "TCEC-SGEMM is instantiated for FP16 tensor cores only");
 };
 
-__device__ __forceinline__ void tile_coords(int tile, const KParams& p, int& m_blk, int& s, int& n_blk) {
-    const int per_m = p.splits * p.n_tiles;
-    m_blk = tile / per_m;
-    const int rem = tile - m_blk * per_m;
-    s = rem / p.n_tiles;
-    n_blk = rem - s * p.n_tiles;
+// ------------------------------------------------------------------ work schedule
+// A CTA (pair) = one work unit of `units` = gridDim.x / CL; every role of the CTA walks the same
+// sequence of pieces, each a contiguous k-block range [kb0, kb0 + nkb) of one output tile.
+//  * Tiles (KParams::sk == 0): tiles (m-block, k-split, n-block), n fastest, are dealt round robin
+//    (tile = unit + it * units); split s covers k-blocks [s*num_kb/S, (s+1)*num_kb/S) (an interleaved
+//    assignment, k-block s + it*S, was measured slower on 4-MB-strided rows).
+//  * Stream-K (sk == 1): the T = tiles * num_kb k-block iterations, tile-major, are cut into `units`
+//    equal contiguous ranges [u*T/U, (u+1)*T/U), so every SM pair gets the same work (no partly idle
+//    last wave: 64 pair tiles of RSVD's projection on 74 pairs would otherwise leave 14% of the
+//    tensor cores idle). A range covers the tail of one tile, whole tiles, and the head of another;
+//    the pieces of a tile that one unit does not cover completely are PARTIAL and are summed by the
+//    epilogue of whichever of them finishes last (sk_fixup), in fixed k order.
+struct Piece {
+    int m_blk, n_blk, s;
+    int kb0, nkb;      // global first k-block, k-block count
+    int64_t tile;      // output tile (m_blk * n_tiles + n_blk) (stream-K)
+    int slot;          // stream-K partial-plane slot (2 per unit: its first / last piece), -1 = whole tile
+};
+
+// This unit's stream-K range [g0, g1) of k-block iterations and its first tile, computed once per CTA
+// (64-bit divisions stay out of the roles' loops: the control warps run with 32 registers)
+struct SkRange {
+    int64_t g0, g1, t0;
+};
+
+__device__ __forceinline__ SkRange sk_range(const KParams& p, int unit, int units) {
+    SkRange r{0, 0, 0};
+    if (p.sk) {
+        r.g0 = static_cast<int64_t>(unit) * p.sk_total / units;
+        r.g1 = static_cast<int64_t>(unit + 1) * p.sk_total / units;
+        r.t0 = r.g0 / p.num_kb;
+    }
+    return r;
 }
 
-// Split s covers the contiguous k-block range [s*num_kb/S, (s+1)*num_kb/S); loops run over the
-// local iteration index it in [0, count) and map it to the global k-block with kb_global.
-// (An interleaved assignment, k-block s + it*S, was measured slower on 4-MB-strided rows.)
-__device__ __forceinline__ void kb_range(int s, const KParams& p, int& lo, int& hi) {
-    lo = 0;
-    hi = static_cast<int>((static_cast<int64_t>(s + 1) * p.num_kb) / p.splits -
-                          (static_cast<int64_t>(s) * p.num_kb) / p.splits);
+__device__ __forceinline__ bool next_piece(const KParams& p, int unit, int units, const SkRange& sr, int it,
+                                           Piece& w) {
+    if (!p.sk) {
+        const int tile = unit + it * units;
+        if (tile >= p.m_tiles * p.splits * p.n_tiles) return false;
+        const int per_m = p.splits * p.n_tiles;
+        w.m_blk = tile / per_m;
+        const int rem = tile - w.m_blk * per_m;
+        w.s = rem / p.n_tiles;
+        w.n_blk = rem - w.s * p.n_tiles;
+        w.kb0 = static_cast<int>((static_cast<int64_t>(w.s) * p.num_kb) / p.splits);
+        w.nkb = static_cast<int>((static_cast<int64_t>(w.s + 1) * p.num_kb) / p.splits) - w.kb0;
+        w.tile = tile;
+        w.slot = -1;
+        return true;
+    }
+    // stream-K (the planner guarantees n_tiles == 1 and splits == 1): tile = m-block
+    const int64_t K = p.num_kb;
+    const int64_t tau = sr.t0 + it;
+    const int64_t lo = tau * K > sr.g0 ? tau * K : sr.g0, hi = (tau + 1) * K < sr.g1 ? (tau + 1) * K : sr.g1;
+    if (lo >= hi) return false;
+    w.tile = tau;
+    w.m_blk = static_cast<int>(tau);
+    w.n_blk = 0;
+    w.s = 0;
+    w.kb0 = static_cast<int>(lo - tau * K);
+    w.nkb = static_cast<int>(hi - lo);
+    w.slot = (w.kb0 == 0 && w.nkb == K) ? -1 : 2 * unit + (it == 0 ? 0 : 1);
+    return true;
 }
 
-__device__ __forceinline__ int kb_global(int it, int s, const KParams& p) {
-    return static_cast<int>((static_cast<int64_t>(s) * p.num_kb) / p.splits) + it;
+// stream-K: the unit whose range holds k-block iteration x (the largest u with u*T/U <= x)
+__device__ __forceinline__ int sk_unit_of(int64_t x, int64_t T, int units) {
+    return static_cast<int>(((x + 1) * units - 1) / T);
 }
 
 __device__ __forceinline__ void advance(uint32_t& stage, uint32_t& phase, uint32_t n) {
@@ -273,18 +331,6 @@ __device__ __forceinline__ void commit_to(uint64_t* bar, uint16_t mask = 3) {
     } else {
         tc_commit(bar);
     }
-}
-
-// Omega tile load for CTA pairs, multicast to the CTAs in `mask` (the same half of every pair of
-// the cluster); each destination's transaction bytes land on ITS pair leader's barrier
-__device__ __forceinline__ void tma_load_omega_mc(void* smem_dst, const CUtensorMap* map, uint64_t* bar, int32_t c0,
-                                                  int32_t c1, uint16_t mask, uint64_t policy) {
-    asm volatile(
-        "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster"
-        ".L2::cache_hint [%0], [%1, {%4, %5}], [%2], %3, %6;"
-        ::"r"(smem_u32(smem_dst)), "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar) & kPeerBitMask),
-          "h"(mask), "r"(c0), "r"(c1), "l"(policy)
-        : "memory");
 }
 
 // Omega tile load; in a pair the transaction bytes land on the leader's (even CTA's) barrier.
@@ -414,15 +460,10 @@ __device__ __forceinline__ void acquire_flag(const uint32_t* f) {
 // PAIR          : CTA pair (launch with cluster dims (2,1,1)); see the header comment.
 // TF32          : SHGEMM-TF32 (Cfg's header); mapB0/B1 then describe the FP32 (TF32) copy of Omega.
 // TCEC          : TCEC-SGEMM (Cfg's header): two B tiles per stage, three MMA groups per chunk.
-// NP            : CTA pairs per cluster (PAIR only). NP > 1 runs NP pairs on NP consecutive m-blocks in
-//                 lockstep (a ragged last group runs dummy tiles) and MULTICASTS every Omega stage to them: stage t
-//                 of chunk c is loaded by pair (c*KC + t) % NP into the same half of every pair, so
-//                 Omega's L2 reads drop NP-fold (the power-cap lever). Chunk slots are
-//                 released to all pairs (ch_empty counts NP commits).
 // OMGEN         : cooperative in-kernel Omega (KParams::om_gen; single CTAs, SHGEMM-FP16, k-tiled Omega,
 //                 one tile per CTA): compiled only into the instantiations project() uses for it, so
 //                 the other kernels' epilogues carry no generator registers.
-template <int BN, bool MMAJOR, bool PAIR, bool TF32 = false, bool TCEC = false, int NP = 1, bool OMGEN = false>
+template <int BN, bool MMAJOR, bool PAIR, bool TF32 = false, bool TCEC = false, bool OMGEN = false>
 __global__ void __launch_bounds__(kThreads, 1)
 shgemm_sm100_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB0,
                     const __grid_constant__ CUtensorMap mapB1, const KParams p) {
@@ -450,35 +491,25 @@ shgemm_sm100_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_const
     uint64_t* acc_full = ch_empty + NCH;     // D slot complete                     (tcgen05.commit)
     uint64_t* acc_empty = acc_full + NSLOT;  // D slot drained                      (leader: 4|8 warps, SPLITH 8|16)
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + NSLOT);
+    uint32_t* sk_flag = tmem_slot + 1;       // stream-K: "this CTA sums the tile" (epilogue broadcast)
 
     const uint32_t warp = warp_id();
     const uint32_t lane = threadIdx.x & 31u;
-    static_assert(NP == 1 || (PAIR && NP >= 2 && NP <= 4), "Omega multicast needs CTA pairs");
     static_assert(!OMGEN || (!PAIR && !TF32 && !TCEC && BN <= 192), "in-kernel Omega: single-CTA SHGEMM-FP16");
-    constexpr int CL = PAIR ? 2 * NP : 1;                         // CTAs per cluster
-    const uint32_t crank_cl = PAIR ? cluster_ctarank() : 0u;
-    const uint32_t crank = crank_cl & 1u;                         // rank in the pair: 0 = leader (issues the MMAs)
-    const uint32_t pp = crank_cl >> 1;                            // pair index in the cluster
-    const uint32_t lead = crank_cl & ~1u;                         // cluster rank of this pair's leader
-    const uint16_t pair_mask = static_cast<uint16_t>(3u << lead);
-    const uint16_t cl_mask = static_cast<uint16_t>((1u << CL) - 1u);
-    uint16_t half_mask = 0;                                       // this half in every pair of the cluster
-#pragma unroll
-    for (int q = 0; q < NP; ++q) half_mask |= static_cast<uint16_t>(1u << (2 * q + static_cast<int>(crank)));
-    const int cta_of_tile = static_cast<int>(blockIdx.x) / CL;
-    const int tile_stride = static_cast<int>(gridDim.x) / CL;
+    constexpr int CL = PAIR ? 2 : 1;                              // CTAs per cluster
+    const uint32_t crank = PAIR ? cluster_ctarank() : 0u;         // rank in the pair: 0 = leader (issues the MMAs)
+    const uint32_t lead = 0u;                                     // cluster rank of the pair's leader
+    const uint16_t pair_mask = 3u;
+    const int unit = static_cast<int>(blockIdx.x) / CL;           // this CTA's (pair's) work unit
+    const int units = static_cast<int>(gridDim.x) / CL;
+    const SkRange sr = sk_range(p, unit, units);
     constexpr int kPair = PAIR ? 2 : 1;
-    // cluster tiles (m-group, k-split, n-block); pair pp of the cluster takes m-block mg * NP + pp
-    auto coords = [&](int tile, int& m_blk, int& s, int& n_blk) {
-        tile_coords(tile, p, m_blk, s, n_blk);
-        m_blk = m_blk * NP + static_cast<int>(pp);
-    };
 
     if (threadIdx.x == 0) {
         for (int i = 0; i < SA; ++i) { mbar_init(&a_full[i], 1); mbar_init(&a_empty[i], kNumSplitWarps); }
         for (int i = 0; i < NCH; ++i) {
             mbar_init(&ch_ready[i], kPair * (kNumSplitWarps + 1));
-            mbar_init(&ch_empty[i], NP);
+            mbar_init(&ch_empty[i], 1);
         }
         for (int i = 0; i < NSLOT; ++i) { mbar_init(&acc_full[i], 1); mbar_init(&acc_empty[i], (SPLITH ? 8 : 4) * kPair); }
         fence_mbar_init();
@@ -502,9 +533,6 @@ shgemm_sm100_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_const
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
 
-    // m-groups of NP pair tiles; a ragged last group runs dummy tiles past m (TMA zero-fills their
-    // A rows, the epilogue's row < m mask drops their stores) so every pair of a cluster stays in step
-    const int num_tiles = ((p.m_tiles + NP - 1) / NP) * p.splits * p.n_tiles;
     const long long t_kernel0 = clock64();
 
     if (warp < kNumSplitWarps) {
@@ -521,10 +549,11 @@ shgemm_sm100_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_const
         long long w_a = 0, w_b = 0, stages = 0;
         const long long t_begin = clock64();
         const bool skip_math = (p.dbg & 2u) != 0;
-        for (int tile = cta_of_tile; tile < num_tiles; tile += tile_stride) {
-            int m_blk, s, n_blk, kb0, kb1;
-            coords(tile, m_blk, s, n_blk);
-            kb_range(s, p, kb0, kb1);
+        Piece wk;
+        for (int it = 0; next_piece(p, unit, units, sr, it, wk); ++it) {
+            const int m_blk = wk.m_blk, n_blk = wk.n_blk, kb0 = 0, kb1 = wk.nkb;
+            (void)m_blk;
+            (void)n_blk;
             for (int kb = kb0; kb < kb1; kb += KC) {
                 const int nst = (kb1 - kb) < KC ? (kb1 - kb) : KC;
 #pragma unroll
@@ -657,14 +686,15 @@ shgemm_sm100_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_const
         long long w_full = 0, t_store = 0;
         const bool skip_ld = (p.dbg & 1u) != 0;
         const int etid = static_cast<int>(threadIdx.x) - kEpiWarp0 * 32;   // 0..255
-        for (int tile = cta_of_tile; tile < num_tiles; tile += tile_stride) {
-            int m_blk, s, n_blk, kb0, kb1;
-            coords(tile, m_blk, s, n_blk);
-            kb_range(s, p, kb0, kb1);
+        Piece wk;
+        for (int it = 0; next_piece(p, unit, units, sr, it, wk); ++it) {
+            const int m_blk = wk.m_blk, n_blk = wk.n_blk, kb0 = 0, kb1 = wk.nkb;
+            (void)m_blk;
+            (void)n_blk;
             // cooperative Omega (p.om_gen): this CTA generates the tiles kb0s + m_blk + i * m_tiles of
             // its split, each before the epilogue reaches the chunk kOmGenLookahead tiles earlier
             // (a fixed schedule, uniform over the 8 warps: deadlock-free by induction over chunks)
-            const int64_t kb0s = kb_global(kb0, s, p);
+            const int64_t kb0s = (wk.kb0 + (kb0));
             int64_t gen_next = kb0s + m_blk;
             const int64_t gen_end = OMGEN ? kb0s + (kb1 - kb0) : 0;
             auto gen_upto = [&](int64_t limit) {
@@ -681,7 +711,7 @@ shgemm_sm100_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_const
 #pragma unroll
             for (int i = 0; i < NACC; ++i) acc[i] = 0.0f;
             for (int kb = kb0; kb < kb1; kb += CF::KC, ++stage) {   // one promotion per K_c chunk
-                gen_upto(kb_global(kb, s, p) + CF::KC + kOmGenLookahead);
+                gen_upto((wk.kb0 + (kb)) + CF::KC + kOmGenLookahead);
 #pragma unroll
                 for (int part = 0; part < NQ; ++part) {
                     if (!mine(part)) continue;
@@ -721,8 +751,70 @@ shgemm_sm100_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_const
                 }
             }
             gen_upto(gen_end);
-            // ---- store the tile rows owned by this thread (its half of every part's columns)
             const long long ts0 = clock64();
+            if (wk.slot >= 0) {
+                // ---- stream-K partial piece (sk_fixup): publish this piece's sums in its slot's plane
+                // (column-major 128-row planes per CTA half: a warp's 32 rows are one 128-B run), count
+                // it, and the tile's LAST piece to arrive reads all of them back and sums them in
+                // ascending k order (deterministic; nobody waits, so no co-residency is assumed)
+                const int r_in = 32 * q + static_cast<int>(lane);
+                const int64_t plane_el = static_cast<int64_t>(BN) * kBM;
+                float* mine_pl = p.sk_ws + (static_cast<int64_t>(wk.slot) * kPair + crank) * plane_el + r_in;
+#pragma unroll
+                for (int part = 0; part < NQ; ++part) {
+                    if (!mine(part)) continue;
+                    const int hw = (part == NQ - 1) ? HPL : HP0;
+                    const int aoff = SPLITH ? part * HP0 : 0;
+                    const int c0 = part * W + (SPLITH ? h * hw : 0);
+#pragma unroll
+                    for (int i = 0; i < HP0; ++i)
+                        if (i < hw) __stcg(mine_pl + static_cast<int64_t>(c0 + i) * kBM, acc[aoff + i]);
+                }
+                __threadfence();
+                epi_bar();
+                const int64_t K = p.num_kb, T = p.sk_total;
+                const int u0 = sk_unit_of(wk.tile * K, T, units), u1 = sk_unit_of(wk.tile * K + K - 1, T, units);
+                if (etid == 0) {
+                    const uint32_t old = atomicAdd(p.sk_cnt + wk.tile * kPair + crank, 1u);
+                    *sk_flag = (old + 1 == static_cast<uint32_t>(u1 - u0 + 1)) ? 1u : 0u;
+                }
+                epi_bar();
+                if (*reinterpret_cast<volatile uint32_t*>(sk_flag) == 0u) {
+                    t_store += clock64() - ts0;
+                    continue;
+                }
+                __threadfence();
+                // column groups of 8 outer (unrolled), the tile's pieces inner: 8 live sums, so the
+                // fix-up adds no register pressure to the epilogue's accumulators
+#pragma unroll
+                for (int part = 0; part < NQ; ++part) {
+                    if (!mine(part)) continue;
+                    const int hw = (part == NQ - 1) ? HPL : HP0;
+                    const int aoff = SPLITH ? part * HP0 : 0;
+                    const int c0 = part * W + (SPLITH ? h * hw : 0);
+#pragma unroll
+                    for (int i = 0; i < HP0; i += 8) {
+                        if (i < hw) {
+                            float t8[8];
+                            for (int u = u0; u <= u1; ++u) {
+                                // unit u's piece of this tile is its first piece iff u's range starts
+                                // inside the tile: floor(u*T/U) >= tile*K  <=>  u*T >= tile*K*U
+                                const int sl = 2 * u + (static_cast<int64_t>(u) * T >= wk.tile * K * units ? 0 : 1);
+                                const float* pl = p.sk_ws + (static_cast<int64_t>(sl) * kPair + crank) * plane_el + r_in +
+                                                  static_cast<int64_t>(c0 + i) * kBM;
+#pragma unroll
+                                for (int e = 0; e < 8; ++e) {
+                                    const float v = __ldcg(pl + e * kBM);
+                                    t8[e] = (u == u0) ? v : __fadd_rn(t8[e], v);
+                                }
+                            }
+#pragma unroll
+                            for (int e = 0; e < 8; ++e) acc[aoff + i + e] = t8[e];
+                        }
+                    }
+                }
+            }
+            // ---- store the tile rows owned by this thread (its half of every part's columns)
             const int64_t row = static_cast<int64_t>(m_blk) * CF::kTileM + static_cast<int64_t>(crank) * kBM + 32 * q +
                                 static_cast<int>(lane);
             if (row < p.m) {
@@ -733,7 +825,7 @@ shgemm_sm100_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_const
                     const int aoff = SPLITH ? part * HP0 : 0;
                     const int64_t col0 = static_cast<int64_t>(n_blk) * BN + part * W + (SPLITH ? h * hw : 0);
                     if (col0 >= p.n) continue;
-                    float* dst = p.out + static_cast<int64_t>(s) * p.split_stride + row * p.ldo_out + col0;
+                    float* dst = p.out + static_cast<int64_t>(wk.s) * p.split_stride + row * p.ldo_out + col0;
                     const int64_t valid = (p.n - col0) < hw ? (p.n - col0) : hw;
                     bool bad = false;
                     if (p.vec_store && valid == hw) {
@@ -775,15 +867,16 @@ shgemm_sm100_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_const
                 const uint64_t pol = p.n_tiles > 1 ? policy_evict_normal() : policy_evict_first();
                 uint32_t sa = 0, pa = 0;
                 long long w = 0;
-                for (int tile = cta_of_tile; tile < num_tiles; tile += tile_stride) {
-                    int m_blk, s, n_blk, kb0, kb1;
-                    coords(tile, m_blk, s, n_blk);
-                    kb_range(s, p, kb0, kb1);
+                Piece wk;
+                for (int it = 0; next_piece(p, unit, units, sr, it, wk); ++it) {
+                    const int m_blk = wk.m_blk, n_blk = wk.n_blk, kb0 = 0, kb1 = wk.nkb;
+                    (void)m_blk;
+                    (void)n_blk;
                     const int m0 = m_blk * CF::kTileM + static_cast<int>(crank) * kBM;
                     for (int kb = kb0; kb < kb1; ++kb) {
                         mbar_wait_prof(&a_empty[sa], pa ^ 1u, w);
                         mbar_arrive_expect_tx(&a_full[sa], kA32StageBytes);
-                        const int64_t kk = static_cast<int64_t>(kb_global(kb, s, p)) * kBK;
+                        const int64_t kk = static_cast<int64_t>((wk.kb0 + (kb))) * kBK;
                         const int c0 = static_cast<int>(kk % p.k_inner);
                         const int c2 = static_cast<int>(kk / p.k_inner);
                         uint8_t* dst = a32 + sa * kA32StageBytes;
@@ -819,12 +912,12 @@ shgemm_sm100_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_const
                 const uint64_t pol = policy_evict_last();
                 const bool tiled = p.om_tiled != 0;
                 uint32_t cs = 0, pc = 0;
-                uint32_t chunk_ctr = 0;
                 long long w = 0;
-                for (int tile = cta_of_tile; tile < num_tiles; tile += tile_stride) {
-                    int m_blk, s, n_blk, kb0, kb1;
-                    coords(tile, m_blk, s, n_blk);
-                    kb_range(s, p, kb0, kb1);
+                Piece wk;
+                for (int it = 0; next_piece(p, unit, units, sr, it, wk); ++it) {
+                    const int m_blk = wk.m_blk, n_blk = wk.n_blk, kb0 = 0, kb1 = wk.nkb;
+                    (void)m_blk;
+                    (void)n_blk;
                     const int n0 = n_blk * BN;
                     for (int kb = kb0; kb < kb1; kb += KC) {
                         const int nst = (kb1 - kb) < KC ? (kb1 - kb) : KC;
@@ -837,9 +930,7 @@ shgemm_sm100_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_const
                         }
                         if (!skip) {
                             for (int t = 0; t < nst; ++t) {
-                                // NP > 1: one pair per stage loads it for all pairs (multicast)
-                                if (NP > 1 && static_cast<uint32_t>((chunk_ctr * KC + t) % NP) != pp) continue;
-                                const int kcoord = kb_global(kb + t, s, p) * kBK;
+                                const int kcoord = (wk.kb0 + (kb + t)) * kBK;
                                 if constexpr (OMGEN) acquire_flag(p.om_flags + kcoord / kBK);   // generated in-kernel
                                 // FP16: one 128-B box row = 64 k; TF32: two k-halves of 32 k
 #pragma unroll
@@ -850,12 +941,7 @@ shgemm_sm100_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_const
                                     for (int bt = 0; bt < CF::NB; ++bt) {   // TCEC: B_low tile, then dB_low
                                         uint8_t* d2 = dst + bt * CF::kOmTileBytes;
                                         const int nb0 = n0 + bt * p.b_lo_col;
-                                        if constexpr (PAIR && NP > 1) {
-                                            tma_load_omega_mc(d2, &mapB0, &ch_ready[cs], kc,
-                                                              nb0 + static_cast<int>(crank) * CF::R0, half_mask, pol);
-                                            tma_load_omega_mc(d2 + CF::R0 * 128, &mapB1, &ch_ready[cs], kc,
-                                                              nb0 + W + static_cast<int>(crank) * CF::R1, half_mask, pol);
-                                        } else if constexpr (PAIR) {
+                                        if constexpr (PAIR) {
                                             tma_load_omega<PAIR, TF32>(d2, &mapB0, &ch_ready[cs], kc,
                                                                  nb0 + static_cast<int>(crank) * CF::R0, pol, tiled);
                                             tma_load_omega<PAIR, TF32>(d2 + CF::R0 * 128, &mapB1, &ch_ready[cs], kc,
@@ -872,7 +958,6 @@ shgemm_sm100_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_const
                             }
                         }
                         advance(cs, pc, NCH);
-                        ++chunk_ctr;
                     }
                 }
                 if (p.prof) p.prof[blockIdx.x * kProfSlots + kProfProdBEmpty] = w;
@@ -882,10 +967,11 @@ shgemm_sm100_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_const
             uint32_t cs = 0, pc = 0, g = 0;
             long long w_acc = 0, w_hl = 0, w_om = 0;
             const bool skip_mma = (p.dbg & 4u) != 0;
-            for (int tile = cta_of_tile; tile < num_tiles; tile += tile_stride) {
-                int m_blk, s, n_blk, kb0, kb1;
-                coords(tile, m_blk, s, n_blk);
-                kb_range(s, p, kb0, kb1);
+            Piece wk;
+            for (int it = 0; next_piece(p, unit, units, sr, it, wk); ++it) {
+                const int m_blk = wk.m_blk, n_blk = wk.n_blk, kb0 = 0, kb1 = wk.nkb;
+                (void)m_blk;
+                (void)n_blk;
                 for (int kb = kb0; kb < kb1; kb += KC) {
                     const int nst = (kb1 - kb) < KC ? (kb1 - kb) : KC;   // stages in this chunk
                     mbar_wait_prof(&ch_ready[cs], pc, w_hl);
@@ -944,7 +1030,7 @@ shgemm_sm100_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_const
                         }
                         __syncwarp();
                     }
-                    if (elect_one()) commit_to<PAIR>(&ch_empty[cs], NP > 1 ? cl_mask : pair_mask);
+                    if (elect_one()) commit_to<PAIR>(&ch_empty[cs], pair_mask);
                     __syncwarp();
                     advance(cs, pc, NCH);
                 }

@@ -10,13 +10,13 @@ template <bool MMAJOR>
 shg_status_t dispatch(int bn, const CUtensorMap& a, const CUtensorMap& b0, const CUtensorMap& b1,
                       const shg::KParams& kp, int grid, cudaStream_t s) {
     switch (bn) {
-        case 32: return launch_tc<32, MMAJOR, false, false, false, 1, true>(a, b0, b1, kp, grid, s);
-        case 64: return launch_tc<64, MMAJOR, false, false, false, 1, true>(a, b0, b1, kp, grid, s);
-        case 96: return launch_tc<96, MMAJOR, false, false, false, 1, true>(a, b0, b1, kp, grid, s);
-        case 128: return launch_tc<128, MMAJOR, false, false, false, 1, true>(a, b0, b1, kp, grid, s);
-        case 144: return launch_tc<144, MMAJOR, false, false, false, 1, true>(a, b0, b1, kp, grid, s);
-        case 160: return launch_tc<160, MMAJOR, false, false, false, 1, true>(a, b0, b1, kp, grid, s);
-        case 192: return launch_tc<192, MMAJOR, false, false, false, 1, true>(a, b0, b1, kp, grid, s);
+        case 32: return launch_tc<32, MMAJOR, false, false, false, true>(a, b0, b1, kp, grid, s);
+        case 64: return launch_tc<64, MMAJOR, false, false, false, true>(a, b0, b1, kp, grid, s);
+        case 96: return launch_tc<96, MMAJOR, false, false, false, true>(a, b0, b1, kp, grid, s);
+        case 128: return launch_tc<128, MMAJOR, false, false, false, true>(a, b0, b1, kp, grid, s);
+        case 144: return launch_tc<144, MMAJOR, false, false, false, true>(a, b0, b1, kp, grid, s);
+        case 160: return launch_tc<160, MMAJOR, false, false, false, true>(a, b0, b1, kp, grid, s);
+        case 192: return launch_tc<192, MMAJOR, false, false, false, true>(a, b0, b1, kp, grid, s);
         default: return SHG_ERR_INVALID_VALUE;
     }
 }

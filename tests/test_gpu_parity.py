@@ -500,40 +500,13 @@ def test_a_box_layouts(shg, orc, m, k, n, tune):
         shg.shgemm(cuda(synth.gaussian(64, 100, seed=1)), shg.gen_omega(100, 16), tune={"a_box": 2})
 
 
-@pytest.mark.parametrize("m,k,n,mmajor", [(2048, 1000, 256, False), (4096, 640, 144, False), (1024, 3000, 200, True),
-                                          (2048, 512, 130, False)])
-@pytest.mark.parametrize("mc", [2, 3, 4])
-def test_omega_multicast_bitwise_identical(shg, orc, m, k, n, mmajor, mc):
-    """Omega stages multicast to 2 / 4 CTA pairs of a cluster change only who loads Omega, not the
-    arithmetic: Y is bitwise identical to the unicast pair kernel (and meets the bars)."""
-    rng = np.random.default_rng(m + n + mc)
-    A = rng.standard_normal((m, k)).astype(np.float32)
-    Om = shg.gen_omega(k, n, seed=3)
-    if mmajor:
-        At = cuda(np.ascontiguousarray(A.T))
-        y1 = shg.shgemm_at(At, Om, tune={"omega_mcast": 1, "pair": 1})
-        ym = shg.shgemm_at(At, Om, tune={"omega_mcast": mc, "pair": 1})
-    else:
-        Ad = cuda(A)
-        y1 = shg.shgemm(Ad, Om, tune={"omega_mcast": 1, "pair": 1})
-        ym = shg.shgemm(Ad, Om, tune={"omega_mcast": mc, "pair": 1})
-    torch.cuda.synchronize()
-    assert shg.plan(m, n, k, {"omega_mcast": mc, "pair": 1})["omega_mcast"] == mc
-    assert torch.equal(y1, ym)
-    check_bars(orc, A, omega_bits(Om), to_np(ym))
-
-
-def test_omega_multicast_ragged_groups_and_rejections(shg):
-    """A pair-tile count that is not a multiple of the pairs per cluster runs dummy tiles in the
-    last group (zero-filled A rows, masked stores): still bitwise equal; BN = 64 has no pairs."""
-    g = torch.Generator(device="cuda").manual_seed(9)
-    A = torch.randn(5 * 256 + 17, 1000, device="cuda", generator=g)       # 6 pair tiles, ragged rows
-    Om = shg.gen_omega(1000, 256, seed=1)
-    y1 = shg.shgemm(A, Om, tune={"omega_mcast": 1})
-    for mc in (3, 4):
-        assert torch.equal(shg.shgemm(A, Om, tune={"omega_mcast": mc}), y1)
-    with pytest.raises(shg.SHGError):
-        shg.plan(4096, 64, 512, {"omega_mcast": 2})         # BN = 64: single CTAs, no pairs
+def test_omega_multicast_option_removed(shg):
+    """Round 2 removed the Omega-multicast instantiations (no steady-state gain):
+    omega_mcast 0 / 1 plan normally, 2..4 are rejected instead of silently ignored."""
+    assert shg.plan(4096, 256, 512, {"omega_mcast": 1})["omega_mcast"] == 1
+    for mc in (2, 3, 4, -1):
+        with pytest.raises(shg.SHGError):
+            shg.plan(4096, 256, 512, {"omega_mcast": mc})
 
 
 @pytest.mark.parametrize("m,k,n,tune", [(1000, 1500, 272, None), (600, 777, 288, None), (130, 640, 270, None),
