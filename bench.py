@@ -35,6 +35,8 @@ CONFIGS = {
     "cfg1": (512, 512, 32, "BASELINE config 1 shape: A 512x512 FP32 . Omega 512x32 FP16 (fits in L2: L2 flushed "
                            "between timed steps, only the steps timed)"),
     "cfg4": (4194304, 4096, 256, "BASELINE config 4: tall projection A 4,194,304x4096 FP32 . Omega 4096x256 FP16"),
+    "cfg2proj": (16384, 16384, 272, "BASELINE config 2's projection (RSVD Alg 1 line 1): A 16384x16384 FP32 . "
+                                    "Omega 16384x272 FP16"),
     "cfg5n64": (32768, 32768, 64, "BASELINE config 5 sweep point n=64 (m=k=32768)"),
     "cfg5n256": (32768, 32768, 256, "BASELINE config 5 sweep point n=256 (m=k=32768)"),
     "cfg5n1024": (32768, 32768, 1024, "BASELINE config 5 sweep point n=1024 (m=k=32768)"),

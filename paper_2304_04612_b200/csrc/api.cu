@@ -230,9 +230,12 @@ struct OmGen {
     uint32_t* flags;        // ceil(k/64) zero-initialised ready flags
 };
 
-// Stream-K is planned when whole tiles would leave the last wave under this fraction of the
-// units busy (e.g. 64 pair tiles of RSVD's projection on 74 pairs: 0.86)
-constexpr double kSkMinWaveEff = 0.92;
+// Stream-K is an opt-in schedule (tune->stream_k = 1): auto does not pick it. Measured interleaved
+// against whole tiles under the 1000 W cap (profiles/r02_ab_streamk.jsonl): cfg2's projection 0.298
+// vs 0.297 ms (the 10 extra pairs run 13% more cycles per stage at a lower clock) and cfg5 n = 256
+// 0.930 vs 0.951 ms: the idle last wave of whole tiles is paid back by the power cap.
+constexpr bool kSkAuto = false;
+constexpr double kSkMinWaveEff = 0.92;   // the auto rule if kSkAuto were set
 
 
 // om_rm: Omega is row-major; the FP16 tensor-core path then reads a column-major copy
@@ -298,8 +301,8 @@ Plan make_plan(int64_t m, int64_t n, int64_t k, bool fast_ok, const shg_tune_t* 
     const double wave_eff = static_cast<double>(mn_tiles) / static_cast<double>(waves * slots);
     const bool sk_fits = allow_sk && pl.n_tiles == 1 && mn_tiles * pl.num_kb >= int64_t(4) * slots &&
                          !(tune && tune->split_k > 1);
-    pl.sk = sk_fits && (sk_mode == 1 || (sk_mode == 0 && wave_eff < kSkMinWaveEff && 2 * mn_tiles >= slots &&
-                                          pl.num_kb >= 16));
+    pl.sk = sk_fits && (sk_mode == 1 || (kSkAuto && sk_mode == 0 && wave_eff < kSkMinWaveEff &&
+                                          2 * mn_tiles >= slots && pl.num_kb >= 16));
     if (sk_mode == 1 && !sk_fits) { pl.path = -1; return pl; }
     int splits = 1;
     if (tune && tune->split_k > 0) {

@@ -138,10 +138,26 @@ __device__ __forceinline__ void mbar_wait_prof(uint64_t* bar, uint32_t parity, l
     acc += clock64() - t0;
 }
 
-// arrive on the copy of `bar` (a local smem address) in CTA `cta` of the cluster. RELAXED: the only
-// data these arrivals publish is tensor memory, already ordered by tcgen05.wait::st /
-// tcgen05.fence::before_thread_sync; a .release.cluster arrive would emit MEMBAR.ALL.GPU (measured
-// ~1000 cycles per handoff on the MMA thread's critical path).
+// arrive on the copy of `bar` (a local smem address) in CTA `cta` of the cluster. RELAXED, because
+// these arrivals publish no generic-proxy memory, only the completion of the arriving thread's own
+// tensor-memory accesses, and that completion is established by blocking waits BEFORE the arrive:
+//  (1) ch_ready (follower splitter -> leader MMA): the follower's tcgen05.st of hi/lo into its TMEM
+//      are followed by tcgen05.wait::st, which does not return until every prior tcgen05.st of the
+//      thread has completed (the values are in TMEM); then tcgen05.fence::before_thread_sync orders
+//      those tcgen05 ops before the arrive, the arrive can only execute after the wait returned, the
+//      leader's try_wait observes the phase it completes, and tcgen05.fence::after_thread_sync keeps
+//      the leader's tcgen05.mma (which reads the follower's TMEM half) from being issued before that
+//      observation. Causality runs st-complete -> arrive -> phase flip -> wait returns -> MMA issue.
+//  (2) acc_empty (follower epilogue -> leader MMA): tcgen05.ld of the accumulator, then
+//      tcgen05.wait::ld (the values are in registers) -> fence::before_thread_sync -> arrive; the
+//      leader's next MMA into that slot is issued after its wait + fence::after_thread_sync, so the
+//      overwrite cannot reach the slot before the reads completed (write-after-read).
+// Neither handoff carries data through shared or global memory, so no release/acquire is needed
+// for visibility; a .release.cluster arrive would emit MEMBAR.ALL.GPU (measured ~1000 cycles per
+// handoff on the MMA thread's critical path). The Omega TMA bytes (complete_tx on the leader's
+// barrier) and the MMA completions (tcgen05.commit multicast) are hardware arrivals that fire only
+// after their data has landed / their operand reads have finished. (compute-sanitizer racecheck
+// does not model TMEM; this argument plus the bitwise parity suite are the evidence.)
 __device__ __forceinline__ void mbar_arrive_cluster(uint64_t* bar, uint32_t cta) {
     asm volatile(
         "{\n\t.reg .b32 ra;\n\t"

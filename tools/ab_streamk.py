@@ -1,0 +1,16 @@
+"""A/B of the stream-K schedule (tune stream_k = 1) against whole tiles (stream_k = 2), interleaved on
+the same inputs: median ms, cycles per stage and effective SM clock (profiles/r02_ab_streamk.jsonl)."""
+import json
+import sys
+
+sys.path.insert(0, '.')
+from tools.ab import run  # noqa: E402
+
+if __name__ == '__main__':
+    allres = []
+    for shape in [(16384, 16384, 272), (32768, 32768, 256), (32768, 32768, 128),
+                  (8192, 16384, 256), (20000, 8192, 192)]:
+        allres += run(shape, [('tiles', {'stream_k': 2}), ('stream_k', {'stream_k': 1})], rounds=7, reps=10)
+    with open('gpurun_out/r02_ab_streamk.jsonl', 'w') as f:
+        for r in allres:
+            f.write(json.dumps(r) + '\n')
