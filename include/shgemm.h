@@ -116,11 +116,6 @@ typedef struct {
                              (deterministic). Measured no faster under the 1000 W cap
                              (DESIGN.md §5), so auto keeps whole tiles. Needs one N tile, no split_k
                              > 1 and >= 4 k-blocks per unit: otherwise SHG_ERR_INVALID_VALUE. */
-    int32_t lockstep;     /* several N tiles (n > BN): 0 auto (= on), 1 on, 2 off. On, the grid is a
-                             multiple of the N-tile count and the A stagers of an m-block's N tiles stay
-                             within 4 stages of each other, so A is read from HBM about once (bounded
-                             waits: never a deadlock; results identical). Costs workspace for one
-                             counter per tile. Other values: SHG_ERR_INVALID_VALUE. */
 } shg_tune_t;
 
 /* Plan the library would use for an (m, n, k) shgemm on the current device. */

@@ -39,8 +39,7 @@ class Tune(ctypes.Structure):
     _fields_ = [("bn", ctypes.c_int32), ("split_k", ctypes.c_int32), ("max_ctas", ctypes.c_int32),
                 ("force_simt", ctypes.c_int32), ("debug_flags", ctypes.c_int32), ("pair", ctypes.c_int32),
                 ("a_box", ctypes.c_int32), ("tc", ctypes.c_int32), ("omega_mcast", ctypes.c_int32),
-                ("prof", ctypes.c_void_p), ("omega_layout", ctypes.c_int32), ("stream_k", ctypes.c_int32),
-                ("lockstep", ctypes.c_int32)]
+                ("prof", ctypes.c_void_p), ("omega_layout", ctypes.c_int32), ("stream_k", ctypes.c_int32)]
 
 
 class Plan(ctypes.Structure):

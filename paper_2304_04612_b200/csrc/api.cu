@@ -211,8 +211,6 @@ struct Plan {
     bool tcec = false;        // TCEC-SGEMM (FP32 B split into B_low / dB_low)
     bool sk = false;          // stream-K schedule (KParams::sk): equal k-ranges per SM (pair), in-kernel fix-up
     int64_t sk_planes = 0;    // stream-K: bytes of the partial planes (the counters follow, 256-B aligned)
-    int ls_window = 0;        // N-tile lockstep window in stages (KParams::ls_window), 0 = off
-    int64_t ls_off = 0, ls_bytes = 0;   // its counters: workspace offset and bytes
     // workspace = [split-K planes, 256-B aligned][TF32 copy of Omega | TCEC split of B]
     int64_t ws_bytes = 0, ld_ws = 0, sk_bytes = 0, om_bytes = 0, ldo32 = 0;
     int64_t ldh = 0, noff = 0;  // TCEC: split B column-major, ld ldh; dB_low starts at column noff
@@ -237,7 +235,6 @@ struct OmGen {
 // vs 0.297 ms (the 10 extra pairs run 13% more cycles per stage at a lower clock) and cfg5 n = 256
 // 0.930 vs 0.951 ms: the idle last wave of whole tiles is paid back by the power cap.
 constexpr bool kSkAuto = false;
-constexpr int kLsWindow = 4;              // N-tile lockstep: max stages an A stager runs ahead of its group
 constexpr double kSkMinWaveEff = 0.92;   // the auto rule if kSkAuto were set
 
 
@@ -289,7 +286,6 @@ Plan make_plan(int64_t m, int64_t n, int64_t k, bool fast_ok, const shg_tune_t* 
     if (mc < 0 || mc > 1) { pl.path = -1; return pl; }
     const int sk_mode = tune ? tune->stream_k : 0;   // 0 auto, 1 force on, 2 off
     if (sk_mode < 0 || sk_mode > 2) { pl.path = -1; return pl; }
-    if (tune && (tune->lockstep < 0 || tune->lockstep > 2)) { pl.path = -1; return pl; }
     const int tile_m = pl.pair ? 2 * shg::kBM : shg::kBM;
     int cap = (tune && tune->max_ctas > 0) ? tune->max_ctas : sms;
     const int cl = pl.pair ? 2 : 1;                 // CTAs per cluster (= per work unit)
@@ -322,15 +318,6 @@ Plan make_plan(int64_t m, int64_t n, int64_t k, bool fast_ok, const shg_tune_t* 
     pl.splits = splits;
     const int64_t tiles = mn_tiles * splits;
     pl.grid = pl.sk ? slots * cl : static_cast<int>(std::min<int64_t>(tiles * cl, cap));
-    // several N tiles: the units are a multiple of n_tiles, so the N tiles of an m-block always run
-    // in the same round, and their A stagers keep within kLsWindow stages of each other (A from HBM
-    // once, the rest from L2). Under the power cap the 2 of 74 pairs this idles at n_tiles = 4 cost
-    // nothing measurable, while the re-reads of A cost HBM energy.
-    const int ls_mode = tune ? tune->lockstep : 0;   // 0 auto (on), 1 on, 2 off
-    if (!pl.sk && pl.n_tiles > 1 && ls_mode != 2 && pl.grid / cl >= pl.n_tiles) {
-        pl.grid = (pl.grid / cl) / pl.n_tiles * pl.n_tiles * cl;
-        pl.ls_window = kLsWindow;
-    }
     pl.grid = std::max(cl, pl.grid / cl * cl);
     if (splits > 1) {
         pl.ld_ws = (n + 3) / 4 * 4;
@@ -352,11 +339,6 @@ Plan make_plan(int64_t m, int64_t n, int64_t k, bool fast_ok, const shg_tune_t* 
         pl.om_bytes = n * pl.ldt * 2;
     }
     pl.ws_bytes = (pl.om_bytes ? up256(pl.sk_bytes) : pl.sk_bytes) + pl.om_bytes;
-    if (pl.ls_window > 0) {   // lockstep counters after everything else
-        pl.ls_off = up256(pl.ws_bytes);
-        pl.ls_bytes = up256(static_cast<int64_t>(pl.m_tiles) * pl.splits * pl.n_tiles * cl * 4);
-        pl.ws_bytes = pl.ls_off + pl.ls_bytes;
-    }
     return pl;
 }
 
@@ -545,12 +527,6 @@ shg_status_t run_shgemm(int64_t m, int64_t n, int64_t k, const AView& av, const 
     kp.om_tiled = om_tiled ? 1 : 0;
     const bool gen = og != nullptr;
     kp.sk = pl.sk ? 1 : 0;
-    if (pl.ls_window > 0) {
-        kp.ls_window = pl.ls_window;
-        kp.ls_cnt = reinterpret_cast<uint32_t*>(wsb + pl.ls_off);
-        const cudaError_t e = cudaMemsetAsync(kp.ls_cnt, 0, static_cast<size_t>(pl.ls_bytes), stream);
-        if (e != cudaSuccess) return finish(cuda_fail(e, "cudaMemsetAsync(lockstep counters)"));
-    }
     if (pl.sk) {
         kp.sk_total = static_cast<int64_t>(pl.m_tiles) * pl.n_tiles * pl.num_kb;
         kp.sk_ws = reinterpret_cast<float*>(wsb);

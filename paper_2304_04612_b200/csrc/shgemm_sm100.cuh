@@ -90,13 +90,6 @@ struct KParams {
     int64_t sk_total;
     float* sk_ws;
     uint32_t* sk_cnt;
-    // N-tile lockstep (ls_window > 0; n_tiles > 1, units a multiple of n_tiles): the A stagers of the
-    // n_tiles CTAs (per pair half) that read the same m-block publish their k progress in ls_cnt
-    // (one zeroed uint32 per tile and pair half) and hold back while more than ls_window stages
-    // ahead of the slowest, so every A stage is still in L2 when the others fetch it (A read once
-    // from HBM). A bounded spin: a member that is not resident only costs the wait budget.
-    int32_t ls_window;
-    uint32_t* ls_cnt;
     uint32_t dbg;           // diagnostics: bit0 skip promotion loads, bit1 skip split math, bit2 skip MMAs,
                             //              bit3 skip the Omega TMA (results are wrong when dbg != 0)
     long long* prof;        // diagnostics: per-CTA wait-cycle counters [gridDim.x][16] (ProfSlot)
@@ -896,32 +889,7 @@ shgemm_sm100_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_const
                     (void)m_blk;
                     (void)n_blk;
                     const int m0 = m_blk * CF::kTileM + static_cast<int>(crank) * kBM;
-                    // lockstep group: the n_tiles tiles of this m-block and split, same pair half
-                    // (only when every group runs in one round of the round-robin: units % n_tiles == 0)
-                    uint32_t* ls_grp = (p.ls_window > 0 && units % p.n_tiles == 0)
-                        ? p.ls_cnt + ((static_cast<int64_t>(m_blk) * p.splits + wk.s) * p.n_tiles) * kPair + crank
-                        : nullptr;
                     for (int kb = kb0; kb < kb1; ++kb) {
-                        if (ls_grp) {
-                            // publish this stage, then hold while > ls_window stages ahead of a member
-                            asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(ls_grp + n_blk * kPair),
-                                         "r"(static_cast<uint32_t>(kb)) : "memory");
-                            if (kb > p.ls_window) {
-                                const uint32_t need = static_cast<uint32_t>(kb - p.ls_window);
-                                for (int j = 0; j < p.n_tiles && ls_grp; ++j) {
-                                    if (j == n_blk) continue;
-                                    uint32_t v, spins = 0;
-                                    do {
-                                        asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];"
-                                                     : "=r"(v) : "l"(ls_grp + j * kPair) : "memory");
-                                    } while (v < need && ++spins < 2048u);
-                                    // a member that is not progressing (not resident: another kernel
-                                    // holds its SM) ends the lockstep for this tile instead of
-                                    // stalling every stage
-                                    if (v < need) ls_grp = nullptr;
-                                }
-                            }
-                        }
                         mbar_wait_prof(&a_empty[sa], pa ^ 1u, w);
                         mbar_arrive_expect_tx(&a_full[sa], kA32StageBytes);
                         const int64_t kk = static_cast<int64_t>((wk.kb0 + (kb))) * kBK;

@@ -116,39 +116,3 @@ def test_stream_k_config2_full_size(shg, orc):
     rows = np.unique(np.concatenate([np.arange(0, m, 97), [m - 1]]))
     A_s = orc.synth_rows("gauss", 2, 0x101, rows, k)
     check_bars(orc, A_s, omega_bits(Om), to_np(Y)[rows])
-
-
-# ------------------------------------------------------------------ N-tile lockstep (n > BN)
-@pytest.mark.parametrize("m,k,n,tune", [
-    (8192, 2048, 512, {}),                     # 2 N tiles of 256 (pairs)
-    (6000, 3000, 1024, {}),                    # 4 N tiles, ragged m
-    (5000, 2000, 560, {}),                     # 3 N tiles
-    (3000, 1500, 600, {"tc": "tf32"}),         # SHGEMM-TF32
-    (4000, 1000, 300, {"pair": 2}),            # single CTAs, 2 N tiles
-])
-def test_lockstep_bitwise_identical(shg, m, k, n, tune):
-    """The lockstep only delays A loads (and makes the grid a multiple of the N-tile count): every
-    tile is still computed by one CTA (pair) in the same order, so Y is bitwise unchanged."""
-    A = _A(m, k, m + 3 * n)
-    Om = shg.gen_omega(k, n, seed=9)
-    on, off = dict(tune, lockstep=1), dict(tune, lockstep=2)
-    p_on = shg.plan(m, n, k, on)
-    assert p_on["n_tiles"] > 1 and p_on["grid"] % (p_on["n_tiles"] * (2 if p_on["cta_pair"] else 1)) == 0
-    assert torch.equal(shg.shgemm(A, Om, tune=on), shg.shgemm(A, Om, tune=off))
-
-
-def test_lockstep_concurrent_kernels(shg):
-    """Lockstep kernels on four streams at once (their groups cannot all be resident): the bounded
-    waits give up on non-progressing members, the results are unchanged."""
-    A = _A(8192, 4096, 11)
-    Om = shg.gen_omega(4096, 1024, seed=2)
-    ref = shg.shgemm(A, Om, tune={"lockstep": 2})
-    torch.cuda.synchronize()
-    streams = [torch.cuda.Stream() for _ in range(4)]
-    outs = []
-    for s in streams:
-        with torch.cuda.stream(s):
-            outs.append(shg.shgemm(A, Om, stream=s))
-    torch.cuda.synchronize()
-    for y in outs:
-        assert torch.equal(y, ref)
