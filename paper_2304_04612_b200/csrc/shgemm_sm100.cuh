@@ -699,6 +699,7 @@ shgemm_sm100_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_const
         // parts drained by this group: SPLITH all of them (its half of each), else part h only
         auto mine = [&](int part) { return SPLITH || part == h; };
         uint32_t stage = 0;
+        uint32_t e_use0 = 0, e_use1 = 0;   // WIDE: drains per accumulator slot (= part)
         long long w_full = 0, t_store = 0;
         const bool skip_ld = (p.dbg & 1u) != 0;
         const int etid = static_cast<int>(threadIdx.x) - kEpiWarp0 * 32;   // 0..255
@@ -731,11 +732,19 @@ shgemm_sm100_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_const
 #pragma unroll
                 for (int part = 0; part < NQ; ++part) {
                     if (!mine(part)) continue;
+                    // WIDE: part q is promoted on stages with (local stage + q) odd and on the
+                    // piece's last stage, in the same pairing as the MMA issuer's
+                    if (CF::WIDE && !((((kb - kb0) + part) & 1) == 1 || kb + 1 == kb1)) continue;
                     const int hw = (part == NQ - 1) ? HPL : HP0;       // this group's columns of the part
                     const int aoff = SPLITH ? part * HP0 : 0;
                     const uint32_t g = stage * NQ + part;
-                    const uint32_t slot = g % NSLOT;
-                    mbar_wait_prof(&acc_full[slot], (g / NSLOT) & 1u, w_full);
+                    const uint32_t slot = CF::WIDE ? static_cast<uint32_t>(part) : g % NSLOT;
+                    const uint32_t par = CF::WIDE ? ((part ? e_use1 : e_use0) & 1u) : ((g / NSLOT) & 1u);
+                    if (CF::WIDE) {
+                        if (part) ++e_use1;
+                        else ++e_use0;
+                    }
+                    mbar_wait_prof(&acc_full[slot], par, w_full);
                     tc_fence_after();
                     const uint32_t taddr = tmem_base + lane_addr + slot * W + (SPLITH ? h * hw : 0);
                     if (!skip_ld) {
@@ -983,11 +992,103 @@ shgemm_sm100_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_const
             uint32_t cs = 0, pc = 0, g = 0;
             long long w_acc = 0, w_hl = 0, w_om = 0;
             const bool skip_mma = (p.dbg & 4u) != 0;
+            // wide tiles: per-slot use counts (part 0 every stage, part 1 every second stage)
+            uint32_t u0 = 0, u1 = 0;
             Piece wk;
             for (int it = 0; next_piece(p, unit, units, sr, it, wk); ++it) {
                 const int m_blk = wk.m_blk, n_blk = wk.n_blk, kb0 = 0, kb1 = wk.nkb;
                 (void)m_blk;
                 (void)n_blk;
+                if constexpr (CF::WIDE) {
+                    // WIDE (KC = 1, 3 stage slots): each part is folded and promoted every TWO
+                    // stages (K_c = 128 per part: lo MMAs of stages s and s+1 accumulate, then hi of
+                    // s with scale-input-d = 11 and hi of s+1), the parts staggered by one stage so
+                    // that one part (<= 144 columns) is drained per stage instead of all 272: the
+                    // wide tile is bound by the TMEM read port otherwise. A stage slot
+                    // is released one stage later (when both parts have consumed it).
+                    auto part_mmas = [&](int part, uint32_t a_st, uint64_t b_st, int kind, bool first) {
+                        // kind 0: lo (+ TCEC's A_low . dB_low); kind 1: hi, first with scale-input-d
+                        const uint32_t d = tmem_base + part * W;
+                        const uint32_t idesc = idesc_f16_f32(CF::kTileM, part ? WLAST : W);
+                        const uint64_t b = b_st + static_cast<uint64_t>(((part ? CF::R0 : 0) * 128) >> 4);
+                        if (kind == 0) {
+#pragma unroll
+                            for (int j = 0; j < NMMA; ++j)
+                                mma_ts<PAIR, false>(d, a_st + AST / 2 + 8 * j, b + static_cast<uint64_t>(2 * j), idesc,
+                                                    (first && j == 0) ? 0u : 1u);
+                            if constexpr (TCEC) {
+#pragma unroll
+                                for (int j = 0; j < NMMA; ++j)
+                                    mma_ts<PAIR, false>(d, a_st + 8 * j,
+                                                        b + static_cast<uint64_t>(CF::kOmTileBytes >> 4) +
+                                                            static_cast<uint64_t>(2 * j),
+                                                        idesc, 1u);
+                            }
+                        } else {
+#pragma unroll
+                            for (int j = 0; j < NMMA; ++j) {
+                                const uint32_t a = a_st + 8 * j;
+                                const uint64_t bb = b + static_cast<uint64_t>(2 * j);
+                                if (first && j == 0) mma_ts_scale11<PAIR, false>(d, a, bb, idesc);
+                                else mma_ts<PAIR, false>(d, a, bb, idesc, 1u);
+                            }
+                        }
+                    };
+                    // part q folds and promotes PAIRS of stages, part 0 closing on odd local stages
+                    // and part 1 on even ones (stage 0 alone), and both on the piece's last stage:
+                    // one part is drained per stage, with two stages of MMAs to hide it
+                    bool pend0 = false, pend1 = false;
+                    uint32_t cs_prev = 0, a_prev = 0;
+                    uint64_t b_prev = 0;
+                    for (int kb = kb0; kb < kb1; ++kb) {
+                        mbar_wait_prof(&ch_ready[cs], pc, w_hl);
+                        const uint32_t a_cur = tmem_base + ABASE + cs * AST;
+                        const uint64_t b_cur = sw128_kmajor_desc(smem_u32(om + cs * kOm));
+                        const bool last = kb + 1 == kb1;
+#pragma unroll
+                        for (int q = 0; q < 2; ++q) {
+                            bool& pend = q ? pend1 : pend0;
+                            uint32_t& u = q ? u1 : u0;
+                            const bool close = (((kb - kb0) + q) & 1) == 1 || last;
+                            if (!pend) {
+                                mbar_wait_prof(&acc_empty[q], (u & 1u) ^ 1u, w_acc);
+                                tc_fence_after();
+                            }
+                            if (elect_one()) {
+                                if (!skip_mma) {
+                                    part_mmas(q, a_cur, b_cur, 0, !pend);
+                                    if (close) {
+                                        if (pend) {
+                                            part_mmas(q, a_prev, b_prev, 1, true);
+                                            part_mmas(q, a_cur, b_cur, 1, false);
+                                        } else {
+                                            part_mmas(q, a_cur, b_cur, 1, true);
+                                        }
+                                    }
+                                }
+                                if (close) commit_to<PAIR>(&acc_full[q], pair_mask);
+                            }
+                            __syncwarp();
+                            if (close) {
+                                ++u;
+                                pend = false;
+                            } else {
+                                pend = true;
+                            }
+                        }
+                        // the previous stage is now consumed by both parts; the last one too at the end
+                        if (elect_one()) {
+                            if (kb > kb0) commit_to<PAIR>(&ch_empty[cs_prev], pair_mask);
+                            if (last) commit_to<PAIR>(&ch_empty[cs], pair_mask);
+                        }
+                        __syncwarp();
+                        cs_prev = cs;
+                        a_prev = a_cur;
+                        b_prev = b_cur;
+                        advance(cs, pc, NCH);
+                    }
+                    continue;
+                }
                 for (int kb = kb0; kb < kb1; kb += KC) {
                     const int nst = (kb1 - kb) < KC ? (kb1 - kb) : KC;   // stages in this chunk
                     mbar_wait_prof(&ch_ready[cs], pc, w_hl);
