@@ -521,6 +521,15 @@ def main():
     ms_per_step = total_ms / args.steps
     flops_total = 2.0 * m_total * k * n
     value = flops_total / (ms_per_step * 1e-3) / 1e12
+    fused = None
+    if flush and world == 1:
+        # the same step as ONE kernel: project(A, mode 0, n) with Omega generated
+        # inside the mainloop (its stream_id 0 = gen_omega's), replayed from a CUDA graph like the
+        # two-kernel step; reported beside it (latency-bound shapes only)
+        try:
+            fused = measure_fused_step(shg, torch, A, n, args.steps, scrub)
+        except Exception as exc:  # noqa: BLE001
+            fused = {"error": repr(exc)[:200]}
 
     hbm, tc16, tc16_sus, peak_src = load_peaks()
     # Roofline (north_star): min(P_FP16 / 2, AI x BW) with the BURST tensor peak (the
@@ -602,11 +611,48 @@ def main():
                           "plan": shg.plan(m, n, k, tc=args.tc)},
                "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
                "clocks": clk, "omega_gen_ms": gen_ms, "shgemm_ms": gemm_ms, "other_workloads": extras,
+               "fused_single_launch_step": fused,
                "gbs_algorithmic": achieved_gbs}
         print(json.dumps(out), flush=True)
     if dist:
         dist.barrier()
         dist.destroy_process_group()
+
+
+def measure_fused_step(shg, torch, A, n, steps, scrub):
+    """One step = project(A, 0, n, seed) with in-kernel Omega (one mainloop launch + a memset of its
+    tile flags), CUDA-graph replay, L2 scrubbed between steps; per-step device time in us."""
+    m, k = A.shape
+    ws = torch.empty(shg.project_workspace_size([m, k], 0, n), dtype=torch.uint8, device="cuda")
+    W = torch.empty((m, n), device="cuda")
+    shg.set_inkernel_omega(True)
+    try:
+        side = torch.cuda.Stream()
+        side.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(side):
+            for _ in range(3):
+                shg.project(A, 0, n, seed=OMEGA_SEED, workspace=ws, out=W)
+        torch.cuda.current_stream().wait_stream(side)
+        g = torch.cuda.CUDAGraph()
+        c0 = shg.launch_count()
+        with torch.cuda.graph(g):
+            shg.project(A, 0, n, seed=OMEGA_SEED, workspace=ws, out=W)
+        launches = shg.launch_count() - c0
+    finally:
+        shg.set_inkernel_omega(False)
+    torch.cuda.synchronize()
+    ts = []
+    for i in range(steps):
+        scrub.fill_(i & 0xFF)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        g.replay()
+        b.record()
+        torch.cuda.synchronize()
+        ts.append(a.elapsed_time(b) * 1e3)
+    return {"us_per_step": statistics.mean(ts), "us_median": statistics.median(ts), "kernels_per_step": launches,
+            "tflops": 2.0 * m * k * n / (statistics.mean(ts) * 1e-6) / 1e12,
+            "step": "project(A, mode 0, n) with Omega generated in the mainloop (OMGEN)"}
 
 
 def measure_extras(shg, torch, hbm, tc16_burst, tc_ratio, reps=10):
