@@ -21,12 +21,22 @@ for mode in range(3):
 shg.set_inkernel_omega(True)
 shg.project(T, 0, 16)
 shg.set_inkernel_omega(False)
-# later paths: Omega multicast (2 / 3 pairs per cluster), wide 288, k-tiled Omega, project slab views
+# later paths: pairs, wide 288, k-tiled Omega, project slab views
 # with S % 32 == 0 (second half of a stage continues in the next slab), row-sharded Omega, probes
 A2 = torch.randn(1100, 512, device="cuda", generator=g)
 Om2 = shg.gen_omega(512, 256, seed=3)
-for mc in (2, 3):
-    shg.shgemm(A2, Om2, tune={"pair": 1, "omega_mcast": mc})
+shg.shgemm(A2, Om2, tune={"pair": 1})
+# round 2: row-major Omega (transpose pass; TF32 widening; CUDA-core fallback), stream-K (pairs, wide,
+# single CTAs), several N tiles (evict_normal A), shgemm_host with a short last chunk
+Om_row = shg.gen_omega(512, 256, seed=3, layout="row")
+shg.shgemm(A2, Om_row)
+shg.shgemm(A2, Om_row, tc="tf32")
+shg.shgemm(A2, Om_row, tune={"force_simt": 1})
+A3 = torch.randn(1100, 4096, device="cuda", generator=g)
+for n, t in ((256, {"stream_k": 1}), (272, {"stream_k": 1}), (64, {"stream_k": 1, "pair": 2, "max_ctas": 64})):
+    shg.shgemm(A3, shg.gen_omega(4096, n, seed=6), tune=t)
+shg.shgemm(A2, shg.gen_omega(512, 600, seed=7))
+shg.shgemm_host(A2.cpu().pin_memory(), Om_row, chunk_rows=512)
 shg.shgemm(A2, shg.gen_omega(512, 288, seed=4))
 shg.shgemm_tiled(A2, shg.gen_omega_tiled(512, 200, seed=5), 200)
 T2 = torch.randn(6, 32, 96, device="cuda", generator=g)
