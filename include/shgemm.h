@@ -93,7 +93,8 @@ typedef struct {
     int32_t force_simt;  /* 1 = force the CUDA-core fallback (tests) */
     /* Diagnostics only (results are WRONG when debug_flags != 0): bit0 skip the TMEM->register
      * promotion loads, bit1 skip the splitter arithmetic, bit2 skip the MMAs, bit3 skip the Omega
-     * loads. */
+     * loads, bit4 load Omega k-tile 0 for every stage (constant B data), bit5 load A's k-block 0 of
+     * its rows for every stage (L2 hits instead of the HBM stream). */
     int32_t debug_flags;
     int32_t pair;        /* CTA pairs (tcgen05.mma.cta_group::2): 0 auto (BN >= 128 and m > 128), 1 on, 2 off */
     int32_t a_box;       /* row-major A staging: 0 auto (2 if k % 32 == 0 and lda >= 2 MiB, else 1), 1 two TMA boxes of

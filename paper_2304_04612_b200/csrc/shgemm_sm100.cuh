@@ -91,7 +91,10 @@ struct KParams {
     float* sk_ws;
     uint32_t* sk_cnt;
     uint32_t dbg;           // diagnostics: bit0 skip promotion loads, bit1 skip split math, bit2 skip MMAs,
-                            //              bit3 skip the Omega TMA (results are wrong when dbg != 0)
+                            //              bit3 skip the Omega TMA, bit4 Omega TMA always loads k-tile 0
+                            //              (same transfers, constant B data), bit5 A TMA always loads
+                            //              k-block 0 of its rows (L2 hits, no HBM stream)
+                            //              (results are wrong when dbg != 0)
     long long* prof;        // diagnostics: per-CTA wait-cycle counters [gridDim.x][16] (ProfSlot)
 };
 
@@ -901,7 +904,7 @@ shgemm_sm100_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_const
                     for (int kb = kb0; kb < kb1; ++kb) {
                         mbar_wait_prof(&a_empty[sa], pa ^ 1u, w);
                         mbar_arrive_expect_tx(&a_full[sa], kA32StageBytes);
-                        const int64_t kk = static_cast<int64_t>((wk.kb0 + (kb))) * kBK;
+                        const int64_t kk = (p.dbg & 32u) ? 0 : static_cast<int64_t>((wk.kb0 + (kb))) * kBK;
                         const int c0 = static_cast<int>(kk % p.k_inner);
                         const int c2 = static_cast<int>(kk / p.k_inner);
                         uint8_t* dst = a32 + sa * kA32StageBytes;
@@ -955,7 +958,7 @@ shgemm_sm100_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_const
                         }
                         if (!skip) {
                             for (int t = 0; t < nst; ++t) {
-                                const int kcoord = (wk.kb0 + (kb + t)) * kBK;
+                                const int kcoord = (p.dbg & 16u) ? 0 : (wk.kb0 + (kb + t)) * kBK;
                                 if constexpr (OMGEN) acquire_flag(p.om_flags + kcoord / kBK);   // generated in-kernel
                                 // FP16: one 128-B box row = 64 k; TF32: two k-halves of 32 k
 #pragma unroll

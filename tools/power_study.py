@@ -6,7 +6,9 @@ import paper_2304_04612_b200 as shg
 m, k, n = 1 << 21, 4096, 256
 A = shg.synth('gauss', 2, 0x100, m, k); Om = shg.gen_omega(k, n); Y = torch.empty((m, n), device='cuda')
 pl = shg.plan(m, n, k); prof = torch.zeros((pl['grid'], 16), dtype=torch.int64, device='cuda')
-for flags, name in [(0, 'full'), (8, 'no_omega_tma'), (1, 'no_promotion_loads'), (2, 'no_split_math'), (4, 'no_mma'), (0, 'full_again')]:
+CASES = [(0, 'full'), (8, 'no_omega_tma'), (16, 'omega_const_tile'), (32, 'a_const_kblock'), (48, 'both_const'),
+         (1, 'no_promotion_loads'), (2, 'no_split_math'), (3, 'no_split_no_promo'), (4, 'no_mma'), (0, 'full_again')]
+for flags, name in CASES:
     time.sleep(1.0)
     tune = {'prof': prof.data_ptr(), 'debug_flags': flags}
     t0 = time.time(); reps = 0
