@@ -111,12 +111,15 @@ typedef struct {
     int64_t *prof;
     int32_t omega_layout; /* shg_omega_layout_t of the Omega argument: SHG_OMEGA_ROW_MAJOR (0, default;
                              ldo >= n) or SHG_OMEGA_COL_MAJOR (ldo >= k). A NULL tune means row-major. */
-    int32_t stream_k;     /* work schedule: 0 auto (= whole tiles), 1 stream-K, 2 whole tiles. Stream-K
-                             cuts the (tile, k-block) iterations into one equal contiguous range per SM
-                             (pair) and sums the partial tiles in-kernel in fixed k order
-                             (deterministic). Measured no faster under the 1000 W cap
-                             (DESIGN.md §5), so auto keeps whole tiles. Needs one N tile, no split_k
-                             > 1 and >= 4 k-blocks per unit: otherwise SHG_ERR_INVALID_VALUE. */
+    int32_t stream_k;     /* work schedule: 0 auto, 1 stream-K, 2 whole tiles. Stream-K cuts the
+                             (tile, k-block) iterations into one equal contiguous range per SM (pair)
+                             and sums the partial tiles in-kernel in fixed k order (deterministic).
+                             Auto uses it on the HBM side (BN <= 160) when whole tiles would leave the
+                             last wave < 92% busy (one N tile, >= half as many tiles as SMs (pairs),
+                             k >= 1024): e.g. m = k = 32768, n = 128, 15% faster. Needs
+                             one N tile, no split_k > 1 and >= 4 k-blocks per unit: otherwise
+                             SHG_ERR_INVALID_VALUE. Row shards of one Y are bitwise equal to the
+                             unsharded Y only under whole tiles (stream-K's sums depend on the grid). */
 } shg_tune_t;
 
 /* Plan the library would use for an (m, n, k) shgemm on the current device. */

@@ -230,12 +230,15 @@ struct OmGen {
     uint32_t* flags;        // ceil(k/64) zero-initialised ready flags
 };
 
-// Stream-K is an opt-in schedule (tune->stream_k = 1): auto does not pick it. Measured interleaved
-// against whole tiles under the 1000 W cap (profiles/r02_ab_streamk.jsonl): cfg2's projection 0.298
-// vs 0.297 ms (the 10 extra pairs run 13% more cycles per stage at a lower clock) and cfg5 n = 256
-// 0.930 vs 0.951 ms: the idle last wave of whole tiles is paid back by the power cap.
-constexpr bool kSkAuto = false;
-constexpr double kSkMinWaveEff = 0.92;   // the auto rule if kSkAuto were set
+// Stream-K is chosen automatically only on the HBM side of the roofline (BN <= kSkAutoMaxBn), where
+// a partly idle last wave of whole tiles cannot keep HBM busy: measured interleaved under the 1000 W
+// cap (profiles/r02_ab_streamk2.jsonl), m = k = 32768: n = 128 0.863 -> 0.749 ms, n = 64 0.694 ->
+// 0.653, n = 96 0.685 -> 0.646. On the tensor side the idle wave is paid back by the power cap
+// (profiles/r02_ab_streamk.jsonl: cfg2's projection 0.297 vs 0.298 ms, n = 192 0.970 vs 0.992), and
+// short-wide split-K shapes (cfg3's unfoldings) stay split (r02_ab_streamk3.jsonl).
+constexpr bool kSkAuto = true;
+constexpr int kSkAutoMaxBn = 160;
+constexpr double kSkMinWaveEff = 0.92;   // ... and whole tiles would leave the last wave < 92% busy
 
 
 // om_rm: Omega is row-major; the FP16 tensor-core path then reads a column-major copy
@@ -301,8 +304,8 @@ Plan make_plan(int64_t m, int64_t n, int64_t k, bool fast_ok, const shg_tune_t* 
     const double wave_eff = static_cast<double>(mn_tiles) / static_cast<double>(waves * slots);
     const bool sk_fits = allow_sk && pl.n_tiles == 1 && mn_tiles * pl.num_kb >= int64_t(4) * slots &&
                          !(tune && tune->split_k > 1);
-    pl.sk = sk_fits && (sk_mode == 1 || (kSkAuto && sk_mode == 0 && wave_eff < kSkMinWaveEff &&
-                                          2 * mn_tiles >= slots && pl.num_kb >= 16));
+    pl.sk = sk_fits && (sk_mode == 1 || (kSkAuto && sk_mode == 0 && pl.bn <= kSkAutoMaxBn &&
+                                          wave_eff < kSkMinWaveEff && 2 * mn_tiles >= slots && pl.num_kb >= 16));
     if (sk_mode == 1 && !sk_fits) { pl.path = -1; return pl; }
     int splits = 1;
     if (tune && tune->split_k > 0) {

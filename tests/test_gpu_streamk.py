@@ -28,9 +28,15 @@ def _A(m, k, seed):
     return torch.randn(m, k, device="cuda", generator=g)
 
 
-def test_stream_k_is_opt_in(shg):
-    """Auto keeps whole tiles (stream-K measured no faster under the power cap)."""
+def test_stream_k_auto_rule(shg):
+    """Auto: stream-K on the HBM side with a badly quantised last wave (m = k = 32768, n = 64..128:
+    256 / 128 tiles on 148 / 74 units), whole tiles on the tensor side (no gain under the power cap)
+    and where the waves are full."""
+    assert shg.plan(32768, 128, 32768)["stream_k"] == 1
+    assert shg.plan(32768, 64, 32768)["stream_k"] == 1
+    assert shg.plan(32768, 256, 32768)["stream_k"] == 0
     assert shg.plan(16384, 272, 16384)["stream_k"] == 0
+    assert shg.plan(1024, 64, 1 << 20)["stream_k"] == 0 and shg.plan(1024, 64, 1 << 20)["split_k"] > 1
     assert shg.plan(16384, 272, 16384, {"stream_k": 1})["stream_k"] == 1
     assert shg.plan(32768, 256, 32768, {"stream_k": 1})["stream_k"] == 1
     assert shg.plan(4194304, 256, 4096)["stream_k"] == 0
