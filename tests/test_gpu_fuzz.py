@@ -33,15 +33,18 @@ def case(i):
         tune["split_k"] = int(r.integers(1, 6))
     if r.random() < 0.2:
         tune["pair"] = int(r.integers(1, 3))
+    if r.random() < 0.25:
+        tune["stream_k"] = int(r.integers(1, 3))     # forced stream-K / whole tiles (0 = auto)
+    row_omega = r.random() < 0.3                      # SURVEY §8(b)'s row-major Omega
     dist = int(r.integers(0, 4)) if kind != "tcec" else 0
     tiled = kind == "fp16" and not mmajor and k % 4 == 0 and r.random() < 0.3
     scale = float(np.exp(r.uniform(-4, 4)))
-    return m, k, n, kind, mmajor, tune, dist, tiled, scale
+    return m, k, n, kind, mmajor, tune, dist, tiled, scale, row_omega
 
 
 @pytest.mark.parametrize("i", range(240))
 def test_fuzz(shg, orc, i):
-    m, k, n, kind, mmajor, tune, dist, tiled, scale = case(i)
+    m, k, n, kind, mmajor, tune, dist, tiled, scale, row_omega = case(i)
     r = np.random.default_rng(i)
     A = (r.standard_normal((m, k)) * scale).astype(np.float32)
     # the M-major path needs a 16-B aligned row pitch for the tensor-core route; pad the stored
@@ -66,7 +69,7 @@ def test_fuzz(shg, orc, i):
             assert np.all(np.abs(C - y64) <= bound + 1e-300)
             assert e <= 1e-5 and (k < 16 or e <= 2 * e32), (e, e32)
             return
-        Om = shg.gen_omega(k, n, seed=i, dist=dist)
+        Om = shg.gen_omega(k, n, seed=i, dist=dist, layout="row" if row_omega else "col")
         Ad = dev_A()
         if tiled:
             Y = shg.shgemm_tiled(Ad, shg.gen_omega_tiled(k, n, seed=i, dist=dist), n, tune=tune or None)

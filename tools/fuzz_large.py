@@ -28,13 +28,16 @@ def case(i):
         tune["split_k"] = int(r.integers(1, 5))
     if r.random() < 0.2:
         tune["pair"] = int(r.integers(1, 3))
+    if r.random() < 0.25:
+        tune["stream_k"] = int(r.integers(1, 3))     # forced stream-K / whole tiles (0 = auto)
+    row_omega = r.random() < 0.3                      # SURVEY §8(b)'s row-major Omega
     dist = int(r.integers(0, 4)) if kind != "tcec" else 0
     scale = float(np.exp(r.uniform(-3, 3)))
-    return m, k, n, kind, mmajor, tune, dist, scale
+    return m, k, n, kind, mmajor, tune, dist, scale, row_omega
 
 
 def run(i):
-    m, k, n, kind, mmajor, tune, dist, scale = case(i)
+    m, k, n, kind, mmajor, tune, dist, scale, row_omega = case(i)
     g = torch.Generator(device="cuda").manual_seed(i)
     A = torch.randn(m, k, device="cuda", generator=g) * scale
     if mmajor:
@@ -59,7 +62,7 @@ def run(i):
             assert np.all(np.abs(Cn - y64) <= bound), float(np.max(np.abs(Cn - y64) / np.maximum(bound, 1e-300)))
             assert orc.relative_error(Cn, y64) <= 1e-5
             return
-        Om = shg.gen_omega(k, n, seed=i, dist=dist)
+        Om = shg.gen_omega(k, n, seed=i, dist=dist, layout="row" if row_omega else "col")
         if mmajor:
             Y = shg.shgemm_at(Ad.t(), Om, tune=tune or None, tc=kind)
         else:
