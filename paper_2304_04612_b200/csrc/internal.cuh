@@ -65,14 +65,14 @@ shg_status_t launch_tc(const CUtensorMap& mapA, const CUtensorMap& mapB0, const 
     if (attr_err != cudaSuccess) return cuda_fail(attr_err, "cudaFuncSetAttribute");
     if constexpr (!PAIR) {
         // plain launch: a cluster-dimension attribute (even 1x1x1) takes a slower launch path
-        kern<<<grid, shg::kThreads, CF::kSmemBytes, stream>>>(mapA, mapB0, mapB1, kp);
+        kern<<<grid, shg::threads_for<OMGEN>(), CF::kSmemBytes, stream>>>(mapA, mapB0, mapB1, kp);
         g_launches.fetch_add(1, std::memory_order_relaxed);
         SHG_CUDA(cudaGetLastError());
         return SHG_OK;
     }
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(grid);
-    cfg.blockDim = dim3(shg::kThreads);
+    cfg.blockDim = dim3(shg::threads_for<OMGEN>());
     cfg.dynamicSmemBytes = CF::kSmemBytes;
     cfg.stream = stream;
     cudaLaunchAttribute attr[1];
@@ -146,5 +146,5 @@ shg_status_t dispatch_tc_tcec(int bn, bool mmajor, bool pair, const CUtensorMap&
 // SHGEMM-FP16 single CTAs with cooperative in-kernel Omega generation (tc_f16_gen.cu), BN <= 192
 shg_status_t dispatch_tc_f16_gen(int bn, bool mmajor, const CUtensorMap& a, const CUtensorMap& b0,
                                  const CUtensorMap& b1, const shg::KParams& kp, int grid, cudaStream_t s);
-constexpr int kOmGenMaxBn = 192;
+constexpr int kOmGenMaxBn = shg::kOmGenMaxBnKernel;
 }  // namespace shg_api

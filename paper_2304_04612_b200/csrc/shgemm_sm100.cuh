@@ -49,6 +49,13 @@ constexpr int kNumSplitWarps = 8;                 // warps 0..7
 constexpr int kEpiWarp0 = 8;                      // warps 8..15
 constexpr int kWarpProdA = 16, kWarpMMA = 17, kWarpProdB = 18;   // warp 19 idle
 constexpr int kThreads = 640;
+// OMGEN kernels (in-kernel Omega) add 8 generator warps (20..27): 896 threads, 72 registers each at
+// launch; the roles then take splitter 256 x 56 + epilogue 256 x 104 + control 128 x 32 + generator
+// 256 x 72 = 63488 of the 64512 (BN <= kOmGenMaxBnKernel keeps the epilogue's accumulators in 104)
+constexpr int kThreadsGen = 896;
+constexpr int kWarpGen0 = 20;
+constexpr int kOmGenMaxBnKernel = 128;
+template <bool OMGEN> constexpr int threads_for() { return OMGEN ? kThreadsGen : kThreads; }
 // Register budget: setmaxnreg moves registers inside the CTA's own pool (640 threads x 96 = 61440):
 // splitter 256 x 56 + epilogue 256 x 168 + control 128 x 32 = 61440.
 constexpr int kSmemLimit = 232448;                // max dynamic smem per block on sm_100
@@ -70,7 +77,7 @@ struct KParams {
     int32_t b_lo_col;       // TCEC: column (n) coordinate of dB_low in the B tensor maps (B_low at 0)
     int32_t om_tiled;       // Omega in the k-tiled layout (3-D maps {64, n_pad, k/64}; SHGEMM-FP16 only)
     // Cooperative in-kernel Omega (om_gen = 1; single CTAs, one tile per CTA, n_tiles == 1): the
-    // epilogue warps of the CTA (m_blk, s) generate the k-tiles t of split s with
+    // generator warps (20..27) of the CTA (m_blk, s) generate the k-tiles t of split s with
     // (t - first tile of s) % m_tiles == m_blk into om_buf (k-tiled layout) and release flag[t];
     // the Omega stager acquires flag[t] before its TMA. Every tile is generated once, by one of the
     // m_tiles CTAs that read it.
@@ -421,12 +428,12 @@ __device__ __forceinline__ void add2_rn(float& a, float& b, float c, float d) {
 #endif
 
 // ------------------------------------------------------------------ cooperative Omega (om_gen)
-constexpr int kOmGenLookahead = 16;   // 64-k tiles generated ahead of the epilogue's current chunk
 
 __device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, 256;" ::: "memory"); }
+__device__ __forceinline__ void gen_bar() { asm volatile("bar.sync 2, 256;" ::: "memory"); }
 
 // 64-k tile t of the k-tiled Omega (rows 64t..64t+63 of this operand, all n columns) by the 256
-// epilogue threads (tid 0..255): OMEGA_SPEC blocks q = om_q0 + 16t + ql; rows >= k written as 0.
+// generator threads (tid 0..255): OMEGA_SPEC blocks q = om_q0 + 16t + ql; rows >= k written as 0.
 __device__ __forceinline__ void gen_omega_tile(const KParams& p, int64_t t, int tid) {
     const omega::Keys keys = omega::philox_keys(p.om_seed);
     uint16_t* tile = p.om_buf + t * p.n * 64;
@@ -483,7 +490,7 @@ __device__ __forceinline__ void acquire_flag(const uint32_t* f) {
 //                 one tile per CTA): compiled only into the instantiations project() uses for it, so
 //                 the other kernels' epilogues carry no generator registers.
 template <int BN, bool MMAJOR, bool PAIR, bool TF32 = false, bool TCEC = false, bool OMGEN = false>
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __launch_bounds__(threads_for<OMGEN>(), 1)
 shgemm_sm100_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB0,
                     const __grid_constant__ CUtensorMap mapB1, const KParams p) {
     using CF = Cfg<BN, PAIR, TF32, TCEC>;
@@ -514,7 +521,7 @@ shgemm_sm100_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_const
 
     const uint32_t warp = warp_id();
     const uint32_t lane = threadIdx.x & 31u;
-    static_assert(!OMGEN || (!PAIR && !TF32 && !TCEC && BN <= 192), "in-kernel Omega: single-CTA SHGEMM-FP16");
+    static_assert(!OMGEN || (!PAIR && !TF32 && !TCEC && BN <= kOmGenMaxBnKernel), "in-kernel Omega: single-CTA SHGEMM-FP16");
     constexpr int CL = PAIR ? 2 : 1;                              // CTAs per cluster
     const uint32_t crank = PAIR ? cluster_ctarank() : 0u;         // rank in the pair: 0 = leader (issues the MMAs)
     const uint32_t lead = 0u;                                     // cluster rank of the pair's leader
@@ -690,7 +697,8 @@ shgemm_sm100_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_const
         // taking the h-th half of its columns, so a part's slot is released after half the per-warp
         // TMEM loads (the next stage's MMAs wait on it; K_c = 64 there). Otherwise group h drains
         // all of part h, which overlaps the other part's MMAs (measured 2.7% faster at BN = 256).
-        asm volatile("setmaxnreg.inc.sync.aligned.u32 168;");
+        if constexpr (OMGEN) asm volatile("setmaxnreg.inc.sync.aligned.u32 104;");
+        else asm volatile("setmaxnreg.inc.sync.aligned.u32 168;");
         const int q = static_cast<int>(warp & 3u);                       // TMEM lane quarter (warp_id % 4)
         const int h = static_cast<int>((warp - kEpiWarp0) >> 2);         // epilogue group
         const uint32_t lane_addr = static_cast<uint32_t>(32 * q) << 16;
@@ -711,27 +719,10 @@ shgemm_sm100_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_const
             const int m_blk = wk.m_blk, n_blk = wk.n_blk, kb0 = 0, kb1 = wk.nkb;
             (void)m_blk;
             (void)n_blk;
-            // cooperative Omega (p.om_gen): this CTA generates the tiles kb0s + m_blk + i * m_tiles of
-            // its split, each before the epilogue reaches the chunk kOmGenLookahead tiles earlier
-            // (a fixed schedule, uniform over the 8 warps: deadlock-free by induction over chunks)
-            const int64_t kb0s = (wk.kb0 + (kb0));
-            int64_t gen_next = kb0s + m_blk;
-            const int64_t gen_end = OMGEN ? kb0s + (kb1 - kb0) : 0;
-            auto gen_upto = [&](int64_t limit) {
-                if constexpr (!OMGEN) return;
-                while (gen_next < gen_end && gen_next < limit) {
-                    gen_omega_tile(p, gen_next, etid);
-                    epi_bar();
-                    if (etid == 0) release_flag(p.om_flags + gen_next);
-                    gen_next += p.m_tiles;
-                }
-            };
-            gen_upto(kb0s + kOmGenLookahead);
             float acc[NACC];
 #pragma unroll
             for (int i = 0; i < NACC; ++i) acc[i] = 0.0f;
             for (int kb = kb0; kb < kb1; kb += CF::KC, ++stage) {   // one promotion per K_c chunk
-                gen_upto((wk.kb0 + (kb)) + CF::KC + kOmGenLookahead);
 #pragma unroll
                 for (int part = 0; part < NQ; ++part) {
                     if (!mine(part)) continue;
@@ -778,7 +769,6 @@ shgemm_sm100_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_const
                     }
                 }
             }
-            gen_upto(gen_end);
             const long long ts0 = clock64();
             if (wk.slot >= 0) {
                 // ---- stream-K partial piece (sk_fixup): publish this piece's sums in its slot's plane
@@ -881,6 +871,23 @@ shgemm_sm100_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_const
             long long* pr = p.prof + blockIdx.x * kProfSlots;
             pr[kProfEpiAccFull] = w_full;
             pr[kProfEpiStore] = t_store;
+        }
+    } else if (OMGEN && warp >= kWarpGen0) {
+        // ============================================================ Omega generator (OMGEN)
+        // cooperative in-kernel Omega (p.om_gen): the CTA (m_blk, s) generates the 64-k tiles
+        // kb0s + m_blk + i * m_tiles of its split into the k-tiled buffer, in increasing k, and
+        // releases each tile's flag; the Omega stagers of the split's m_tiles CTAs acquire the flags
+        // before their TMA. Generation never waits on anything, so every flag is eventually set.
+        asm volatile("setmaxnreg.dec.sync.aligned.u32 72;");
+        const int gtid = static_cast<int>(threadIdx.x) - kWarpGen0 * 32;   // 0..255
+        Piece wk;
+        for (int it = 0; next_piece(p, unit, units, sr, it, wk); ++it) {
+            const int64_t kb0s = wk.kb0;
+            for (int64_t t = kb0s + wk.m_blk; t < kb0s + wk.nkb; t += p.m_tiles) {
+                gen_omega_tile(p, t, gtid);
+                gen_bar();
+                if (gtid == 0) release_flag(p.om_flags + t);
+            }
         }
     } else {
         asm volatile("setmaxnreg.dec.sync.aligned.u32 32;");

@@ -14,9 +14,6 @@ shg_status_t dispatch(int bn, const CUtensorMap& a, const CUtensorMap& b0, const
         case 64: return launch_tc<64, MMAJOR, false, false, false, true>(a, b0, b1, kp, grid, s);
         case 96: return launch_tc<96, MMAJOR, false, false, false, true>(a, b0, b1, kp, grid, s);
         case 128: return launch_tc<128, MMAJOR, false, false, false, true>(a, b0, b1, kp, grid, s);
-        case 144: return launch_tc<144, MMAJOR, false, false, false, true>(a, b0, b1, kp, grid, s);
-        case 160: return launch_tc<160, MMAJOR, false, false, false, true>(a, b0, b1, kp, grid, s);
-        case 192: return launch_tc<192, MMAJOR, false, false, false, true>(a, b0, b1, kp, grid, s);
         default: return SHG_ERR_INVALID_VALUE;
     }
 }
