@@ -565,6 +565,14 @@ def main():
     spec_tc = 2250.0 * tc_ratio
     roof["frac_spec_min(tc/2, AI*hbm)"] = useful_tflops / min(spec_tc / 2.0, ai * 8000.0 / 1e3)
 
+    # e2e on EVERY rank at once (each GPU streams its own row sample over its own PCIe link from
+    # pinned host memory): aggregate rows / max-over-ranks time
+    e2e = None
+    if not args.no_e2e:
+        try:
+            e2e = measure_e2e(shg, torch, k, n, steps=3, rank=rank, world=world, dist=dist, backend=backend)
+        except Exception as exc:  # noqa: BLE001
+            e2e = {"error": repr(exc)[:300]}
     out = None
     if rank == 0:
         # the other BASELINE configs first (device only, this workload's 64 GiB released: a resident
@@ -579,12 +587,6 @@ def main():
             except Exception as exc:  # noqa: BLE001
                 extras = {"error": repr(exc)[:300]}
                 torch.cuda.empty_cache()
-        e2e = None
-        if not args.no_e2e:
-            try:
-                e2e = measure_e2e(shg, torch, k, n, steps=3)
-            except Exception as exc:  # noqa: BLE001
-                e2e = {"error": repr(exc)[:300]}
         cpu = None
         if not args.no_cpu_baseline and world == 1:
             cpu = cpu_baseline(m_total, k, n)
@@ -808,12 +810,13 @@ def measure_pipelines(torch, reps=3):
     return out
 
 
-def measure_e2e(shg, torch, k, n, steps=3):
-    """Same metric through the C ABI with HOST buffers: each step copies a row sample of A from
-    pinned host memory to the device, projects it (shgemm_host streams overlapped chunks) and
-    copies Y back; host<->device copies are inside the timed region."""
+def measure_e2e(shg, torch, k, n, steps=3, rank=0, world=1, dist=None, backend=None):
+    """Same metric through the C ABI with HOST buffers: each step copies this rank's row sample of A
+    from pinned host memory to its device, projects it (shgemm_host streams overlapped chunks) and
+    copies Y back; host<->device copies are inside the timed region. All ranks run at once (a
+    barrier before the timed steps); value = all ranks' rows / the max-over-ranks time."""
     rows = 262144 if k <= 4096 else max(128, (1 << 30) // (4 * k))
-    A_h = shg.synth("gauss", DATA_SEED, DATA_STREAM, rows, k).cpu().pin_memory()
+    A_h = shg.synth("gauss", DATA_SEED, DATA_STREAM, rows, k, row0=rank * rows).cpu().pin_memory()
     Y_h = torch.empty((rows, n), dtype=torch.float32).pin_memory()
     ws = torch.empty(shg.host_workspace_size(n, k), dtype=torch.uint8, device="cuda")
 
@@ -824,6 +827,8 @@ def measure_e2e(shg, torch, k, n, steps=3):
     for _ in range(2):
         step()
     torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
     s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     s.record()
     for _ in range(steps):
@@ -831,9 +836,14 @@ def measure_e2e(shg, torch, k, n, steps=3):
     e.record()
     torch.cuda.synchronize()
     dt = s.elapsed_time(e) / 1e3 / steps
-    return {"value": 2.0 * rows * k * n / dt / 1e12, "unit": "TFLOP/s", "h2d_bytes_per_step": rows * k * 4,
-            "d2h_bytes_per_step": rows * n * 4, "rows_per_step": rows, "ms_per_step": dt * 1e3,
-            "api": "shgemm_host (C ABI, pinned host A/Y, overlapped chunk streaming)"}
+    if dist:
+        t = torch.tensor([dt], device="cuda" if backend == "nccl" else "cpu")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dt = float(t.item())
+    return {"value": 2.0 * world * rows * k * n / dt / 1e12, "unit": "TFLOP/s",
+            "h2d_bytes_per_step": world * rows * k * 4, "d2h_bytes_per_step": world * rows * n * 4,
+            "rows_per_step": world * rows, "ms_per_step": dt * 1e3, "ranks": world,
+            "api": "shgemm_host (C ABI, pinned host A/Y, overlapped chunk streaming), every rank"}
 
 
 if __name__ == "__main__":
