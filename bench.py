@@ -38,6 +38,7 @@ CONFIGS = {
     "cfg2proj": (16384, 16384, 272, "BASELINE config 2's projection (RSVD Alg 1 line 1): A 16384x16384 FP32 . "
                                     "Omega 16384x272 FP16"),
     "cfg5n64": (32768, 32768, 64, "BASELINE config 5 sweep point n=64 (m=k=32768)"),
+    "cfg5n128": (32768, 32768, 128, "BASELINE config 5 sweep point n=128 (m=k=32768)"),
     "cfg5n256": (32768, 32768, 256, "BASELINE config 5 sweep point n=256 (m=k=32768)"),
     "cfg5n1024": (32768, 32768, 1024, "BASELINE config 5 sweep point n=1024 (m=k=32768)"),
 }
@@ -510,6 +511,15 @@ def main():
     if dist:
         dist.barrier()
     clk = clocks.stop()
+    # §8(e) check: every rank regenerated the identical Omega from the shared seed (CRC32 of its bits,
+    # all-gathered; no Omega ever crossed between ranks)
+    from paper_2304_04612_b200.shard import checksum_bits
+    crc = checksum_bits(om_buf[:, :k])
+    crcs = [crc]
+    if dist:
+        got = [None] * world
+        dist.all_gather_object(got, crc)
+        crcs = got
     total_ms = (sum(ev[i][0].elapsed_time(ev[i][2]) for i in range(args.steps)) if flush
                 else t_start.elapsed_time(t_end))
     gemm_ms = statistics.mean(ev[i][1].elapsed_time(ev[i][2]) for i in range(args.steps))
@@ -614,6 +624,7 @@ def main():
                "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
                "clocks": clk, "omega_gen_ms": gen_ms, "shgemm_ms": gemm_ms, "other_workloads": extras,
                "fused_single_launch_step": fused,
+               "omega_crc32_per_rank": crcs, "omega_identical_on_all_ranks": len(set(crcs)) == 1,
                "gbs_algorithmic": achieved_gbs}
         print(json.dumps(out), flush=True)
     if dist:
