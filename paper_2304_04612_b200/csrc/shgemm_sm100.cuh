@@ -1055,8 +1055,14 @@ shgemm_sm100_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_const
                         const uint32_t a_cur = tmem_base + ABASE + cs * AST;
                         const uint64_t b_cur = sw128_kmajor_desc(smem_u32(om + cs * kOm));
                         const bool last = kb + 1 == kb1;
+                        // the part that closes at this stage goes FIRST: its drain then has the other
+                        // part's MMAs of this stage and the next one's (~1200 cycles) to hide behind
+                        // before it is reused (closing it last left ~300 cycles: the MMA waited on
+                        // acc_empty every other stage, profiles/r02_diag_wide2.jsonl)
+                        const int cfirst = ((kb - kb0) & 1) ? 0 : 1;
 #pragma unroll
-                        for (int q = 0; q < 2; ++q) {
+                        for (int qi = 0; qi < 2; ++qi) {
+                            const int q = qi ^ cfirst;
                             bool& pend = q ? pend1 : pend0;
                             uint32_t& u = q ? u1 : u0;
                             const bool close = (((kb - kb0) + q) & 1) == 1 || last;
