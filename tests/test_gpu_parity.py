@@ -304,6 +304,10 @@ def test_config4_full_size_sampled(shg, orc):
     A = shg.synth("gauss", 2, 0x100, m, k)
     Om = shg.gen_omega(k, n, seed=0)
     Y = shg.shgemm(A, Om)
+    # the same product through §8(b)'s row-major Omega: bitwise the same Y at full size
+    Y_rm = shg.shgemm(A[: 1 << 20], shg.gen_omega(k, n, seed=0, layout="row"))
+    assert torch.equal(Y_rm, Y[: 1 << 20])
+    del Y_rm
     torch.cuda.synchronize()
     rng = np.random.default_rng(0)
     rows = np.unique(np.concatenate([[0, 127, 128, m - 1], rng.integers(0, m, 252)]))
@@ -400,8 +404,9 @@ def test_concurrent_streams_and_threads(shg):
 
 
 def test_config5_full_size_sampled(shg, orc):
-    """BASELINE config 5 at full size (A 32768^2 FP32 = 4 GiB) for n = 16 (HBM-bound, split-K),
-    n = 1024 and n = 4096 (tensor-bound, several N tiles): 64 sampled rows each against the oracle."""
+    """BASELINE config 5 at full size (A 32768^2 FP32 = 4 GiB) for n = 16 and 128 (HBM-bound,
+    stream-K plans; n = 128 with the row-major Omega of §8(b)), n = 1024 and n = 4096 (tensor-bound,
+    several N tiles): 64 sampled rows each against the oracle."""
     m = k = 32768
     A = shg.synth("gauss", 5, 0x105, m, k)
     rng = np.random.default_rng(5)
@@ -409,8 +414,8 @@ def test_config5_full_size_sampled(shg, orc):
     ridx = torch.from_numpy(rows).cuda()
     Arows = to_np(A[ridx])
     assert np.array_equal(Arows[:3], orc.synth_rows("gauss", 5, 0x105, rows[:3], k))
-    for n in (16, 1024, 4096):
-        Om = shg.gen_omega(k, n, seed=n)
+    for n in (16, 128, 1024, 4096):       # 16 / 128: stream-K plans (auto), 1024 / 4096: 4 / 16 N tiles
+        Om = shg.gen_omega(k, n, seed=n, layout="row" if n == 128 else "col")
         Ys = to_np(shg.shgemm(A, Om)[ridx])
         check_bars(orc, Arows, omega_bits(Om), Ys)
         del Om
