@@ -122,3 +122,26 @@ def test_stream_k_config2_full_size(shg, orc):
     rows = np.unique(np.concatenate([np.arange(0, m, 97), [m - 1]]))
     A_s = orc.synth_rows("gauss", 2, 0x101, rows, k)
     check_bars(orc, A_s, omega_bits(Om), to_np(Y)[rows])
+
+
+@pytest.mark.parametrize("variant", ["auto", "row_major", "tf32", "tcec_mmajor"])
+def test_config2_projection_full_size_variants(shg, orc, variant):
+    """BASELINE config 2's projection (16384^2 . 16384 x 272) on the default plan (one wide pair
+    tile, staggered two-stage promotion), with §8(b)'s row-major Omega, on SHGEMM-TF32, and the
+    pipeline's line-3 product B^T = A^T Q (TCEC-SGEMM, A read in place as MN-major, wide pair tile);
+    sampled rows against the oracle."""
+    m = k = 16384
+    n = 272
+    A = shg.synth("gauss", 3, 0x101, m, k)
+    rows = np.unique(np.concatenate([np.arange(0, m, 131), [m - 1]]))
+    if variant == "tcec_mmajor":
+        Q = _A(k, n, 17)
+        C = shg.tcec_sgemm(A.t(), Q)                     # (A^T) Q: A^T is MN-major, m x k = 16384^2
+        At_rows = np.ascontiguousarray(to_np(A.t()[torch.from_numpy(rows).cuda()]))
+        e = orc.relative_error(to_np(C)[rows], orc.gemm_y64_f32b(At_rows, to_np(Q)))
+        assert e <= 1e-5, e
+        return
+    Om = shg.gen_omega(k, n, seed=0, layout="row" if variant == "row_major" else "col")
+    Y = shg.shgemm(A, Om, tc="tf32" if variant == "tf32" else None)
+    A_s = orc.synth_rows("gauss", 3, 0x101, rows, k)
+    check_bars(orc, A_s, omega_bits(Om), to_np(Y)[rows])
