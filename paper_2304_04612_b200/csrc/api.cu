@@ -639,8 +639,12 @@ HostWs host_ws(int64_t m, int64_t n, int64_t k, int64_t chunk_rows, bool om_rm) 
     col.omega_layout = SHG_OMEGA_COL_MAJOR;
     size_t sk = 0;
     const int sms = std::max(1, dev_info().sms);
-    for (int64_t rows = 128; rows <= w.chunk; rows += 128)
+    // split-K scratch only exists while the m-tiles do not fill the SMs (<= sms x 256 rows); past
+    // that the plan's scratch (stream-K planes) no longer depends on the height
+    const int64_t scan = std::min<int64_t>(w.chunk, int64_t(sms) * 256 + 256);
+    for (int64_t rows = 128; rows <= scan; rows += 128)
         sk = std::max(sk, static_cast<size_t>(make_plan(rows, n, k, true, &col, sms).ws_bytes));
+    sk = std::max(sk, static_cast<size_t>(make_plan(w.chunk, n, k, true, &col, sms).ws_bytes));
     w.sk_bytes = up(sk);
     w.total = w.om_bytes + 2 * (w.a_bytes + w.y_bytes + w.sk_bytes);
     return w;
