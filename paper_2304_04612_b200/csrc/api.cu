@@ -640,11 +640,16 @@ HostWs host_ws(int64_t m, int64_t n, int64_t k, int64_t chunk_rows, bool om_rm) 
     size_t sk = 0;
     const int sms = std::max(1, dev_info().sms);
     // split-K scratch only exists while the m-tiles do not fill the SMs (<= sms x 256 rows); past
-    // that the plan's scratch (stream-K planes) no longer depends on the height
+    // that a height can only plan stream-K, whose planes do not depend on it and whose counters
+    // grow with it: bounded by the forced stream-K plan of the full chunk
     const int64_t scan = std::min<int64_t>(w.chunk, int64_t(sms) * 256 + 256);
     for (int64_t rows = 128; rows <= scan; rows += 128)
         sk = std::max(sk, static_cast<size_t>(make_plan(rows, n, k, true, &col, sms).ws_bytes));
     sk = std::max(sk, static_cast<size_t>(make_plan(w.chunk, n, k, true, &col, sms).ws_bytes));
+    shg_tune_t col_sk = col;
+    col_sk.stream_k = 1;
+    const Plan psk = make_plan(w.chunk, n, k, true, &col_sk, sms);
+    if (psk.path == 0) sk = std::max(sk, static_cast<size_t>(psk.ws_bytes));
     w.sk_bytes = up(sk);
     w.total = w.om_bytes + 2 * (w.a_bytes + w.y_bytes + w.sk_bytes);
     return w;
