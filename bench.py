@@ -720,6 +720,27 @@ def measure_extras(shg, torch, hbm, tc16_burst, tc_ratio, reps=10):
         return d
 
     out = {}
+    # a READ-ONLY HBM stream (reported beside the copy bandwidth of MEASURED_PEAKS.json):
+    # the library's TMA-only probe streams a 4 GiB matrix into shared memory in the mainloop's tile
+    # order (one 4-D box of 2 x 32 k x 128 rows per stage, no math)
+    try:
+        import ctypes
+        L = shg.lib()
+        buf = torch.empty(32768 * 32768, device="cuda")
+        cnt = torch.zeros(1, dtype=torch.int64, device="cuda")
+
+        def tma_read():
+            st = L.shg_probe_tma_read(ctypes.c_void_p(buf.data_ptr()), 32768, 32768, 32768, 2, 64, 128, 1, 148,
+                                      ctypes.c_void_p(cnt.data_ptr()), ctypes.c_void_p(torch.cuda.current_stream().cuda_stream))
+            assert st == 0, st
+        ms = med_ms(tma_read)
+        out["hbm_read_only_probe"] = {"ms": ms, "gbs": 4.0 * 32768 * 32768 / ms / 1e6,
+                                      "note": "shg_probe_tma_read: TMA-only read of 4 GiB (256 B per row visit), "
+                                              "back to back; the HBM-bound kernels' GB/s can be read against it too"}
+        del buf, cnt
+        torch.cuda.empty_cache()
+    except Exception as exc:  # noqa: BLE001
+        out["hbm_read_only_probe"] = {"error": repr(exc)[:200]}
     # context for the power cap: cuBLAS bf16 on cfg4's own shape (one 16-bit product, half the A bytes)
     m4, k4, n4 = 4194304, 4096, 256
     Ab = torch.randn(m4, k4, device="cuda", dtype=torch.bfloat16)
