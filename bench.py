@@ -418,7 +418,9 @@ def main():
     torch.cuda.set_device(local)
     dist = None
     backend = None
-    if world > 1:
+    # SHG_BENCH_FORCE_DIST=1 (under torchrun): set up the process group even for one rank, so the
+    # NCCL plumbing (barrier, MAX all-reduce of the time, Omega CRC all-gather) runs on a 1-GPU box
+    if world > 1 or (os.environ.get("SHG_BENCH_FORCE_DIST") == "1" and "WORLD_SIZE" in os.environ):
         import torch.distributed as dist
         # one rank per GPU over NCCL (the driver's launch); more ranks than GPUs (a functional test of
         # the sharded path on one device) cannot share a GPU under NCCL, so that case uses gloo.

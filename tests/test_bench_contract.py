@@ -73,3 +73,26 @@ def test_row_partition_covers_rows_once():
             else:
                 assert sum(r for _, r in covered) == m
                 assert all(covered[i][0] + covered[i][1] == covered[i + 1][0] for i in range(g - 1) if covered[i + 1][1])
+
+
+@pytest.mark.gpu
+def test_bench_nccl_plumbing_one_rank():
+    """The NCCL path of the multi-rank bench (process group on the GPU, barrier, MAX all-reduce of the
+    timed region, all-gather of the per-rank Omega CRC) on a one-GPU box: torchrun with one rank and
+    SHG_BENCH_FORCE_DIST=1."""
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    env = dict(os.environ, SHG_BENCH_FORCE_DIST="1")
+    res = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=1",
+                          "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.join(ROOT, "bench.py"),
+                          "--config", "cfg5n64", "--steps", "3", "--warmup", "3", "--no-extras", "--no-cpu-baseline",
+                          "--no-e2e"], capture_output=True, text=True, timeout=600, cwd=ROOT, env=env)
+    assert res.returncode == 0, res.stderr[-2000:]
+    d = json.loads([l for l in res.stdout.splitlines() if l.startswith("{")][-1])
+    assert d["config"]["dist_backend"] == "nccl" and d["n_gpus"] == 1
+    assert d["omega_identical_on_all_ranks"] is True and d["value"] > 0
