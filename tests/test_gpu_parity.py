@@ -682,3 +682,30 @@ def test_nonfinite_flag_every_plan(shg, m, k, n, tune, mmajor):
             assert bool(finite_rows.all())
         else:
             assert int(flag.item()) == 0 and bool(finite_rows.all())
+
+
+def test_omega_statistics_1e8(shg):
+    """the Gaussian Omega's statistics on >= 1e8 samples (device-generated; bit-identical
+    to the oracle's stream, test_omega_bit_exact_1e8): mean 0 and variance 1 within 5 sigma_MC of the
+    FP16-rounded N(0,1) truncated at |z| <= 5.77 (OMEGA_SPEC), kurtosis 3, symmetry of the signs, and
+    the FP16-subnormal-or-zero rate 2 phi(0) 2^-14 = 4.87e-5 (reading c4-20)."""
+    import math
+    n_tot, s1, s2, s4, neg, sub = 0, 0.0, 0.0, 0.0, 0, 0
+    for stream in range(2):
+        Om = shg.gen_omega(1 << 20, 64, seed=99, stream_id=stream, layout="row")    # 2^26 per stream
+        z = Om.double().flatten()
+        n_tot += z.numel()
+        s1 += float(z.sum())
+        s2 += float((z * z).sum())
+        s4 += float((z ** 4).sum())
+        neg += int((z < 0).sum())
+        sub += int(((Om.view(torch.int16) & 0x7C00) == 0).sum())
+    assert n_tot >= 1e8
+    mean, var = s1 / n_tot, s2 / n_tot
+    kurt = (s4 / n_tot) / var ** 2
+    assert abs(mean) < 5.0 / math.sqrt(n_tot), mean
+    assert abs(var - 1.0) < 5.0 * math.sqrt(2.0 / n_tot) + 1e-6, var      # + FP16 rounding of the draws
+    assert abs(kurt - 3.0) < 5.0 * math.sqrt(24.0 / n_tot) + 1e-4, kurt
+    assert abs(neg / n_tot - 0.5) < 5.0 * 0.5 / math.sqrt(n_tot), neg / n_tot
+    p = 2.0 / math.sqrt(2 * math.pi) * 2.0 ** -14
+    assert abs(sub / n_tot - p) < 5.0 * math.sqrt(p / n_tot), sub / n_tot

@@ -169,3 +169,13 @@ def test_sparse_sign(orc, dist, k, s):
     assert set(np.unique(om).tolist()) <= {0, 0x3C00, 0xBC00}
     T = orc.sparse_threshold(dist, k)
     assert T == math.floor(2 ** 31 / s)
+
+
+@pytest.mark.parametrize("stream_id", [0, 1, 2])
+def test_square_blocks_full_rank(orc, stream_id):
+    """SURVEY c6 / S:317: k x k blocks of the FP16 Gaussian Omega are of full rank for k <= 64 (a
+    generator with a stuck counter field or a repeated column would produce rank-deficient blocks)."""
+    for k in (1, 2, 3, 4, 8, 16, 32, 64):
+        for seed in (0, 7, 12345):
+            om = orc.f16_bits_as_float(orc.omega_f16(k, k, seed=seed, stream_id=stream_id)).astype(np.float64)
+            assert np.linalg.matrix_rank(om) == k, (k, seed, stream_id)
