@@ -709,3 +709,19 @@ def test_omega_statistics_1e8(shg):
     assert abs(neg / n_tot - 0.5) < 5.0 * 0.5 / math.sqrt(n_tot), neg / n_tot
     p = 2.0 / math.sqrt(2 * math.pi) * 2.0 ** -14
     assert abs(sub / n_tot - p) < 5.0 * math.sqrt(p / n_tot), sub / n_tot
+
+
+@pytest.mark.parametrize("dist", ["normal", "uniform"])
+@pytest.mark.parametrize("k", [16, 64, 256, 1024, 4096])
+def test_elementwise_bar_100_trials(shg, orc, dist, k):
+    """SURVEY c6 "Bounds": the elementwise bar of c5 (P:594-597 plus the split term) and the
+    Frobenius bars hold in 100 trials per k for both A distributions of the paper's accuracy
+    experiment (A ~ N(0,1) and U(0,1); Gaussian Omega), 64 x k x 32 each."""
+    m, n = 64, 32
+    worst = 0.0
+    for t in range(100):
+        A = synth.gaussian(m, k, seed=7000 + t) if dist == "normal" else synth.uniform(m, k, seed=7000 + t)
+        om, Y = _run(shg, A, k, n, seed=t)
+        _, _, w = check_bars(orc, A, om, Y)
+        worst = max(worst, w)
+    assert worst <= 1.0
