@@ -176,12 +176,17 @@ def omega_layout(Omega: torch.Tensor):
     stride(0) == 1, row-major if stride(1) == 1; the layout is passed explicitly, never inferred
     from ldo by the library."""
     k, n = Omega.shape
+    s0, s1 = Omega.stride()
     if k <= 1 and n <= 1:
         return OMEGA_COL_MAJOR, max(k, 1)
-    if n <= 1 or (k > 1 and Omega.stride(0) == 1):
-        return OMEGA_COL_MAJOR, (Omega.stride(1) if n > 1 else max(k, 1))
-    if k <= 1 or Omega.stride(1) == 1:
-        return OMEGA_ROW_MAJOR, (Omega.stride(0) if k > 1 else max(n, 1))
+    if k <= 1:     # one row: element (0, j) at j * s1 -> row-major if s1 == 1, else column-major, ldo = s1
+        return (OMEGA_ROW_MAJOR, max(n, 1)) if s1 == 1 else (OMEGA_COL_MAJOR, s1)
+    if n <= 1:     # one column: element (i, 0) at i * s0 -> column-major if s0 == 1, else row-major, ldo = s0
+        return (OMEGA_COL_MAJOR, max(k, 1)) if s0 == 1 else (OMEGA_ROW_MAJOR, s0)
+    if s0 == 1:
+        return OMEGA_COL_MAJOR, s1
+    if s1 == 1:
+        return OMEGA_ROW_MAJOR, s0
     raise ValueError(f"Omega must have one contiguous dimension (strides {Omega.stride()})")
 
 

@@ -113,6 +113,10 @@ def test_binding_omega_layout_from_strides(shg):
     assert shg.omega_layout(row) == (shg.OMEGA_ROW_MAJOR, 32)
     assert shg.omega_layout(torch.zeros(k, 1, dtype=torch.float16)) == (shg.OMEGA_COL_MAJOR, k)
     assert shg.omega_layout(torch.zeros(1, n, dtype=torch.float16)) == (shg.OMEGA_ROW_MAJOR, n)
+    # a single row / column whose one element per column / row is strided: the stride is the ldo
+    # (round-2 fuzz case: the k = 1 column-major view of gen_omega has strides (1, 8))
+    assert shg.omega_layout(torch.zeros(n, 8, dtype=torch.float16)[:, :1].t()) == (shg.OMEGA_COL_MAJOR, 8)
+    assert shg.omega_layout(torch.zeros(k, 16, dtype=torch.float16)[:, :1]) == (shg.OMEGA_ROW_MAJOR, 16)
     with pytest.raises(ValueError):
         shg.omega_layout(torch.zeros(k, 2 * n, dtype=torch.float16)[:, ::2])
 

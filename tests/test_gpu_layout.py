@@ -147,3 +147,19 @@ def test_shgemm_host_threads(shg):
     assert not err, err
     for t in range(4):
         assert torch.equal(outs[t], ref), t
+
+
+@pytest.mark.parametrize("k,n", [(1, 64), (1, 1), (40, 1), (1, 300), (7, 1)])
+@pytest.mark.parametrize("layout", ["row", "col"])
+def test_degenerate_omega_shapes(shg, orc, k, n, layout):
+    """k = 1 or n = 1 in both layouts: the binding passes the real stride as ldo (a (1, n)
+    column-major view has strides (1, ldo)); found by the round-2 fuzz."""
+    g = torch.Generator(device="cuda").manual_seed(k * 1000 + n)
+    A = torch.randn(300, k, device="cuda", generator=g)
+    Om = shg.gen_omega(k, n, seed=3, layout=layout)
+    Y = shg.shgemm(A, Om)
+    Yt = shg.shgemm_at(A.t().contiguous(), Om)
+    torch.cuda.synchronize()
+    ref = to_np(A).astype(np.float64) @ orc.f16_bits_as_float(omega_bits(Om)).astype(np.float64)
+    np.testing.assert_allclose(to_np(Y), ref, rtol=1e-6, atol=1e-6)
+    np.testing.assert_allclose(to_np(Yt), ref, rtol=1e-6, atol=1e-6)
