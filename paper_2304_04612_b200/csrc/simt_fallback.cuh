@@ -1,7 +1,8 @@
 // simt_fallback.cuh — correctness-only SHGEMM on CUDA cores, used when the tensor-core path's
 // TMA alignment preconditions fail (base pointers not 16-B aligned, lda % 4 != 0, ldo % 8 != 0).
 // Same numerics contract as the mainloop: Eqs 14-16 with the hi+lo partial
-// of every 64-k chunk folded with RN into an FP32 accumulator (RZ avoidance).
+// of every 64-k chunk (summed in FP64, one rounding to FP32) folded with RN into an FP32 accumulator
+// (RZ avoidance).
 #pragma once
 #include <cstdint>
 #include <cuda_fp16.h>
@@ -24,7 +25,11 @@ __global__ void shgemm_simt_kernel(int64_t m, int64_t n, int64_t k, const float*
         float acc = 0.0f;
         for (int64_t k0 = 0; k0 < k; k0 += 64) {
             const int64_t k1 = k0 + 64 < k ? k0 + 64 : k;
-            float s_hi = 0.0f, s_lo = 0.0f;
+            // the chunk's hi and lo sums in FP64: every product of two FP16 (or TF32) values is exact
+            // there and 64 of them sum with a relative error below 2^-47, so the chunk costs ONE
+            // rounding to FP32 (like the tensor cores' fused K-step, not k-1 sequential FP32 roundings,
+            // which exceed the c5 elementwise bar at small k: round-2 edge fuzz, DESIGN R26)
+            double s_hi = 0.0, s_lo = 0.0;
             for (int64_t l = k0; l < k1; ++l) {
                 float hf, lf;
                 if (tf32) {   // SHGEMM-TF32 split
@@ -38,11 +43,11 @@ __global__ void shgemm_simt_kernel(int64_t m, int64_t n, int64_t k, const float*
                     hf = __half2float(__ushort_as_half(static_cast<uint16_t>(h & 0xFFFFu)));
                     lf = __half2float(__ushort_as_half(static_cast<uint16_t>(lo & 0xFFFFu)));
                 }
-                const float wf = __half2float(__ushort_as_half(w[l * so_k]));
-                s_hi = __fmaf_rn(hf, wf, s_hi);
-                s_lo = __fmaf_rn(lf, wf, s_lo);
+                const double wf = static_cast<double>(__half2float(__ushort_as_half(w[l * so_k])));
+                s_hi = __fma_rn(static_cast<double>(hf), wf, s_hi);
+                s_lo = __fma_rn(static_cast<double>(lf), wf, s_lo);
             }
-            acc = __fadd_rn(acc, __fmaf_rn(s_lo, 4.8828125e-4f, s_hi));
+            acc = __fadd_rn(acc, __double2float_rn(__fma_rn(s_lo, 4.8828125e-4, s_hi)));
         }
         Y[i * ldc + j] = acc;
         if (nonfinite && !isfinite(acc)) atomicOr(nonfinite, 1);

@@ -58,19 +58,21 @@ __global__ void tcec_simt_kernel(int64_t m, int64_t n, int64_t k, const float* _
         float acc = 0.0f;
         for (int64_t k0 = 0; k0 < k; k0 += 64) {
             const int64_t k1 = k0 + 64 < k ? k0 + 64 : k;
-            float s_hh = 0.0f, s_c = 0.0f;
+            // chunk sums in FP64 (exact FP16 x FP16 products, one rounding per chunk), as in
+            // shgemm_simt_kernel (DESIGN R26)
+            double s_hh = 0.0, s_c = 0.0;
             for (int64_t l = k0; l < k1; ++l) {
                 uint32_t h, lo;
                 split2(a[l * sa_col], 0.0f, h, lo);
-                const float ah = __half2float(__ushort_as_half(static_cast<uint16_t>(h & 0xFFFFu)));
-                const float al = __half2float(__ushort_as_half(static_cast<uint16_t>(lo & 0xFFFFu)));
-                const float bhf = __half2float(__ushort_as_half(bh[l]));
-                const float blf = __half2float(__ushort_as_half(bl[l]));
-                s_hh = __fmaf_rn(ah, bhf, s_hh);
-                s_c = __fmaf_rn(al, bhf, s_c);
-                s_c = __fmaf_rn(ah, blf, s_c);
+                const double ah = __half2float(__ushort_as_half(static_cast<uint16_t>(h & 0xFFFFu)));
+                const double al = __half2float(__ushort_as_half(static_cast<uint16_t>(lo & 0xFFFFu)));
+                const double bhf = __half2float(__ushort_as_half(bh[l]));
+                const double blf = __half2float(__ushort_as_half(bl[l]));
+                s_hh = __fma_rn(ah, bhf, s_hh);
+                s_c = __fma_rn(al, bhf, s_c);
+                s_c = __fma_rn(ah, blf, s_c);
             }
-            acc = __fadd_rn(acc, __fmaf_rn(s_c, 4.8828125e-4f, s_hh));
+            acc = __fadd_rn(acc, __double2float_rn(__fma_rn(s_c, 4.8828125e-4, s_hh)));
         }
         C[i * ldc + j] = acc;
     }

@@ -31,7 +31,11 @@ def check_bars(orc, A, om_bits, Y, rows=None, ratio=2.0, abs_bar=1e-5, slack=1.2
     err = np.abs(Y.astype(np.float64) - y64)
     worst = float(np.max(err / np.maximum(bound, 1e-300)))
     assert e_gpu <= abs_bar, (e_gpu, e_32)
-    if ratio != float("inf"):
-        assert e_gpu <= ratio * e_32, (e_gpu, e_32)
     assert worst <= 1.0, worst
+    # the ratio bar compares two Frobenius errors, i.e. two sums of independent roundings: with fewer
+    # than 64 outputs it is a high-variance statistic (a single naive FP32 dot product can round to
+    # its exact value by chance), so it applies from 64 outputs on (DESIGN R26); the elementwise bar
+    # above always applies
+    if ratio != float("inf") and Y.size >= 64:
+        assert e_gpu <= ratio * e_32, (e_gpu, e_32)
     return e_gpu, e_32, worst
