@@ -64,7 +64,10 @@ def run(i):
         # per-chunk device products on the same rows: bitwise equal
         rows = shg.lib().shg_host_workspace_size(n, k, chunk, shg.OMEGA_ROW_MAJOR if layout == "row" else shg.OMEGA_COL_MAJOR)
         assert rows > 0
-        Ad = A.cuda()
+        # the device reference reads A with the same row pitch shgemm_host stages it at (k rounded
+        # up to 4: the pitch decides between the tensor-core path and the CUDA-core fallback)
+        Ad = padded(m, k, (k + 3) // 4 * 4 - k, torch.float32, "cuda")
+        Ad.copy_(A)
         ch = chunk if chunk > 0 else None
         if ch is None:
             ref = shg.shgemm(Ad, Om)
