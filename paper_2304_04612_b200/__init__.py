@@ -227,6 +227,14 @@ def gen_omega_tiled(k: int, n: int, seed: int = 0, dist="gaussian", stream_id: i
     return buf
 
 
+def _ld(t: torch.Tensor, rows: int, cols: int) -> int:
+    """Leading dimension of a row-major (rows, cols) tensor for the C ABI: its row stride, also for a
+    single row when that stride is a valid pitch (a 1-row slice of a padded matrix keeps its 16-B
+    aligned pitch and with it the tensor-core path), else max(cols, 1)."""
+    s0 = t.stride(0)
+    return s0 if (rows > 1 or s0 >= max(cols, 1)) else max(cols, 1)
+
+
 def _check_out(out, m, n, device):
     """A caller's Y: (m, n) float32 with unit column stride (every wrapper writes m rows of n)."""
     if out is None:
@@ -246,8 +254,8 @@ def shgemm_tiled(A: torch.Tensor, Omega_tiled: torch.Tensor, n: int, out=None, t
         raise ValueError("Omega_tiled must be float16 with ceil(k/64) * n * 64 elements")
     out = _check_out(out, m, n, A.device)
     ws_bytes = 0 if workspace is None else workspace.numel() * workspace.element_size()
-    _check(lib().shgemm_tiled(m, n, k, _p(A), A.stride(0) if m > 1 else max(k, 1), _p(Omega_tiled), _p(out),
-                              out.stride(0) if m > 1 else max(n, 1), _tune(tune), _p(workspace), ws_bytes, None,
+    _check(lib().shgemm_tiled(m, n, k, _p(A), _ld(A, m, k), _p(Omega_tiled), _p(out),
+                              _ld(out, m, n), _tune(tune), _p(workspace), ws_bytes, None,
                               _stream(stream)), "shgemm_tiled")
     return out
 
@@ -295,8 +303,8 @@ def shgemm(A: torch.Tensor, Omega: torch.Tensor, out: torch.Tensor | None = None
         raise ValueError("A must be row-major (stride(1) == 1)")
     lay, ldo = omega_layout(Omega)
     out = _check_out(out, m, n, A.device)
-    lda = A.stride(0) if m > 1 else max(k, 1)
-    ldc = out.stride(0) if m > 1 else max(n, 1)
+    lda = _ld(A, m, k)
+    ldc = _ld(out, m, n)
     ws_bytes = 0 if workspace is None else workspace.numel() * workspace.element_size()
     _check(lib().shgemm_ex(m, n, k, _p(A), lda, _p(Omega), ldo, _p(out), ldc, _tune(tune, tc, lay), _p(workspace),
                            ws_bytes, _p(nonfinite), _stream(stream)), "shgemm_ex")
@@ -315,8 +323,8 @@ def shgemm_at(At: torch.Tensor, Omega: torch.Tensor, out: torch.Tensor | None = 
     lay, ldo = omega_layout(Omega)
     out = _check_out(out, m, n, At.device)
     ws_bytes = 0 if workspace is None else workspace.numel() * workspace.element_size()
-    _check(lib().shgemm_at(m, n, k, _p(At), At.stride(0) if k > 1 else max(m, 1), _p(Omega), ldo, _p(out),
-                           out.stride(0) if m > 1 else max(n, 1), _tune(tune, tc, lay), _p(workspace), ws_bytes,
+    _check(lib().shgemm_at(m, n, k, _p(At), _ld(At, k, m), _p(Omega), ldo, _p(out),
+                           _ld(out, m, n), _tune(tune, tc, lay), _p(workspace), ws_bytes,
                            _p(nonfinite), _stream(stream)), "shgemm_at")
     return out
 
@@ -341,8 +349,8 @@ def shgemm_host(A_host: torch.Tensor, Omega: torch.Tensor, Y_host: torch.Tensor 
           or (m and n > 1 and Y_host.stride(1) != 1)):
         raise ValueError("Y_host must be an (m, n) float32 row-major host tensor")
     ws_bytes = 0 if workspace is None else workspace.numel() * workspace.element_size()
-    _check(lib().shgemm_host(m, n, k, _h(A_host), A_host.stride(0) if m > 1 else max(k, 1), _p(Omega), ldo, lay,
-                             _h(Y_host), Y_host.stride(0) if m > 1 else max(n, 1), chunk_rows, _p(workspace),
+    _check(lib().shgemm_host(m, n, k, _h(A_host), _ld(A_host, m, k), _p(Omega), ldo, lay,
+                             _h(Y_host), _ld(Y_host, m, n), chunk_rows, _p(workspace),
                              ws_bytes, _stream(stream)), "shgemm_host")
     return Y_host
 
@@ -395,7 +403,7 @@ def tcec_sgemm(A: torch.Tensor, B: torch.Tensor, out: torch.Tensor | None = None
         out = torch.empty((m, n), dtype=torch.float32, device=A.device)
     elif out.dtype != torch.float32 or tuple(out.shape) != (m, n) or (m and n and out.stride(1) != 1):
         raise ValueError("out must be (m, n) float32 row-major")
-    ldc = out.stride(0) if m > 1 else max(n, 1)
+    ldc = _ld(out, m, n)
     ws_bytes = 0 if workspace is None else workspace.numel() * workspace.element_size()
     _check(lib().tcec_sgemm_ex(m, n, k, _p(A), lda, a_layout, _p(B), ldb, b_layout, _p(out), ldc, _tune(tune),
                                _p(workspace), ws_bytes, _stream(stream)), "tcec_sgemm_ex")
@@ -434,11 +442,11 @@ def project(T: torch.Tensor, mode: int, n: int, seed: int = 0, dist="gaussian", 
     ws_bytes = 0 if workspace is None else workspace.numel() * workspace.element_size()
     if omega is not None:
         _check(lib().project_omega(_p(T), len(dims), d, mode, n, _p(omega), _p(out),
-                                   out.stride(0) if M > 1 else max(n, 1), _p(workspace),
+                                   _ld(out, M, n), _p(workspace),
                                    ws_bytes, _stream(stream)), "project_omega")
         return out
     _check(lib().project_shard(_p(T), len(dims), d, mode, n, seed, _dist(dist), _tc(tc), omega_row0, k_total,
-                               _p(out), out.stride(0) if M > 1 else max(n, 1), _p(workspace), ws_bytes,
+                               _p(out), _ld(out, M, n), _p(workspace), ws_bytes,
                                _stream(stream)), "project_shard")
     return out
 
@@ -469,7 +477,7 @@ def synth(kind: str, seed: int, stream_id: int, m: int, k: int, row0: int = 0, o
     if out is None:
         out = torch.empty((m, k), dtype=torch.float32, device=device or "cuda")
     _check(lib().shg_synth_f32(0 if kind == "gauss" else 1, seed, stream_id, m, k, row0, _p(out),
-                               out.stride(0) if m > 1 else max(k, 1), _stream(stream)), "shg_synth_f32")
+                               _ld(out, m, k), _stream(stream)), "shg_synth_f32")
     return out
 
 
