@@ -120,6 +120,14 @@ typedef struct {
                              one N tile, no split_k > 1 and >= 4 k-blocks per unit: otherwise
                              SHG_ERR_INVALID_VALUE. Row shards of one Y are bitwise equal to the
                              unsharded Y only under whole tiles (stream-K's sums depend on the grid). */
+    int32_t a_mcast;      /* A multicast: 0 auto, 1 off, 2 or 4 = CTA pairs per cluster that take one m-block
+                             and that many N tiles together, each A stage fetched once per cluster and
+                             multicast by TMA to the CTAs holding its rows (A read once for n_tiles ==
+                             a_mcast; PAPER.md:652 counts the A100 design's mnk/b_n loads of A). Needs
+                             SHGEMM-FP16 CTA pairs, K-major A (shgemm / project, not shgemm_at), BN in
+                             {128, 192, 256}, n_tiles % a_mcast == 0, no split-K and no stream-K:
+                             otherwise SHG_ERR_INVALID_VALUE. Bitwise-identical Y (the arithmetic is
+                             unchanged). */
 } shg_tune_t;
 
 /* Plan the library would use for an (m, n, k) shgemm on the current device. */
@@ -132,6 +140,7 @@ typedef struct {
     int32_t omega_mcast; /* always 1 (no Omega multicast) */
     int32_t stream_k;    /* 1 if the plan uses the stream-K schedule (shg_tune_t.stream_k) */
     int64_t workspace_bytes;
+    int32_t a_mcast;     /* CTA pairs per cluster sharing each A stage (shg_tune_t.a_mcast); 1 = none */
 } shg_plan_t;
 
 /* ---------------------------------------------------------------------------------------------
@@ -346,6 +355,12 @@ shg_status_t shg_probe_tma_read(const float *A, int64_t m, int64_t k, int64_t ld
  * publish per-tile flags that the Omega stager acquires. Same bits as gen_omega_f16_tiled. Off by
  * default (measured slower on B200); process-wide; SHG_OMGEN=1 sets the default. */
 void shg_set_inkernel_omega(int on);
+
+/* Process-wide default of shg_tune_t.a_mcast for calls whose tune leaves it 0 (and for project(),
+ * tcec paths excluded): 0 = the automatic rule (2 pairs per cluster when the N tiles pair up,
+ * DESIGN.md §5), 1 = off, 2 or 4 = that many pairs per cluster where the plan is eligible (silently
+ * off where not). Returns the previous value, or -1 (unchanged) for any other npa. */
+int shg_set_a_mcast(int npa);
 
 /* Number of kernels this library has launched in this process (monotonic). */
 uint64_t shg_launch_count(void);

@@ -39,7 +39,8 @@ class Tune(ctypes.Structure):
     _fields_ = [("bn", ctypes.c_int32), ("split_k", ctypes.c_int32), ("max_ctas", ctypes.c_int32),
                 ("force_simt", ctypes.c_int32), ("debug_flags", ctypes.c_int32), ("pair", ctypes.c_int32),
                 ("a_box", ctypes.c_int32), ("tc", ctypes.c_int32), ("omega_mcast", ctypes.c_int32),
-                ("prof", ctypes.c_void_p), ("omega_layout", ctypes.c_int32), ("stream_k", ctypes.c_int32)]
+                ("prof", ctypes.c_void_p), ("omega_layout", ctypes.c_int32), ("stream_k", ctypes.c_int32),
+                ("a_mcast", ctypes.c_int32)]
 
 
 class Plan(ctypes.Structure):
@@ -47,7 +48,8 @@ class Plan(ctypes.Structure):
                 ("m_tiles", ctypes.c_int32), ("split_k", ctypes.c_int32), ("grid", ctypes.c_int32),
                 ("stages_a", ctypes.c_int32), ("stages_b", ctypes.c_int32), ("smem_bytes", ctypes.c_int32),
                 ("kernels", ctypes.c_int32), ("cta_pair", ctypes.c_int32), ("tc", ctypes.c_int32),
-                ("omega_mcast", ctypes.c_int32), ("stream_k", ctypes.c_int32), ("workspace_bytes", ctypes.c_int64)]
+                ("omega_mcast", ctypes.c_int32), ("stream_k", ctypes.c_int32), ("workspace_bytes", ctypes.c_int64),
+                ("a_mcast", ctypes.c_int32)]
 
 
 def lib():
@@ -96,6 +98,8 @@ def lib():
             L.shg_probe_boxmuller.argtypes = [vp, i64, vp, vp, vp, vp]
             L.shg_set_inkernel_omega.argtypes = [i32]
             L.shg_set_inkernel_omega.restype = None
+            L.shg_set_a_mcast.argtypes = [i32]
+            L.shg_set_a_mcast.restype = i32
             L.shg_last_error.restype = ctypes.c_char_p
             L.shg_device_supported.restype = i32
             L.shg_version.restype = ctypes.c_char_p
@@ -149,6 +153,15 @@ def _dist(d) -> int:
 def set_inkernel_omega(on: bool) -> None:
     """project(): generate Omega inside the projection kernel (C ABI shg_set_inkernel_omega)."""
     lib().shg_set_inkernel_omega(1 if on else 0)
+
+
+def set_a_mcast(npa: int) -> int:
+    """Process-wide default A multicast (C ABI shg_set_a_mcast): 0 auto, 1 off, 2 / 4 pairs per
+    cluster where eligible. Returns the previous value."""
+    prev = lib().shg_set_a_mcast(int(npa))
+    if prev < 0:
+        raise ValueError("npa must be 0, 1, 2 or 4")
+    return prev
 
 
 def launch_count() -> int:

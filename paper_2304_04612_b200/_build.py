@@ -9,7 +9,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libshgemm.so")
 SOURCES = ["api.cu", "probes.cu", "tc_f16.cu", "tc_f16_mm.cu", "tc_tf32.cu", "tc_tcec.cu",
-           "tc_f16_gen.cu"]
+           "tc_f16_gen.cu", "tc_f16_amc.cu"]
 HEADERS = ["ptx.cuh", "omega.cuh", "split.cuh", "shgemm_sm100.cuh", "simt_fallback.cuh", "probe_tma.cuh", "tcec.cuh",
            "internal.cuh"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")

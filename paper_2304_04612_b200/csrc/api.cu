@@ -210,6 +210,7 @@ struct Plan {
     bool tf32 = false;        // SHGEMM-TF32 (tune->tc == SHG_TC_TF32)
     bool tcec = false;        // TCEC-SGEMM (FP32 B split into B_low / dB_low)
     bool sk = false;          // stream-K schedule (KParams::sk): equal k-ranges per SM (pair), in-kernel fix-up
+    int npa = 1;              // CTA pairs per cluster sharing each A stage by TMA multicast (NPA > 1)
     int64_t sk_planes = 0;    // stream-K: bytes of the partial planes (the counters follow, 256-B aligned)
     // workspace = [split-K planes, 256-B aligned][TF32 copy of Omega | TCEC split of B]
     int64_t ws_bytes = 0, ld_ws = 0, sk_bytes = 0, om_bytes = 0, ldo32 = 0;
@@ -240,11 +241,25 @@ constexpr bool kSkAuto = true;
 constexpr int kSkAutoMaxBn = 160;
 constexpr double kSkMinWaveEff = 0.92;   // ... and whole tiles would leave the last wave < 92% busy
 
+// A multicast chosen automatically (tune->a_mcast == 0): 2 pairs per cluster whenever the N tiles
+// pair up. Measured in steady state under the 1000 W cap (blocks of >= 1.5 s back-to-back calls per
+// variant, interleaved, profiles/r02_ab_amc_steady.jsonl): m = k = 32768 n = 512 2.12 -> 1.97 ms,
+// n = 1024 3.91 -> 3.82; m = 2^21, k = 4096, n = 512 18.5 -> 17.0, n = 1024 36.4 -> 33.6 (4 pairs
+// per cluster: 33.0, and 3.91 at 32768^2): A is read once per cluster instead of once per N tile,
+// and the SM clock under the cap rises from 0.95-1.05 to 1.16-1.27 GHz, more than paying for the
+// 132 of 148 SMs that clusters of 4 CTAs occupy. shg_set_a_mcast() overrides the default per process.
+std::atomic<int> g_amc_default{0};      // 0 auto, 1 off, 2 / 4 (where eligible)
+inline int auto_amcast(int n_tiles) {
+    const int g = g_amc_default.load(std::memory_order_relaxed);
+    if (g == 1 || g == 2 || g == 4) return g;
+    return (n_tiles >= 2 && n_tiles % 2 == 0) ? 2 : 1;
+}
+
 
 // om_rm: Omega is row-major; the FP16 tensor-core path then reads a column-major copy
 // made in the workspace by transpose_omega_kernel (TF32 widens either layout directly)
 Plan make_plan(int64_t m, int64_t n, int64_t k, bool fast_ok, const shg_tune_t* tune, int sms, bool tcec = false,
-               bool om_rm = false, bool allow_sk = true) {
+               bool om_rm = false, bool allow_sk = true, bool a_kmajor = true) {
     Plan pl;
     pl.tf32 = !tcec && tune && tune->tc == SHG_TC_TF32;
     pl.tcec = tcec;
@@ -308,9 +323,10 @@ Plan make_plan(int64_t m, int64_t n, int64_t k, bool fast_ok, const shg_tune_t* 
                                           wave_eff < kSkMinWaveEff && 2 * mn_tiles >= slots && pl.num_kb >= 16));
     if (sk_mode == 1 && !sk_fits) { pl.path = -1; return pl; }
     int splits = 1;
+    const bool amc_req = tune && tune->a_mcast >= 2;   // an explicit A multicast request keeps whole tiles
     if (tune && tune->split_k > 0) {
         splits = tune->split_k;
-    } else if (!pl.sk && mn_tiles < slots && pl.num_kb >= 16) {
+    } else if (!pl.sk && !amc_req && mn_tiles < slots && pl.num_kb >= 16) {
         // fill the SMs with k-splits, keeping >= 4 k-blocks (256 k) per split; not for k < 1024,
         // where the partial planes and the extra reduce launch cost more than the idle SMs
         // (cfg1, 512 x 512 x 32: split 1/2/4/8 all within 2 us, profiles/r01_small_split.jsonl)
@@ -322,6 +338,27 @@ Plan make_plan(int64_t m, int64_t n, int64_t k, bool fast_ok, const shg_tune_t* 
     const int64_t tiles = mn_tiles * splits;
     pl.grid = pl.sk ? slots * cl : static_cast<int>(std::min<int64_t>(tiles * cl, cap));
     pl.grid = std::max(cl, pl.grid / cl * cl);
+    // A multicast (tune->a_mcast; shgemm_sm100_kernel<..., NPA>): clusters of NPA pairs share each A
+    // stage across NPA N tiles of one m-block. Decided after splits / stream-K, which it does not
+    // change (it needs neither), so the workspace is the same with or without it.
+    const int amc = tune ? tune->a_mcast : 0;      // 0 auto, 1 off, 2 / 4 pairs per cluster
+    if (amc < 0 || amc == 3 || amc > 4) { pl.path = -1; return pl; }
+    const int npa_want = amc >= 2 ? amc : (amc == 1 ? 1 : auto_amcast(pl.n_tiles));
+    if (npa_want > 1) {
+        const bool amc_ok = pl.pair && !pl.tf32 && !tcec && a_kmajor && !pl.sk && splits == 1 &&
+                            !wide_bn(pl.bn) && (pl.bn == 128 || pl.bn == 192 || pl.bn == 256) &&
+                            pl.n_tiles % npa_want == 0 && pl.n_tiles >= npa_want;
+        if (amc_ok) {
+            pl.npa = npa_want;
+            const int cln = 2 * pl.npa;
+            const int64_t groups = static_cast<int64_t>(pl.m_tiles) * (pl.n_tiles / pl.npa);
+            const int capn = std::max(cln, cap / cln * cln);
+            pl.grid = static_cast<int>(std::min<int64_t>(groups * cln, capn));
+        } else if (amc >= 2) {
+            pl.path = -1;
+            return pl;
+        }
+    }
     if (splits > 1) {
         pl.ld_ws = (n + 3) / 4 * 4;
         pl.sk_bytes = static_cast<int64_t>(splits) * m * pl.ld_ws * 4;
@@ -407,7 +444,7 @@ shg_status_t run_shgemm(int64_t m, int64_t n, int64_t k, const AView& av, const 
     const bool fast_ok = aligned16(av.A) && om_ok && (av.row_stride % 4 == 0) && (av.slab % 4 == 0) &&
                          (plain || av.S % 32 == 0) && encode_fn() != nullptr &&
                          k < (int64_t(1) << 31) && av.S < (int64_t(1) << 31) && m < (int64_t(1) << 31);
-    Plan pl = make_plan(m, n, k, fast_ok, tune, d.sms, tcec, om_rm, og == nullptr);
+    Plan pl = make_plan(m, n, k, fast_ok, tune, d.sms, tcec, om_rm, og == nullptr, !av.mmajor);
     if (pl.path < 0) return SHG_ERR_INVALID_VALUE;
     if (pl.path == 1 && tcec) {
         if (!plain) return SHG_ERR_INVALID_VALUE;
@@ -570,6 +607,7 @@ shg_status_t run_shgemm(int64_t m, int64_t n, int64_t k, const AView& av, const 
     shg_status_t st = gen ? dispatch_tc_f16_gen(pl.bn, av.mmajor, mapA, mapB0, mapB1, kp, pl.grid, stream)
                       : tcec      ? dispatch_tc_tcec(pl.bn, av.mmajor, pl.pair, mapA, mapB0, mapB1, kp, pl.grid, stream)
                       : pl.tf32 ? dispatch_tc_tf32(pl.bn, av.mmajor, pl.pair, mapA, mapB0, mapB1, kp, pl.grid, stream)
+                      : pl.npa > 1 ? dispatch_tc_f16_amc(pl.bn, pl.npa, mapA, mapB0, mapB1, kp, pl.grid, stream)
                                 : dispatch_tc_f16(pl.bn, av.mmajor, pl.pair, mapA, mapB0, mapB1, kp, pl.grid, stream);
     if (st != SHG_OK) return finish(st);
     if (pl.splits > 1) {
@@ -825,6 +863,7 @@ shg_status_t tcec_plan(int64_t m, int64_t n, int64_t k, const shg_tune_t* tune, 
         out->cta_pair = pl.pair ? 1 : 0;
         out->stream_k = pl.sk ? 1 : 0;
         out->omega_mcast = 1;
+        out->a_mcast = 1;
         out->kernels = 2 + (pl.splits > 1 ? 1 : 0);
     }
     out->workspace_bytes = pl.ws_bytes;
@@ -855,6 +894,7 @@ shg_status_t shg_plan(int64_t m, int64_t n, int64_t k, const shg_tune_t* tune, s
         out->tc = pl.tf32 ? SHG_TC_TF32 : SHG_TC_FP16;
         out->omega_mcast = 1;
         out->stream_k = pl.sk ? 1 : 0;
+        out->a_mcast = pl.npa;
         out->kernels = 1 + (pl.splits > 1 ? 1 : 0) + (pl.tf32 || pl.ldt > 0 ? 1 : 0);
     } else {
         out->kernels = pl.path == 1 ? 1 : (k == 0 && m > 0 && n > 0 ? 0 : 0);
@@ -1213,6 +1253,11 @@ int shg_device_supported(void) {
 }
 
 void shg_set_inkernel_omega(int on) { g_omgen.store(on ? 1 : 0, std::memory_order_relaxed); }
+
+int shg_set_a_mcast(int npa) {
+    if (npa != 0 && npa != 1 && npa != 2 && npa != 4) return -1;
+    return g_amc_default.exchange(npa, std::memory_order_relaxed);
+}
 
 const char* shg_version(void) { return "shgemm-b200 0.2.0 sm_100a"; }
 

@@ -50,11 +50,11 @@ inline bool valid_bn(int bn) {
     return false;
 }
 
-template <int BN, bool MMAJOR, bool PAIR, bool TF32, bool TCEC = false, bool OMGEN = false>
+template <int BN, bool MMAJOR, bool PAIR, bool TF32, bool TCEC = false, bool OMGEN = false, int NPA = 1>
 shg_status_t launch_tc(const CUtensorMap& mapA, const CUtensorMap& mapB0, const CUtensorMap& mapB1,
                        const shg::KParams& kp, int grid, cudaStream_t stream) {
     using CF = shg::Cfg<BN, PAIR, TF32, TCEC>;
-    auto kern = shg::shgemm_sm100_kernel<BN, MMAJOR, PAIR, TF32, TCEC, OMGEN>;
+    auto kern = shg::shgemm_sm100_kernel<BN, MMAJOR, PAIR, TF32, TCEC, OMGEN, NPA>;
     static std::once_flag flags[64];
     int dev = 0;
     cudaGetDevice(&dev);
@@ -77,14 +77,14 @@ shg_status_t launch_tc(const CUtensorMap& mapA, const CUtensorMap& mapB0, const 
     cfg.stream = stream;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = PAIR ? 2 : 1;
+    attr[0].val.clusterDim.x = PAIR ? 2 * NPA : 1;
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     // The grid is persistent: every cluster must be co-resident, or the clusters that do not fit
-    // run as a second wave. Clusters must sit in one GPC, so fewer than #SMs / 2 may fit (a GPC
-    // with an odd SM count): clamp to the occupancy query. (The kernel reads its unit count from
+    // run as a second wave. Clusters must sit in one GPC, so fewer than #SMs / (2 NPA) may fit (GPC
+    // sizes are not multiples of the cluster size): clamp to the occupancy query. (The kernel reads its unit count from
     // gridDim, so a stream-K schedule follows the clamped grid.)
     static int max_clusters[64];
     static std::once_flag occ_flags[64];
@@ -97,7 +97,7 @@ shg_status_t launch_tc(const CUtensorMap& mapA, const CUtensorMap& mapB0, const 
         }
         max_clusters[di] = nc;
     });
-    constexpr int kCl = PAIR ? 2 : 1;
+    constexpr int kCl = PAIR ? 2 * NPA : 1;
     if (max_clusters[di] > 0 && grid > max_clusters[di] * kCl) cfg.gridDim = dim3(max_clusters[di] * kCl);
     SHG_CUDA(cudaLaunchKernelEx(&cfg, kern, mapA, mapB0, mapB1, kp));
     g_launches.fetch_add(1, std::memory_order_relaxed);
@@ -147,4 +147,7 @@ shg_status_t dispatch_tc_tcec(int bn, bool mmajor, bool pair, const CUtensorMap&
 shg_status_t dispatch_tc_f16_gen(int bn, bool mmajor, const CUtensorMap& a, const CUtensorMap& b0,
                                  const CUtensorMap& b1, const shg::KParams& kp, int grid, cudaStream_t s);
 constexpr int kOmGenMaxBn = shg::kOmGenMaxBnKernel;
+// SHGEMM-FP16 K-major CTA pairs with A multicast across npa = 2 or 4 pairs of a cluster (tc_f16_amc.cu)
+shg_status_t dispatch_tc_f16_amc(int bn, int npa, const CUtensorMap& a, const CUtensorMap& b0, const CUtensorMap& b1,
+                                 const shg::KParams& kp, int grid, cudaStream_t s);
 }  // namespace shg_api

@@ -275,16 +275,21 @@ __device__ __forceinline__ SkRange sk_range(const KParams& p, int unit, int unit
     return r;
 }
 
+// NPA > 1 (A multicast, see the kernel): a unit is a cluster of NPA pairs that take one m-block and
+// NPA consecutive N tiles together (the planner guarantees n_tiles % NPA == 0); pair pr of the
+// cluster gets N tile ng * NPA + pr of the unit's N group ng.
+template <int NPA = 1>
 __device__ __forceinline__ bool next_piece(const KParams& p, int unit, int units, const SkRange& sr, int it,
-                                           Piece& w) {
+                                           Piece& w, int pr = 0) {
     if (!p.sk) {
         const int tile = unit + it * units;
-        if (tile >= p.m_tiles * p.splits * p.n_tiles) return false;
-        const int per_m = p.splits * p.n_tiles;
+        const int ngr = NPA == 1 ? p.n_tiles : p.n_tiles / NPA;
+        if (tile >= p.m_tiles * p.splits * ngr) return false;
+        const int per_m = p.splits * ngr;
         w.m_blk = tile / per_m;
         const int rem = tile - w.m_blk * per_m;
-        w.s = rem / p.n_tiles;
-        w.n_blk = rem - w.s * p.n_tiles;
+        w.s = rem / ngr;
+        w.n_blk = NPA == 1 ? rem - w.s * ngr : (rem - w.s * ngr) * NPA + pr;
         w.kb0 = static_cast<int>((static_cast<int64_t>(w.s) * p.num_kb) / p.splits);
         w.nkb = static_cast<int>((static_cast<int64_t>(w.s + 1) * p.num_kb) / p.splits) - w.kb0;
         w.tile = tile;
@@ -489,7 +494,16 @@ __device__ __forceinline__ void acquire_flag(const uint32_t* f) {
 // OMGEN         : cooperative in-kernel Omega (KParams::om_gen; single CTAs, SHGEMM-FP16, k-tiled Omega,
 //                 one tile per CTA): compiled only into the instantiations project() uses for it, so
 //                 the other kernels' epilogues carry no generator registers.
-template <int BN, bool MMAJOR, bool PAIR, bool TF32 = false, bool TCEC = false, bool OMGEN = false>
+// NPA > 1       : A multicast (SHGEMM-FP16 K-major CTA pairs, several N tiles): a cluster of NPA pairs
+//                 (2 * NPA CTAs) takes one m-block and NPA N tiles, one per pair. Each A stage is
+//                 fetched ONCE per cluster and row half: the even pair's CTA of that half (the issuer)
+//                 multicasts it into the same ring slot of the NPA CTAs holding those rows, which
+//                 split it locally. A peer's stager arms its own a_full for the bytes and then
+//                 arrives on the issuer's a_empty, so the issuer's a_empty phase of a slot's use u
+//                 completes only when every destination has consumed use u and armed use u + 1 (the
+//                 issuer waits for NPA - 1 such arrivals besides its own 8 splitter warps). A comes from L2/HBM once instead of NPA times
+//                 (the A100 design loads A mnk/b_n times).
+template <int BN, bool MMAJOR, bool PAIR, bool TF32 = false, bool TCEC = false, bool OMGEN = false, int NPA = 1>
 __global__ void __launch_bounds__(threads_for<OMGEN>(), 1)
 shgemm_sm100_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB0,
                     const __grid_constant__ CUtensorMap mapB1, const KParams p) {
@@ -522,17 +536,24 @@ shgemm_sm100_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_const
     const uint32_t warp = warp_id();
     const uint32_t lane = threadIdx.x & 31u;
     static_assert(!OMGEN || (!PAIR && !TF32 && !TCEC && BN <= kOmGenMaxBnKernel), "in-kernel Omega: single-CTA SHGEMM-FP16");
-    constexpr int CL = PAIR ? 2 : 1;                              // CTAs per cluster
-    const uint32_t crank = PAIR ? cluster_ctarank() : 0u;         // rank in the pair: 0 = leader (issues the MMAs)
-    const uint32_t lead = 0u;                                     // cluster rank of the pair's leader
-    const uint16_t pair_mask = 3u;
-    const int unit = static_cast<int>(blockIdx.x) / CL;           // this CTA's (pair's) work unit
+    static_assert(NPA == 1 || (PAIR && !MMAJOR && !TF32 && !TCEC && !OMGEN && !CF::WIDE), "A multicast: FP16 K-major pairs");
+    constexpr int CL = PAIR ? 2 * NPA : 1;                        // CTAs per cluster
+    const uint32_t crk = PAIR ? cluster_ctarank() : 0u;
+    const uint32_t crank = crk & 1u;                              // rank in the pair: 0 = leader (issues the MMAs)
+    const int pr = static_cast<int>(crk >> 1);                    // pair of the cluster (NPA > 1)
+    const uint32_t lead = 2u * static_cast<uint32_t>(pr);         // cluster rank of the pair's leader
+    const uint16_t pair_mask = static_cast<uint16_t>(3u << lead);
+    const int unit = static_cast<int>(blockIdx.x) / CL;           // this CTA's (pair's / cluster's) work unit
     const int units = static_cast<int>(gridDim.x) / CL;
     const SkRange sr = sk_range(p, unit, units);
     constexpr int kPair = PAIR ? 2 : 1;
+    const bool a_issuer = NPA == 1 || pr == 0;
 
     if (threadIdx.x == 0) {
-        for (int i = 0; i < SA; ++i) { mbar_init(&a_full[i], 1); mbar_init(&a_empty[i], kNumSplitWarps); }
+        for (int i = 0; i < SA; ++i) {
+            mbar_init(&a_full[i], 1);
+            mbar_init(&a_empty[i], kNumSplitWarps + ((NPA > 1 && a_issuer) ? NPA - 1 : 0));
+        }
         for (int i = 0; i < NCH; ++i) {
             mbar_init(&ch_ready[i], kPair * (kNumSplitWarps + 1));
             mbar_init(&ch_empty[i], 1);
@@ -576,7 +597,7 @@ shgemm_sm100_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_const
         const long long t_begin = clock64();
         const bool skip_math = (p.dbg & 2u) != 0;
         Piece wk;
-        for (int it = 0; next_piece(p, unit, units, sr, it, wk); ++it) {
+        for (int it = 0; next_piece<NPA>(p, unit, units, sr, it, wk, pr); ++it) {
             const int m_blk = wk.m_blk, n_blk = wk.n_blk, kb0 = 0, kb1 = wk.nkb;
             (void)m_blk;
             (void)n_blk;
@@ -715,7 +736,7 @@ shgemm_sm100_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_const
         const bool skip_ld = (p.dbg & 1u) != 0;
         const int etid = static_cast<int>(threadIdx.x) - kEpiWarp0 * 32;   // 0..255
         Piece wk;
-        for (int it = 0; next_piece(p, unit, units, sr, it, wk); ++it) {
+        for (int it = 0; next_piece<NPA>(p, unit, units, sr, it, wk, pr); ++it) {
             const int m_blk = wk.m_blk, n_blk = wk.n_blk, kb0 = 0, kb1 = wk.nkb;
             (void)m_blk;
             (void)n_blk;
@@ -881,7 +902,7 @@ shgemm_sm100_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_const
         asm volatile("setmaxnreg.dec.sync.aligned.u32 72;");
         const int gtid = static_cast<int>(threadIdx.x) - kWarpGen0 * 32;   // 0..255
         Piece wk;
-        for (int it = 0; next_piece(p, unit, units, sr, it, wk); ++it) {
+        for (int it = 0; next_piece<NPA>(p, unit, units, sr, it, wk, pr); ++it) {
             const int64_t kb0s = wk.kb0;
             for (int64_t t = kb0s + wk.m_blk; t < kb0s + wk.nkb; t += p.m_tiles) {
                 gen_omega_tile(p, t, gtid);
@@ -899,23 +920,52 @@ shgemm_sm100_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_const
                 // they run concurrently on neighbouring CTAs; evict_normal keeps a stage in L2
                 // until its last reader has fetched it, so A comes from HBM once instead of
                 // n_tiles times (PAPER.md:652 counts mnk/b_n loads of A on the A100 design).
-                const uint64_t pol = p.n_tiles > 1 ? policy_evict_normal() : policy_evict_first();
+                // (NPA > 1: one cluster covers NPA N tiles, so only n_tiles > NPA re-reads A.)
+                const uint64_t pol = p.n_tiles > NPA ? policy_evict_normal() : policy_evict_first();
+                // A multicast: the CTAs of this row half in every pair of the cluster
+                uint16_t a_mask = 0;
+#pragma unroll
+                for (int j = 0; j < NPA; ++j) a_mask |= static_cast<uint16_t>(1u << (crank + 2u * j));
                 uint32_t sa = 0, pa = 0;
+                uint32_t n_st = 0;     // stages staged so far (NPA > 1: the first SA are first uses)
                 long long w = 0;
                 Piece wk;
-                for (int it = 0; next_piece(p, unit, units, sr, it, wk); ++it) {
+                for (int it = 0; next_piece<NPA>(p, unit, units, sr, it, wk, pr); ++it) {
                     const int m_blk = wk.m_blk, n_blk = wk.n_blk, kb0 = 0, kb1 = wk.nkb;
                     (void)m_blk;
                     (void)n_blk;
                     const int m0 = m_blk * CF::kTileM + static_cast<int>(crank) * kBM;
-                    for (int kb = kb0; kb < kb1; ++kb) {
+                    for (int kb = kb0; kb < kb1; ++kb, ++n_st) {
                         mbar_wait_prof(&a_empty[sa], pa ^ 1u, w);
                         mbar_arrive_expect_tx(&a_full[sa], kA32StageBytes);
+                        if (NPA > 1 && !a_issuer) {
+                            // slot free (its previous use consumed) and armed: tell the issuer of this
+                            // row half, whose multicast fills it. The arrival completes the issuer's
+                            // a_empty phase of that PREVIOUS use, which is what the issuer waits on
+                            // before the next multicast into the slot; a slot's first use needs none
+                            // (the issuer does not wait then, and bytes landing before the arm count
+                            // in the same a_full phase). Relaxed: the arrive publishes no memory, and
+                            // the splitters' reads of the slot completed before their own arrivals.
+                            if (n_st >= static_cast<uint32_t>(SA)) mbar_arrive_cluster(&a_empty[sa], crank);
+                            advance(sa, pa, SA);
+                            continue;
+                        }
                         const int64_t kk = (p.dbg & 32u) ? 0 : static_cast<int64_t>((wk.kb0 + (kb))) * kBK;
                         const int c0 = static_cast<int>(kk % p.k_inner);
                         const int c2 = static_cast<int>(kk / p.k_inner);
                         uint8_t* dst = a32 + sa * kA32StageBytes;
-                        if (MMAJOR) {
+                        if constexpr (NPA > 1) {
+                            if (p.a_rowpair) {
+                                tma_load_4d_mc(dst, &mapA, &a_full[sa], 0, c0 >> 5, m0, c2, a_mask, pol);
+                            } else {
+                                const int64_t kk2 = kk + 32;
+                                const bool wrap = kk2 < p.k && (c0 + 32) >= p.k_inner;
+                                tma_load_3d_mc(dst, &mapA, &a_full[sa], c0, m0, c2, a_mask, pol);
+                                tma_load_3d_mc(dst + kA32StageBytes / 2, &mapA, &a_full[sa],
+                                               wrap ? static_cast<int>(kk2 % p.k_inner) : c0 + 32, m0,
+                                               wrap ? static_cast<int>(kk2 / p.k_inner) : c2, a_mask, pol);
+                            }
+                        } else if (MMAJOR) {
                             // 2-D map {M (inner), K}, no swizzle: one box of 128 rows x 64 k, each
                             // k-line 512 contiguous bytes (4 KB-4 MB apart in HBM: one visit per line)
                             tma_load_2d(dst, &mapA, &a_full[sa], m0, static_cast<int>(kk), pol);
@@ -949,7 +999,7 @@ shgemm_sm100_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_const
                 uint32_t cs = 0, pc = 0;
                 long long w = 0;
                 Piece wk;
-                for (int it = 0; next_piece(p, unit, units, sr, it, wk); ++it) {
+                for (int it = 0; next_piece<NPA>(p, unit, units, sr, it, wk, pr); ++it) {
                     const int m_blk = wk.m_blk, n_blk = wk.n_blk, kb0 = 0, kb1 = wk.nkb;
                     (void)m_blk;
                     (void)n_blk;
@@ -1005,7 +1055,7 @@ shgemm_sm100_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_const
             // wide tiles: per-slot use counts (part 0 every stage, part 1 every second stage)
             uint32_t u0 = 0, u1 = 0;
             Piece wk;
-            for (int it = 0; next_piece(p, unit, units, sr, it, wk); ++it) {
+            for (int it = 0; next_piece<NPA>(p, unit, units, sr, it, wk, pr); ++it) {
                 const int m_blk = wk.m_blk, n_blk = wk.n_blk, kb0 = 0, kb1 = wk.nkb;
                 (void)m_blk;
                 (void)n_blk;
