@@ -783,7 +783,12 @@ def measure_extras(shg, torch, hbm, tc16_burst, tc_ratio, reps=10):
         Y = torch.empty((m, n), device="cuda")
         fn = lambda: (shg.gen_omega(k, n, seed=OMEGA_SEED, out=Om), shg.shgemm(A, Om, out=Y))
         ms = med_ms(fn)
-        out[name] = dict(roof(m, k, n, ms, iso_ms(fn)), m=m, k=k, n=n, step="gen_omega_f16 + shgemm")
+        out[name] = dict(roof(m, k, n, ms, iso_ms(fn)), m=m, k=k, n=n, step="gen_omega_f16 + shgemm",
+                         a_mcast=shg.plan(m, n, k)["a_mcast"])
+        if out[name]["a_mcast"] > 1 and n <= 1024:
+            # the same step with A multicast off (per-pair A loads; DESIGN.md §5 "A read once")
+            fn_off = lambda: (shg.gen_omega(k, n, seed=OMEGA_SEED, out=Om), shg.shgemm(A, Om, out=Y, tune={"a_mcast": 1}))
+            out[name]["a_mcast_off"] = roof(m, k, n, med_ms(fn_off))
         del A, Om, Y
         torch.cuda.empty_cache()
     del A5

@@ -30,6 +30,8 @@ def case(i):
         tune["pair"] = int(r.integers(1, 3))
     if r.random() < 0.25:
         tune["stream_k"] = int(r.integers(1, 3))     # forced stream-K / whole tiles (0 = auto)
+    if r.random() < 0.2:
+        tune["a_mcast"] = int(r.choice([1, 2, 4]))   # A multicast forced off / 2 / 4 pairs (0 = auto)
     row_omega = r.random() < 0.3                      # SURVEY §8(b)'s row-major Omega
     dist = int(r.integers(0, 4)) if kind != "tcec" else 0
     scale = float(np.exp(r.uniform(-3, 3)))
@@ -68,6 +70,11 @@ def run(i):
         else:
             Y = shg.shgemm(Ad, Om, tune=tune or None, tc=kind)
         torch.cuda.synchronize()
+        if kind == "fp16" and not mmajor and shg.plan(m, n, k, tune or None)["a_mcast"] > 1:
+            # A multicast (auto or forced): bitwise equal to per-pair loads on the same whole tiles
+            Y0 = shg.shgemm(Ad, Om, tune=dict(tune, a_mcast=1, split_k=1))
+            torch.cuda.synchronize()
+            assert torch.equal(Y.view(torch.int32), Y0.view(torch.int32)), "a_mcast not bitwise"
     except shg.SHGError as err:
         assert "INVALID" in str(err) and tune, err
         return
