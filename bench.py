@@ -640,6 +640,7 @@ def measure_fused_step(shg, torch, A, n, steps, scrub):
     m, k = A.shape
     ws = torch.empty(shg.project_workspace_size([m, k], 0, n), dtype=torch.uint8, device="cuda")
     W = torch.empty((m, n), device="cuda")
+    prev = shg.get_inkernel_omega()
     shg.set_inkernel_omega(True)
     try:
         side = torch.cuda.Stream()
@@ -654,7 +655,7 @@ def measure_fused_step(shg, torch, A, n, steps, scrub):
             shg.project(A, 0, n, seed=OMEGA_SEED, workspace=ws, out=W)
         launches = shg.launch_count() - c0
     finally:
-        shg.set_inkernel_omega(False)
+        shg.set_inkernel_omega(prev)
     torch.cuda.synchronize()
     ts = []
     for i in range(steps):

@@ -349,12 +349,20 @@ shg_status_t shg_probe_tma_read(const float *A, int64_t m, int64_t k, int64_t ld
                                 shg_stream_t stream);
 
 /* project()/project_shard() with SHGEMM-FP16: generate Omega_(mode) INSIDE the projection kernel
- * (on != 0) instead of a separate gen_omega launch, when the plan has every tile resident at once
- * and single-CTA tiles of BN <= 192 ("fused in-producer Omega"): the m-tiles
- * that share a k range each generate 1/m_tiles of its k-tiled Omega with their epilogue warps and
- * publish per-tile flags that the Omega stager acquires. Same bits as gen_omega_f16_tiled. Off by
- * default (measured slower on B200); process-wide; SHG_OMGEN=1 sets the default. */
+ * (on = 1, the default since round 2) instead of a separate gen_omega launch, when the plan has
+ * one tile per CTA and single-CTA tiles of BN <= 128 ("fused in-producer
+ * Omega"): the m-tiles that share a k range each generate 1/m_tiles of its k-tiled Omega with
+ * dedicated generator warps and publish per-tile flags that the Omega stager acquires; a stager
+ * whose tile is not published within 200 us generates it itself (same bits), so the kernel never
+ * depends on another CTA being resident. Same bits as gen_omega_f16_tiled either way. on = 0: the
+ * separate generator; on = 2 (tests): the generator warps stay idle and every tile comes from the
+ * stagers' fallback. Process-wide; SHG_OMGEN=0 sets the default to the separate generator.
+ * shg_get_inkernel_omega returns the current setting. */
 void shg_set_inkernel_omega(int on);
+int shg_get_inkernel_omega(void);
+/* Test support: how many k-tiles of Omega the stagers' generate-on-timeout fallback has produced in
+ * this process so far (synchronous read of a device counter; UINT64_MAX on a CUDA error). */
+uint64_t shg_inkernel_omega_fallbacks(void);
 
 /* Process-wide default of shg_tune_t.a_mcast for calls whose tune leaves it 0 (and for project(),
  * tcec paths excluded): 0 = the automatic rule (2 pairs per cluster when the N tiles pair up,

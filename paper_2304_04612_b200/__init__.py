@@ -18,7 +18,7 @@ import threading
 import torch
 
 __all__ = ["shgemm", "shgemm_at", "shgemm_tiled", "shgemm_host", "tcec_sgemm", "tcec_plan", "tcec_workspace_size",
-           "gen_omega", "gen_omega_tiled", "project", "project_workspace_size", "set_inkernel_omega", "split",
+           "gen_omega", "gen_omega_tiled", "project", "project_workspace_size", "set_inkernel_omega", "get_inkernel_omega", "split",
            "split_tf32", "synth", "plan", "workspace_size", "launch_count", "device_supported", "version", "lib",
            "probe_umma", "SHGError", "DISTS"]
 
@@ -98,6 +98,10 @@ def lib():
             L.shg_probe_boxmuller.argtypes = [vp, i64, vp, vp, vp, vp]
             L.shg_set_inkernel_omega.argtypes = [i32]
             L.shg_set_inkernel_omega.restype = None
+            L.shg_get_inkernel_omega.argtypes = []
+            L.shg_get_inkernel_omega.restype = i32
+            L.shg_inkernel_omega_fallbacks.argtypes = []
+            L.shg_inkernel_omega_fallbacks.restype = ctypes.c_uint64
             L.shg_set_a_mcast.argtypes = [i32]
             L.shg_set_a_mcast.restype = i32
             L.shg_last_error.restype = ctypes.c_char_p
@@ -150,9 +154,20 @@ def _dist(d) -> int:
     return DISTS[d] if isinstance(d, str) else int(d)
 
 
-def set_inkernel_omega(on: bool) -> None:
-    """project(): generate Omega inside the projection kernel (C ABI shg_set_inkernel_omega)."""
-    lib().shg_set_inkernel_omega(1 if on else 0)
+def set_inkernel_omega(on) -> None:
+    """project(): generate Omega inside the projection kernel (C ABI shg_set_inkernel_omega; on by
+    default). on = 2 is the tests' mode in which every tile comes from the stagers' fallback."""
+    lib().shg_set_inkernel_omega(2 if on == 2 else (1 if on else 0))
+
+
+def get_inkernel_omega() -> int:
+    """The current in-kernel Omega setting (0 off, 1 on, 2 fallback-only test mode)."""
+    return int(lib().shg_get_inkernel_omega())
+
+
+def inkernel_omega_fallbacks() -> int:
+    """Omega k-tiles generated so far by the stagers' generate-on-timeout fallback (test support)."""
+    return int(lib().shg_inkernel_omega_fallbacks())
 
 
 def set_a_mcast(npa: int) -> int:

@@ -230,6 +230,7 @@ struct OmGen {
     int64_t row0;           // spec row of local row 0 (multiple of 4)
     uint32_t* flags;        // ceil(k/64) zero-initialised ready flags
 };
+int omgen_mode();           // shg_set_inkernel_omega's setting (below)
 
 // Stream-K is chosen automatically only on the HBM side of the roofline (BN <= kSkAutoMaxBn), where
 // a partly idle last wave of whole tiles cannot keep HBM busy: measured interleaved under the 1000 W
@@ -579,7 +580,7 @@ shg_status_t run_shgemm(int64_t m, int64_t n, int64_t k, const AView& av, const 
             static_cast<int64_t>(pl.m_tiles) * pl.splits > pl.grid)
             return finish(SHG_ERR_INVALID_VALUE);
         SHG_CUDA(cudaMemsetAsync(og->flags, 0, static_cast<size_t>(pl.num_kb) * 4, stream));
-        kp.om_gen = 1;
+        kp.om_gen = omgen_mode() == 2 ? 2 : 1;
         kp.om_dist = og->dist;
         kp.om_stream = og->stream_id;
         kp.om_thr = og->thr;
@@ -620,19 +621,22 @@ shg_status_t run_shgemm(int64_t m, int64_t n, int64_t k, const AView& av, const 
     return finish(SHG_OK);
 }
 
-// In-kernel Omega generation for project(): off by default — measured slower
-// than the separate generator on cfg3 (1.00 / 0.94 / 0.83 ms vs 0.86 / 0.84 / 0.85 per mode,
-// DESIGN.md §9); switched on per process by shg_set_inkernel_omega(1) or SHG_OMGEN=1.
+// In-kernel Omega generation for project(): ON by default since round 2 — with
+// dedicated generator warps, the packed-f32x2 generator and the stager's generate-on-timeout fallback
+// it is faster than the separate generator launch on cfg3 and does not depend on
+// co-residency; shg_set_inkernel_omega(0) or SHG_OMGEN=0 selects the separate generator.
+// 2 = tests only: the generator warps stay idle, every tile comes from the stagers' fallback.
 std::atomic<int> g_omgen{-1};
-bool omgen_enabled() {
+int omgen_mode() {
     int v = g_omgen.load(std::memory_order_relaxed);
     if (v < 0) {
         const char* e = std::getenv("SHG_OMGEN");
-        v = (e && e[0] == '1') ? 1 : 0;
+        v = (e && e[0] == '0') ? 0 : 1;
         g_omgen.store(v, std::memory_order_relaxed);
     }
-    return v == 1;
+    return v;
 }
+bool omgen_enabled() { return omgen_mode() != 0; }
 
 uint32_t sparse_threshold(int dist, int64_t k_total) {
     if (dist == SHG_DIST_SPARSE3) return 715827882u;
@@ -1003,10 +1007,12 @@ shg_status_t project_impl(const float* A, int ndim, const int64_t* dims, int mod
                (plain_view || av.S % 32 == 0);
     shg_tune_t tt{};
     tt.tc = tc;
-    // Optionally (shg_set_inkernel_omega) Omega is generated INSIDE the projection kernel when every
-    // tile of the plan is resident at once (one tile per CTA) and the tiles are single CTAs of
-    // BN <= 192: the m_tiles CTAs that share a k range each generate 1/m_tiles of its Omega tiles
-    // with their epilogue warps (no separate gen_omega launch, no Omega traffic before the GEMM)
+    // By default (shg_set_inkernel_omega) Omega is generated INSIDE the projection kernel when every
+    // tile of the plan fits the grid at once (one tile per CTA) and the tiles are single CTAs of
+    // BN <= 128: the m_tiles CTAs that share a k range each generate 1/m_tiles of its Omega tiles
+    // with their generator warps (no separate gen_omega launch, no Omega traffic before the GEMM);
+    // a stager whose tile is late generates it itself (acquire_or_generate), so residency is a
+    // performance condition, not a correctness one
     bool om_gen = false;
     if (om_tiled && tc == SHG_TC_FP16 && omega_row0 % 4 == 0 && omgen_enabled()) {
         const Plan pl = make_plan(M, n, K, true, &tt, std::max(1, dev_info().sms), false, false, false);
@@ -1252,7 +1258,8 @@ int shg_device_supported(void) {
     return dev_info().ok ? 1 : 0;
 }
 
-void shg_set_inkernel_omega(int on) { g_omgen.store(on ? 1 : 0, std::memory_order_relaxed); }
+void shg_set_inkernel_omega(int on) { g_omgen.store(on == 2 ? 2 : (on ? 1 : 0), std::memory_order_relaxed); }
+int shg_get_inkernel_omega(void) { return omgen_mode(); }
 
 int shg_set_a_mcast(int npa) {
     if (npa != 0 && npa != 1 && npa != 2 && npa != 4) return -1;

@@ -387,13 +387,23 @@ extern "C" shg_status_t shg_probe_mma_energy(int n, int parts, int iters, long l
 namespace shg {
 __global__ void probe_boxmuller_kernel(const uint32_t* __restrict__ words, int64_t count, float* __restrict__ r,
                                        float* __restrict__ c, float* __restrict__ s) {
-    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < count; i += int64_t(gridDim.x) * blockDim.x) {
-        const uint32_t w = words[i];
-        float cv, sv;
-        omega::bm_angle(w, cv, sv);
-        r[i] = omega::bm_radius(w);
-        c[i] = cv;
-        s[i] = sv;
+    // words 2t and 2t + 1 go through the two lanes of the generator's packed radius / angle (an odd
+    // last word is paired with itself)
+    const int64_t npair = (count + 1) / 2;
+    for (int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; t < npair; t += int64_t(gridDim.x) * blockDim.x) {
+        const int64_t i0 = 2 * t, i1 = (2 * t + 1 < count) ? 2 * t + 1 : 2 * t;
+        const uint32_t w0 = words[i0], w1 = words[i1];
+        float2 cv, sv;
+        omega::bm_angle2(w0, w1, cv, sv);
+        const float2 rv = omega::bm_radius2(w0, w1);
+        r[i0] = rv.x;
+        c[i0] = cv.x;
+        s[i0] = sv.x;
+        if (i1 != i0) {
+            r[i1] = rv.y;
+            c[i1] = cv.y;
+            s[i1] = sv.y;
+        }
     }
 }
 }  // namespace shg

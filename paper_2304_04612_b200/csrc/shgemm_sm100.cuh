@@ -80,7 +80,10 @@ struct KParams {
     // generator warps (20..27) of the CTA (m_blk, s) generate the k-tiles t of split s with
     // (t - first tile of s) % m_tiles == m_blk into om_buf (k-tiled layout) and release flag[t];
     // the Omega stager acquires flag[t] before its TMA. Every tile is generated once, by one of the
-    // m_tiles CTAs that read it.
+    // m_tiles CTAs that read it — or, if that CTA has not published it within kOmGenHelpNs (it may
+    // not be resident yet), by the waiting stager itself (same bits), so no CTA's progress depends
+    // on another CTA being resident. om_gen = 2 (tests): the generator warps stay idle and every
+    // tile takes that fallback.
     int32_t om_gen;
     int32_t om_dist;
     uint32_t om_stream, om_thr;
@@ -439,11 +442,11 @@ __device__ __forceinline__ void gen_bar() { asm volatile("bar.sync 2, 256;" ::: 
 
 // 64-k tile t of the k-tiled Omega (rows 64t..64t+63 of this operand, all n columns) by the 256
 // generator threads (tid 0..255): OMEGA_SPEC blocks q = om_q0 + 16t + ql; rows >= k written as 0.
-__device__ __forceinline__ void gen_omega_tile(const KParams& p, int64_t t, int tid) {
+__device__ __forceinline__ void gen_omega_tile(const KParams& p, int64_t t, int tid, int nthr = 256) {
     const omega::Keys keys = omega::philox_keys(p.om_seed);
     uint16_t* tile = p.om_buf + t * p.n * 64;
     const int nb = 16 * static_cast<int>(p.n);
-    for (int b = tid; b < nb; b += 256) {
+    for (int b = tid; b < nb; b += nthr) {
         const int ql = b & 15;
         const int64_t j = b >> 4;
         const int64_t r0 = t * 64 + 4 * ql;
@@ -469,14 +472,38 @@ __device__ __forceinline__ void release_flag(uint32_t* f) {
     asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(f), "r"(1u) : "memory");
 }
 
-// wait until flag f is set (bounded: a lost flag traps instead of hanging), then order the
-// following async-proxy (TMA) reads after the acquire
-__device__ __forceinline__ void acquire_flag(const uint32_t* f) {
-    uint32_t v, spins = 0;
-    for (;;) {
+__device__ __forceinline__ uint64_t globaltimer_ns() {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
+// The Omega stager's wait for k-tile t (one thread). Normally the tile's generator CTA publishes it
+// within microseconds; if the flag is still clear after kOmGenHelpNs, that CTA may not be resident
+// (another kernel holds its SM, e.g. a second in-kernel-Omega projection on another stream whose
+// stagers wait in turn), so this thread generates the tile itself — the same bits, written to the
+// same place (a concurrent write by the generator CTA stores identical values) — and publishes it.
+// No CTA then waits on another being scheduled: the kernel completes whatever else runs.
+constexpr uint64_t kOmGenHelpNs = 200000;
+static __device__ unsigned long long g_om_helped;   // tiles generated by the fallback (tests read it)
+__device__ __forceinline__ void acquire_or_generate(const KParams& p, int64_t t) {
+    const uint32_t* f = p.om_flags + t;
+    uint64_t t0 = 0;
+    for (uint32_t spins = 0;; ++spins) {
+        uint32_t v;
         asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(f) : "memory");
         if (v != 0) break;
-        if (++spins == (1u << 26)) asm volatile("trap;");
+        if ((spins & 63u) == 0) {
+            const uint64_t now = globaltimer_ns();
+            if (t0 == 0) {
+                t0 = now;
+            } else if (now - t0 > kOmGenHelpNs) {
+                gen_omega_tile(p, t, 0, 1);           // ends with fence.proxy.async.global
+                release_flag(p.om_flags + t);
+                atomicAdd(&g_om_helped, 1ull);
+                break;
+            }
+        }
     }
     asm volatile("fence.proxy.async.global;" ::: "memory");
 }
@@ -904,13 +931,16 @@ shgemm_sm100_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_const
         Piece wk;
         for (int it = 0; next_piece<NPA>(p, unit, units, sr, it, wk, pr); ++it) {
             const int64_t kb0s = wk.kb0;
-            for (int64_t t = kb0s + wk.m_blk; t < kb0s + wk.nkb; t += p.m_tiles) {
+            for (int64_t t = kb0s + wk.m_blk; t < kb0s + wk.nkb && p.om_gen == 1; t += p.m_tiles) {
                 gen_omega_tile(p, t, gtid);
                 gen_bar();
                 if (gtid == 0) release_flag(p.om_flags + t);
             }
         }
     } else {
+        // (one count for the four control warps: ptxas allocates the code after a setmaxnreg for the
+        // count it sees there, so warp-dependent counts before shared code would over-allocate the
+        // warps given fewer; the Omega stager's rare fallback generation spills instead)
         asm volatile("setmaxnreg.dec.sync.aligned.u32 32;");
         if (warp == kWarpProdA) {
             // ======================================================== A stager (TMA, FP32, own rows)
@@ -1016,7 +1046,7 @@ shgemm_sm100_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_const
                         if (!skip) {
                             for (int t = 0; t < nst; ++t) {
                                 const int kcoord = (p.dbg & 16u) ? 0 : (wk.kb0 + (kb + t)) * kBK;
-                                if constexpr (OMGEN) acquire_flag(p.om_flags + kcoord / kBK);   // generated in-kernel
+                                if constexpr (OMGEN) acquire_or_generate(p, kcoord / kBK);   // generated in-kernel
                                 // FP16: one 128-B box row = 64 k; TF32: two k-halves of 32 k
 #pragma unroll
                                 for (int hh = 0; hh < (TF32 ? 2 : 1); ++hh) {

@@ -25,3 +25,10 @@ shg_status_t dispatch_tc_f16_gen(int bn, bool mmajor, const CUtensorMap& a, cons
 }
 
 }  // namespace shg_api
+
+// test support: number of Omega tiles the stagers' fallback has generated in this process
+extern "C" uint64_t shg_inkernel_omega_fallbacks(void) {
+    unsigned long long v = 0;
+    if (cudaMemcpyFromSymbol(&v, shg::g_om_helped, sizeof(v)) != cudaSuccess) return ~0ull;
+    return v;
+}

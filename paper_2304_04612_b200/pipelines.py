@@ -201,9 +201,10 @@ def _tc_view(dims, mode) -> bool:
 
 
 def rp_hosvd(T: torch.Tensor, ranks, seed: int = 0, dist="gaussian", projection="shgemm", timing=False,
-             gemm: str = "sgemm", factor: str = "cusolver", check: bool = True):
+             gemm: str = "sgemm", factor: str = "cusolver", check: bool = True, pregen: bool = True):
     """Alg 2: for each mode W = A'_(i) Omega_(i) (project, stream_id = mode), Q_i = QR(W);
-    g = A x_1 Q_1^T ... x_N Q_N^T. factor='gram': CholeskyQR2 for the QRs."""
+    g = A x_1 Q_1^T ... x_N Q_N^T. factor='gram': CholeskyQR2 for the QRs. pregen=False: each
+    project() generates its Omega_(i) itself (in-kernel by default) instead of the side stream."""
     if gemm not in ("sgemm", "tcec") or factor not in ("cusolver", "gram"):
         raise ValueError((gemm, factor))
     t = _Timer(timing)
@@ -213,7 +214,7 @@ def rp_hosvd(T: torch.Tensor, ranks, seed: int = 0, dist="gaussian", projection=
     if projection == "shgemm":   # one persistent scratch buffer (Omega_(i) + split-K partials) for all modes
         nbytes = max(project_workspace_size(list(T.shape), i, J) for i, J in enumerate(ranks))
         ws = torch.empty(nbytes, dtype=torch.uint8, device=T.device)
-        if T.is_contiguous() and T.data_ptr() % 16 == 0:
+        if pregen and T.is_contiguous() and T.data_ptr() % 16 == 0:
             # every Omega_(i) generated up front on a side stream (k-tiled, as project() streams it):
             # the generator (ALU-bound) fills the gaps of the latency-bound QRs between projections
             side = torch.cuda.Stream(device=T.device)
@@ -258,7 +259,7 @@ def rp_hosvd(T: torch.Tensor, ranks, seed: int = 0, dist="gaussian", projection=
                 g = mode_product(g, Q, i)
         t.mark("end")
     if check and bads and int(sum(bads)) != 0:
-        return rp_hosvd(T, ranks, seed, dist, projection, timing, gemm, "cusolver")
+        return rp_hosvd(T, ranks, seed, dist, projection, timing, gemm, "cusolver", pregen=pregen)
     # check=False (CUDA-graph capture: no synchronisation allowed): the caller checks "bad"
     return {"core": g, "Q": Qs, "times_ms": t.result(), "bad": sum(bads) if bads else None}
 

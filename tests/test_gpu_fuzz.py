@@ -110,11 +110,12 @@ def test_fuzz_project(shg, orc, i):
     dist = int(r.integers(0, 4))
     inkernel = bool(r.integers(0, 2))
     T = r.standard_normal(dims).astype(np.float32)
+    prev = shg.get_inkernel_omega()
     shg.set_inkernel_omega(inkernel)
     try:
         W = to_np(shg.project(torch.from_numpy(T).cuda(), mode, n, seed=i, dist=dist))
     finally:
-        shg.set_inkernel_omega(False)
+        shg.set_inkernel_omega(prev)
     Ai = np.ascontiguousarray(opl.unfold(T, mode))
     K = Ai.shape[1]
     ob = orc.omega_f16(K, n, seed=i, dist=dist, stream_id=mode)

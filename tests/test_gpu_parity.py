@@ -585,32 +585,69 @@ def test_row_shards_concatenate_to_unsharded_bitwise(shg, G):
     assert len(crcs) == 1
 
 
+@pytest.mark.parametrize("gen_mode", [1, 2])
 @pytest.mark.parametrize("dims,mode,n", [((512, 64, 128), 0, 64), ((512, 64, 128), 1, 48), ((512, 64, 128), 2, 32),
                                          ((300, 40, 100), 0, 64), ((96, 2048, 8), 1, 16)])
-def test_project_inkernel_omega_bit_exact(shg, orc, dims, mode, n):
-    """project() generates Omega_(mode) inside the mainloop (epilogue warps, flags per 64-k tile)
+def test_project_inkernel_omega_bit_exact(shg, orc, dims, mode, n, gen_mode):
+    """project() generates Omega_(mode) inside the mainloop (generator warps, flags per 64-k tile)
     when the plan allows it: the Omega it leaves in the caller's workspace is bit-identical to
-    gen_omega_f16_tiled (and the oracle), and W meets the bars."""
+    gen_omega_f16_tiled (and the oracle), and W meets the bars. gen_mode 2: the generator warps stay
+    idle, so every tile comes from the Omega stagers' generate-on-timeout fallback."""
     from oracle import pipelines as opl
     T = synth.gaussian(int(np.prod(dims)), 1, seed=13).reshape(dims)
     Tc = cuda(T)
     ws = torch.zeros(shg.project_workspace_size(list(dims), mode, n), dtype=torch.uint8, device="cuda")
-    shg.set_inkernel_omega(True)
+    prev = shg.get_inkernel_omega()
+    shg.set_inkernel_omega(gen_mode)
     try:
+        helped = shg.inkernel_omega_fallbacks()
         launches = shg.launch_count()
         W = shg.project(Tc, mode, n, seed=4, workspace=ws)
         torch.cuda.synchronize()
         K = int(np.prod(dims)) // dims[mode]
         expect = 1 + (1 if shg.plan(dims[mode], n, K)["split_k"] > 1 else 0)
         assert shg.launch_count() - launches == expect      # mainloop (+ split-K reduce): no gen_omega launch
+        if gen_mode == 2:   # every k-tile came from a stager's fallback (several CTAs may each make one)
+            assert shg.inkernel_omega_fallbacks() - helped >= (K + 63) // 64
     finally:
-        shg.set_inkernel_omega(False)
+        shg.set_inkernel_omega(prev)
     nb = n * ((K + 63) // 64) * 64
     om_ws = to_np(ws[:2 * nb]).view(np.uint16)
     om_ref = to_np(shg.gen_omega_tiled(K, n, seed=4, stream_id=mode)).view(np.uint16)
     np.testing.assert_array_equal(om_ws, om_ref)
     Ai = np.ascontiguousarray(opl.unfold(T, mode))
     check_bars(orc, Ai, orc.omega_f16(K, n, seed=4, stream_id=mode), to_np(W))
+
+
+def test_project_inkernel_omega_concurrent_streams(shg):
+    """Four in-kernel-Omega projections on four streams at once, each of whose plans fills the grid:
+    their CTAs cannot all be resident together, so stagers wait on generator CTAs that are not
+    scheduled and take the generate-on-timeout fallback. Every W equals the sequential result bit
+    for bit (no deadlock, no watchdog trap)."""
+    prev = shg.get_inkernel_omega()
+    shg.set_inkernel_omega(True)
+    try:
+        dims, n = (1024, 1024, 512), 64     # 2 GiB each: one call outlasts the 200-us fallback timeout
+        Ts = [torch.randn(*dims, device="cuda", generator=torch.Generator(device="cuda").manual_seed(i))
+              for i in range(4)]
+        ref = [shg.project(T, 0, n, seed=i) for i, T in enumerate(Ts)]
+        torch.cuda.synchronize()
+        helped = shg.inkernel_omega_fallbacks()
+        streams = [torch.cuda.Stream() for _ in Ts]
+        outs = [torch.empty_like(r) for r in ref]
+        wss = [torch.empty(shg.project_workspace_size(list(dims), 0, n), dtype=torch.uint8, device="cuda")
+               for _ in Ts]
+        for rep in range(3):
+            torch.cuda.synchronize()
+            for i, (T, st) in enumerate(zip(Ts, streams)):
+                with torch.cuda.stream(st):
+                    shg.project(T, 0, n, seed=i, out=outs[i], workspace=wss[i])
+            torch.cuda.synchronize()
+            for o, r in zip(outs, ref):
+                assert torch.equal(o, r)
+        print("fallback tiles in the concurrent calls:", shg.inkernel_omega_fallbacks() - helped)
+    finally:
+        shg.set_inkernel_omega(prev)
 
 
 def test_project_inkernel_omega_equals_separate_generation(shg, tmp_path):
