@@ -32,12 +32,11 @@ T = shg.synth("gauss", 1, 0x102, 1024, 1024 * 1024).view(1024, 1024, 1024)
 ws = torch.empty(max(shg.project_workspace_size([1024] * 3, md, 64) for md in range(3)), dtype=torch.uint8,
                  device="cuda")
 W = torch.empty(1024, 64, device="cuda")
-for gen in (False, True):
-    shg.set_inkernel_omega(gen)
+for gen, tag in ((0, "separate"), (1, "inkernel"), (3, "inkernel_warp")):
+    shg.lib().shg_set_inkernel_omega(gen)
     for mode in range(3):
-        out[f"project_mode{mode}_{'inkernel' if gen else 'separate'}_ms"] = t_ms(
-            lambda: shg.project(T, mode, 64, workspace=ws, out=W), reps=10)
-shg.set_inkernel_omega(False)
+        out[f"project_mode{mode}_{tag}_ms"] = t_ms(lambda: shg.project(T, mode, 64, workspace=ws, out=W), reps=10)
+shg.lib().shg_set_inkernel_omega(0)
 print(json.dumps(out))
 '''
 
