@@ -599,6 +599,13 @@ def main():
             except Exception as exc:  # noqa: BLE001
                 extras = {"error": repr(exc)[:300]}
                 torch.cuda.empty_cache()
+            ceil = (extras or {}).get("cublas_fp16_two_products_cfg4_bytes")
+            if ceil and gemm_ms > 0:
+                # context beside frac (DESIGN §5 "power-cap ceiling"): the same run's cuBLAS fp16 doing
+                # SHGEMM's two products on its A bytes; shgemm time / that time is the share of the
+                # power-capped ceiling the kernel reaches
+                roof["power_cap_ceiling_ms"] = ceil["ms"]
+                roof["frac_of_power_cap_ceiling"] = ceil["ms"] / gemm_ms
         cpu = None
         if not args.no_cpu_baseline and world == 1:
             cpu = cpu_baseline(m_total, k, n)
