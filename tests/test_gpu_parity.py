@@ -609,6 +609,8 @@ def test_project_inkernel_omega_bit_exact(shg, orc, dims, mode, n, gen_mode):
         assert shg.launch_count() - launches == expect      # mainloop (+ split-K reduce): no gen_omega launch
         if gen_mode == 2:   # every k-tile came from a stager's fallback (several CTAs may each make one)
             assert shg.inkernel_omega_fallbacks() - helped >= (K + 63) // 64
+        else:               # one kernel alone, every CTA resident: the generator warps made every tile
+            assert shg.inkernel_omega_fallbacks() == helped
     finally:
         shg.set_inkernel_omega(prev)
     nb = n * ((K + 63) // 64) * 64
