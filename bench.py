@@ -793,6 +793,17 @@ def measure_extras(shg, torch, hbm, tc16_burst, tc_ratio, reps=10):
         ms = med_ms(fn)
         out[name] = dict(roof(m, k, n, ms, iso_ms(fn)), m=m, k=k, n=n, step="gen_omega_f16 + shgemm",
                          a_mcast=shg.plan(m, n, k)["a_mcast"])
+        if name in ("cfg2_projection", "cfg5_n256", "cfg5_n1024", "cfg5_n4096"):
+            # the power-capped ceiling of the method's own tensor work on this shape (as for cfg4):
+            # cuBLAS fp16 doing both products, [A_hi | A_lo] (m x 2k) . [Omega; Omega] (2k x n)
+            A2 = torch.randn(m, 2 * k, device="cuda", dtype=torch.float16)
+            B2 = torch.randn(2 * k, n, device="cuda", dtype=torch.float16)
+            C2 = torch.empty(m, n, device="cuda", dtype=torch.float16)
+            cms = med_ms(lambda: torch.matmul(A2, B2, out=C2))
+            out[name]["power_cap_ceiling_ms"] = cms
+            out[name]["frac_of_power_cap_ceiling"] = cms / ms
+            del A2, B2, C2
+            torch.cuda.empty_cache()
         if out[name]["a_mcast"] > 1 and n <= 1024:
             # the same step with A multicast off (per-pair A loads; DESIGN.md §5 "A read once")
             fn_off = lambda: (shg.gen_omega(k, n, seed=OMEGA_SEED, out=Om), shg.shgemm(A, Om, out=Y, tune={"a_mcast": 1}))
