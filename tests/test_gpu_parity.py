@@ -425,14 +425,21 @@ def test_config3_project_full_size_sampled(shg, orc):
     """BASELINE config 3's projections at full size: a 1024^3 FP32 tensor (4 GiB), W = A_(i) Omega_(i)
     with n = 64 and K = 2^20 for every mode (mode 0 K-major, mode 1 a 3-D slab view, mode 2 M-major in
     place), in bench.py's launch configuration; 16 sampled rows of each W against the oracle with the
-    oracle's own Omega_(i) (stream_id = mode)."""
+    oracle's own Omega_(i) (stream_id = mode). project()'s default generates Omega_(i) inside the
+    projection kernel; the same call with the separate generator gives W bit for bit."""
     I = 1024
     T = shg.synth("gauss", 3, 0x103, I, I * I).view(I, I, I)
     rng = np.random.default_rng(3)
     rows = np.unique(np.concatenate([[0, 127, 128, I - 1], rng.integers(0, I, 12)]))
     ridx = torch.from_numpy(rows).cuda()
+    prev = shg.get_inkernel_omega()
     for mode in range(3):
+        shg.set_inkernel_omega(True)
         W = shg.project(T, mode, 64, seed=0)
+        shg.set_inkernel_omega(False)
+        W_sep = shg.project(T, mode, 64, seed=0)
+        shg.set_inkernel_omega(prev)
+        assert torch.equal(W, W_sep)
         U = to_np(torch.movedim(T, mode, 0)[ridx].reshape(len(rows), -1))
         ob = orc.omega_f16(I * I, 64, seed=0, stream_id=mode)
         check_bars(orc, U, ob, to_np(W[ridx]))
