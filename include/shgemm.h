@@ -266,7 +266,9 @@ shg_status_t shgemm_tiled(int64_t m, int64_t n, int64_t k, const float *A, int64
 
 /* ---------------------------------------------------------------------------------------------
  * project — W[I_mode x n] = A'_(mode) . Omega_(mode) (Alg 2 line 2). With an aligned A
- * view, Omega_(mode) is generated in the k-tiled layout (gen_omega_f16_tiled).
+ * view, Omega_(mode) is generated in the k-tiled layout (gen_omega_f16_tiled) — by default inside
+ * the projection kernel when the plan has one tile per CTA (shg_set_inkernel_omega), else by a
+ * separate gen_omega launch; the bits of Omega and W are the same either way.
  *   A        device, C-order tensor with ndim dims (1 <= ndim <= 8), dims[i] >= 1.
  *   mode     0 <= mode < ndim. The unfolding's column index is the C-order linear index over the
  *            remaining modes in ascending order (== torch.movedim(A, mode, 0).reshape(I_mode, -1)).
