@@ -20,6 +20,9 @@ for mode in range(3):
     shg.project(T, mode, 16)
 shg.set_inkernel_omega(True)
 shg.project(T, 0, 16)
+shg.set_inkernel_omega(2)      # generator warps idle: every Omega tile from the stagers' fallback
+shg.project(T, 0, 16)
+shg.project(T, 1, 16)
 shg.set_inkernel_omega(False)
 # later paths: pairs, wide 288, k-tiled Omega, project slab views
 # with S % 32 == 0 (second half of a stage continues in the next slab), row-sharded Omega, probes
