@@ -133,9 +133,10 @@ class ClockSampler:
                 "power_w": statistics.median(pw) if pw else None}
 
 
-def cpu_baseline(m, k, n, budget_s=10.0):
+def cpu_baseline(m, k, n, budget_s=30.0):
     """The oracle as it stands (naive FP32 GEMM, sequential fmaf over k, OpenMP over rows) on a
-    bounded row sample of the same workload; rate scaled to TFLOP/s."""
+    bounded row sample of the same workload (grown until one timed sample takes ~8-10 s of CPU
+    work); rate scaled to TFLOP/s."""
     import numpy as np
     import oracle
     om = oracle.omega_f16(k, n, seed=OMEGA_SEED)
