@@ -452,14 +452,13 @@ __device__ __forceinline__ void gen_omega_tile(const KParams& p, int64_t t, int 
         const int64_t r0 = t * 64 + 4 * ql;
         uint2 v = make_uint2(0u, 0u);
         if (r0 < p.k) {
-            uint16_t o[4];
-            omega::omega4(keys, p.om_stream, p.om_dist, p.om_thr, static_cast<uint64_t>(p.om_q0 + t * 16 + ql),
-                          static_cast<uint32_t>(j), o);
-#pragma unroll
-            for (int u = 1; u < 4; ++u)
-                if (r0 + u >= p.k) o[u] = 0;
-            v.x = static_cast<uint32_t>(o[0]) | (static_cast<uint32_t>(o[1]) << 16);
-            v.y = static_cast<uint32_t>(o[2]) | (static_cast<uint32_t>(o[3]) << 16);
+            v = omega::omega4p(keys, p.om_stream, p.om_dist, p.om_thr, static_cast<uint64_t>(p.om_q0 + t * 16 + ql),
+                               static_cast<uint32_t>(j));
+            if (r0 + 3 >= p.k) {          // rows >= k of the last tile are +0
+                if (r0 + 1 >= p.k) v.x &= 0xFFFFu;
+                if (r0 + 2 >= p.k) v.y = 0u;
+                else v.y &= 0xFFFFu;
+            }
         }
         *reinterpret_cast<uint2*>(tile + j * 64 + 4 * ql) = v;
     }
